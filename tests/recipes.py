@@ -1,0 +1,104 @@
+"""Seeded test-input recipes shared by the golden generator and the tests.
+
+They reproduce, draw for draw, the input factories of the reference test
+suite -- conftest.random_forest (pkg/tests/conftest.py:21-82),
+conftest.random_micro_instance (:85-98) and test_kernels.make_inputs
+(pkg/tests/test_kernels.py:16-33) -- so the golden outputs recorded from
+the reference apply to inputs regenerated here (or on the GPU box)
+without storing the tensors.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2505_17694_b200.workloads import Spec
+
+PAC_SHAPES = [
+    # (n, n_q, h_q, h_kv, d)
+    (1, 1, 1, 1, 4),
+    (7, 3, 2, 1, 16),
+    (33, 5, 4, 2, 64),
+    (2049, 2, 4, 4, 32),
+    (512, 8, 8, 2, 128),
+]
+
+
+def random_forest_spec(seed, *, max_depth=6, max_arity=5, max_len=64, max_bs=16, with_masks=False):
+    rng = np.random.default_rng(seed)
+    d = int(rng.choice([4, 16, 64]))
+    g = int(rng.choice([1, 2, 4]))
+    h_kv = int(rng.integers(1, 3))
+    h_q = h_kv * g
+    scale = 1.0 / math.sqrt(d)
+    depth = int(rng.integers(1, max_depth + 1))
+    spec = Spec(h_q, h_kv, d)
+
+    def grow(parent):
+        n = int(rng.integers(1, max_len + 1))
+        k = rng.standard_normal((n, h_kv, d)) * scale
+        v = rng.standard_normal((n, h_kv, d)) * scale
+        spec.parent.append(parent)
+        spec.length.append(n)
+        spec.keys.append(k)
+        spec.values.append(v)
+        return spec.n_nodes - 1
+
+    frontier = [grow(0)]
+    for _ in range(depth - 1):
+        nxt = []
+        for nid in frontier:
+            for _ in range(int(rng.integers(0, max_arity + 1))):
+                nxt.append(grow(nid))
+        if not nxt:
+            break
+        frontier = nxt
+
+    inner = set(spec.parent[1:])
+    leaves = [nid for nid in range(1, spec.n_nodes) if nid not in inner]
+    bs = int(rng.integers(1, min(max_bs, len(leaves)) + 1))
+    chosen = sorted(rng.choice(len(leaves), size=bs, replace=False).tolist())
+    for i in chosen:
+        chain = []
+        cur = leaves[i]
+        while cur:
+            chain.append(cur)
+            cur = spec.parent[cur]
+        spec.paths.append(tuple(reversed(chain)))
+
+    spec.visible = [None] * spec.n_nodes
+    if with_masks:
+        for rid, path in enumerate(spec.paths):
+            for nid in path:
+                ln = spec.length[nid]
+                if ln > 1 and rng.random() < 0.25:
+                    if spec.visible[nid] is None:
+                        spec.visible[nid] = {}
+                    spec.visible[nid][rid] = int(rng.integers(1, ln + 1))
+    spec.queries = rng.standard_normal((bs, h_q, d)) * scale
+    return spec
+
+
+def random_micro_tasks(seed):
+    """(tasks, m) of conftest.random_micro_instance; tasks as
+    (node, n_q, n) tuples."""
+    gen = np.random.default_rng(seed)
+    t = int(gen.integers(1, 5))
+    m = int(gen.integers(1, 5))
+    tasks = []
+    for j in range(t):
+        n_q = int(gen.integers(1, 9))
+        n = int(gen.integers(1, 20001))
+        tasks.append((j + 1, n_q, n))
+    return tasks, m
+
+
+def pac_inputs(shape, dtype=np.float64, seed=7, masked=False):
+    n, n_q, h_q, h_kv, d = shape
+    rng = np.random.default_rng(seed)
+    q = (rng.standard_normal((n_q, h_q, d)) / math.sqrt(d)).astype(dtype)
+    k = (rng.standard_normal((n, h_kv, d)) / math.sqrt(d)).astype(dtype)
+    v = rng.standard_normal((n, h_kv, d)).astype(dtype)
+    vis = rng.integers(1, n + 1, size=n_q) if masked else None
+    return q, k, v, vis
