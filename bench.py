@@ -1,0 +1,336 @@
+"""Decode-attention benchmark (BASELINE.json metric) for the B200 path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--no-cpu-baseline]
+
+Workload (config[1] of BASELINE.json): Llama-3-8B shape, 32 q / 8 kv
+heads, d=128, bf16 KV; 256 requests share a 32K-token system prompt, each
+with a private 512-token suffix. Synthetic N(0,1)/sqrt(d) data generated
+on the device (K/V pool 671 MB > 126 MB L2, so every step streams from
+HBM). A "step" = one decode-attention call over all 256 requests.
+
+value = effective unique-KV GB/s over the whole job (all ranks); with N
+GPUs the kv heads are split N ways (tensor-parallel head split) and the
+per-rank outputs are all-gathered over NCCL inside the timed step.
+`e2e` times the same step through the public API with queries copied from
+pinned host memory and the output read back every step.
+
+--impl reference times the reference's CPU algorithm (the oracle port
+under oracle/, numpy, all host threads) on one kv head of the same
+workload per step (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode-attn µs/step & effective KV GB/s (unique bytes) vs HBM roofline, 1-8 GPU"
+CONFIGS = {
+    "cfg2": dict(shared_len=32768, leaf_len=512, batch=256, h_q=32, h_kv=8, d=128,
+                 label="cfg2: Llama-3-8B shape (32 q / 8 kv heads, d128, bf16 KV), 256 requests sharing a "
+                       "32K system prompt + 512-token suffixes"),
+    "cfg5": dict(shared_len=65536, leaf_len=512, batch=1024, h_q=64, h_kv=8, d=128,
+                 label="cfg5: Llama-3-70B shape (64 q / 8 kv heads, d128, bf16 KV), 1024 requests sharing a "
+                       "64K prefix + 512-token suffixes"),
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.path = Path("/tmp") / f"bench_clocks_{os.getpid()}.csv"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_reference_sample(cfg, head=0, workers=None, seed=0):
+    """One kv head of the workload through the oracle port of the reference
+    executor (numpy, host threads): returns (seconds, unique KV bytes of
+    the sample at bf16 width, description)."""
+    from oracle import attention as OA
+    from oracle import plan as OP
+    from oracle import index as OI
+    from paper_2505_17694_b200 import workloads as W
+
+    workers = workers or os.cpu_count()
+    spec = W.two_level(cfg["shared_len"], cfg["leaf_len"], cfg["batch"], h_q=cfg["h_q"] // cfg["h_kv"], h_kv=1,
+                       d=cfg["d"], seed=seed, dtype=np.float32)
+    z = np.zeros((0, 1, cfg["d"]), np.float32)
+    fd = OA.ForestData(spec.parent, [z] + spec.keys[1:], [z] + spec.values[1:], spec.paths)
+    grid = OP.parse_profile((ROOT / "paper_2505_17694_b200" / "profiles" / "b200_d128.csv").read_text())
+    qs = OI.query_sets(spec.paths, spec.n_nodes)
+    plan = OP.divide_and_schedule(OP.node_tasks(qs, spec.length), grid, workers, limit=10000)
+    subs = [(s[1], s[2], s[3]) for s in plan.subtasks]
+    t0 = time.perf_counter()
+    OA.execute(fd, spec.queries, subs, workers=workers)
+    dt = time.perf_counter() - t0
+    kv_bytes = sum(spec.length[1:]) * 1 * cfg["d"] * 2 * 2
+    desc = (f"1 of {cfg['h_kv']} kv heads ({cfg['h_q'] // cfg['h_kv']} q heads), all {cfg['batch']} requests, "
+            f"full {cfg['shared_len']}-token root + suffixes; fp32 numpy oracle port of prefixdec.execute, "
+            f"{workers} threads, plan of {len(subs)} subtasks")
+    return dt, kv_bytes, desc
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    workers = os.cpu_count()
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, workers=workers)
+    times = []
+    for _ in range(args.steps):
+        dt, kv_bytes, desc = cpu_reference_sample(cfg, workers=workers)
+        times.append(dt)
+    t = statistics.mean(times)
+    value = kv_bytes / t / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["label"], "sample": "one kv head per step"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": workers, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--blocks", type=int, default=0, help="planner m (0: SMs // local kv heads)")
+    ap.add_argument("--quick", action="store_true", help="profiling run: no e2e / clocks / cpu baseline")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_17694_b200 as P
+    from paper_2505_17694_b200 import workloads as W
+    from paper_2505_17694_b200.executor import DecodeStep
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    h_kv, h_q, d = cfg["h_kv"], cfg["h_q"], cfg["d"]
+    assert h_kv % world == 0, "kv heads must split evenly across ranks"
+    h_local = h_kv // world
+    h0 = rank * h_local
+    g = h_q // h_kv
+
+    # structure + device-resident synthetic KV pool (heads [h0, h0 + h_local))
+    spec = W.two_level(cfg["shared_len"], cfg["leaf_len"], cfg["batch"], h_q=h_q, h_kv=h_kv, d=d, tensors=False)
+    forest = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, h_kv, d)
+    T = forest.total_tokens
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + h0)
+    sc = 1.0 / math.sqrt(d)
+    kp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
+    vp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
+    hq_local = h_local * g
+    q_host = (torch.randn((cfg["batch"], hq_local, d), generator=torch.Generator().manual_seed(99 + rank)) * sc
+              ).to(torch.bfloat16).pin_memory()
+    q_dev = q_host.to(dev)
+
+    # plan: device tasks (<= 128 query-head rows each) on the B200 profile
+    table = P.load_default_profile()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    m = args.blocks or max(1, sms // h_local)
+    t0 = time.perf_counter()
+    plan = P.divide_and_schedule(P.device_tasks(forest, g), table, m)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    step = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
+                      flags=args.flags)
+    out = torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32, device=dev)
+    gathered = torch.empty((world, cfg["batch"], hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def one_step(qd):
+        step(qd, kp, vp, out=out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+        return out
+
+    work = P.device_work(forest, h_q, element_size=2, head_fraction=h_local / h_kv)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(n, fn):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / n
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(max(args.warmup, 3)):
+        one_step(q_dev)
+    torch.cuda.synchronize(dev)
+    clocks = None if args.quick else ClockSampler(local_rank)
+    ms = timed(args.steps, lambda: one_step(q_dev))
+    clock_rec = clocks.stop() if clocks else None
+
+    # per-kernel phases (same work, launched alone) for the roofline
+    phases = {}
+    info = step.info
+    for name, fl, present in (("tc", 8 | 32 | 64, info.n_tc_groups), ("gemv", 8 | 16 | 64, info.n_gemv_groups),
+                              ("merge", 8 | 16 | 32, info.n_merge)):
+        if not present:
+            continue
+        ph = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
+                        flags=args.flags | fl)
+        for _ in range(3):
+            ph(q_dev, kp, vp, out=out)
+        phases[name] = timed(max(5, args.steps // 2), lambda: ph(q_dev, kp, vp, out=out))
+
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+    total_bytes = work["unique_kv_bytes"] * world
+    value = total_bytes / (ms * 1e-3) / 1e9
+    # bytes / flops attributed to each kernel
+    tc_rows = sum(n.len for n in forest.nodes[1:] if len(n.query_set) * g >= 16)
+    kv_tc = tc_rows * h_local * d * 2 * 2
+    kernels = {}
+    if "tc" in phases:
+        fl = sum(n.len * len(n.query_set) for n in forest.nodes[1:] if len(n.query_set) * g >= 16) * hq_local * 4 * d
+        kernels["tc"] = {"bound": "tensor", "achieved": fl / (phases["tc"] * 1e-3) / 1e12, "peak": tf_burst,
+                         "unit": "TFLOP/s", "ms": phases["tc"], "algorithmic_flops": fl, "kv_bytes": kv_tc}
+        kernels["tc"]["frac"] = kernels["tc"]["achieved"] / tf_burst
+    if "gemv" in phases:
+        kb = work["unique_kv_bytes"] - kv_tc
+        kernels["gemv"] = {"bound": "hbm", "achieved": kb / (phases["gemv"] * 1e-3) / 1e9, "peak": hbm,
+                           "unit": "GB/s", "ms": phases["gemv"], "algorithmic_bytes": kb}
+        kernels["gemv"]["frac"] = kernels["gemv"]["achieved"] / hbm
+    if "merge" in phases:
+        kernels["merge"] = {"ms": phases["merge"]}
+    dominant = max((k for k in kernels if "bound" in kernels[k]), key=lambda k: kernels[k]["ms"], default=None)
+    roof = None
+    if dominant:
+        k = kernels[dominant]
+        roof = {"bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"],
+                "frac": k["frac"], "traffic": None, "kernel": dominant, "peak_kind": peak_kind}
+
+    e2e = None
+    if not args.quick:
+        out_host = torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32).pin_memory()
+        qd2 = torch.empty_like(q_dev)
+
+        def e2e_step():
+            qd2.copy_(q_host, non_blocking=True)
+            one_step(qd2)
+            out_host.copy_(out, non_blocking=True)
+
+        for _ in range(3):
+            e2e_step()
+        e2e_ms = timed(args.steps, e2e_step)
+        e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": q_host.numel() * q_host.element_size(),
+               "d2h_bytes_per_step": out_host.numel() * out_host.element_size()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
+        dt, kvb, desc = cpu_reference_sample(cfg)
+        cpu = {"value": kvb / dt / 1e9, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": desc, "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
+            "config": {"workload": cfg["label"], "bs": cfg["batch"], "h_q": h_q, "h_kv": h_kv, "d": d,
+                       "shared_len": cfg["shared_len"], "suffix_len": cfg["leaf_len"],
+                       "parallelism": f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
+                       "planner": {"m": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,
+                                   "truncated": plan.search_truncated, "ms": plan_ms}},
+            "roofline": roof,
+            "hbm_roofline_step": {"achieved": value / world, "peak": hbm, "unit": "GB/s",
+                                  "frac": value / world / hbm, "frac_of_8tbs": value / world / 8000.0},
+            "kernels": kernels,
+            "work": work,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": step.launches * args.steps,
+            "clocks": clock_rec,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,245 @@
+/*
+ * codec_b200.h -- C ABI of the B200-native prefix-shared decode-attention
+ * path (CoDec, arXiv 2505.17694).
+ *
+ * Plain C types only: pointers, sizes, PODs. No torch / C++ types cross
+ * this boundary. Every function is reentrant (no global mutable state;
+ * the last-error string is thread-local) and every device entry point is
+ * asynchronous on the caller's stream (passed as `void*`, a cudaStream_t).
+ * Ownership: the caller owns every buffer; host-side handles
+ * (codec_index, codec_plan, codec_table) are created and freed here.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/prefixdec/<file>:<line>).  Status codes map
+ * 1:1 onto the reference's exception classes (errors.py:9-102); the
+ * Python host layer raises the same class with codec_last_error() as the
+ * message.
+ */
+#ifndef CODEC_B200_H
+#define CODEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CODEC_API __attribute__((visibility("default")))
+#else
+#define CODEC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+  CODEC_OK = 0,
+  CODEC_ERR_CYCLE_DETECTED = 1,          /* errors.CycleDetected          */
+  CODEC_ERR_DANGLING_PARENT = 2,         /* errors.DanglingParent         */
+  CODEC_ERR_PATH_NOT_PREFIX_CHAIN = 3,   /* errors.PathNotPrefixChain     */
+  CODEC_ERR_DIMENSION_MISMATCH = 4,      /* errors.DimensionMismatch      */
+  CODEC_ERR_UNKNOWN_REQUEST = 5,         /* errors.UnknownRequest         */
+  CODEC_ERR_UNKNOWN_NODE = 6,            /* errors.UnknownNode            */
+  CODEC_ERR_SHAPE_MISMATCH = 7,          /* errors.ShapeMismatch          */
+  CODEC_ERR_EMPTY_VISIBLE_SET = 8,       /* errors.EmptyVisibleSet        */
+  CODEC_ERR_NO_VISIBLE_TOKENS = 9,       /* errors.NoVisibleTokens        */
+  CODEC_ERR_PLAN_FOREST_MISMATCH = 10,   /* errors.PlanForestMismatch     */
+  CODEC_ERR_INCOMPLETE_PARTIALS = 11,    /* errors.IncompletePartials     */
+  CODEC_ERR_SEARCH_SPACE_OVERFLOW = 12,  /* errors.SearchSpaceOverflow    */
+  CODEC_ERR_VALUE = 20,                  /* builtin ValueError            */
+  CODEC_ERR_UNSUPPORTED = 30,            /* shape/dtype the kernels do not cover */
+  CODEC_ERR_CUDA = 31                    /* CUDA runtime/launch failure   */
+} codec_status;
+
+/* Message of the last non-OK status returned on this thread. */
+CODEC_API const char* codec_last_error(void);
+/* ABI version (bumped on any incompatible change). */
+CODEC_API int32_t codec_abi_version(void);
+
+/* element types of q / k / v / partials */
+typedef enum { CODEC_F32 = 0, CODEC_F64 = 1, CODEC_BF16 = 2 } codec_dtype;
+
+/* ======================================================================
+ * K0 -- forest indexing.  Replaces the index half of
+ *   build_forest()            forest.py:160-251
+ *   _preorder_offsets()       forest.py:148-157
+ * Inputs are the structural parts of the node specs and request paths;
+ * tensors stay with the caller. Raises the build_forest error classes
+ * with the reference's messages.
+ * ==================================================================== */
+typedef struct codec_index codec_index;
+
+CODEC_API int32_t codec_index_build(int32_t n_nodes,            /* incl. virtual root 0 */
+                          const int32_t* parent,      /* [n_nodes]; parent[0] ignored */
+                          const int64_t* length,      /* [n_nodes]; length[0] ignored (0) */
+                          int32_t bs,
+                          const int64_t* path_ptr,    /* [bs+1] CSR of request paths */
+                          const int32_t* path_idx,
+                          int64_t n_vis,              /* visible_len entries */
+                          const int32_t* vis_node,    /* [n_vis] */
+                          const int32_t* vis_req,     /* [n_vis] */
+                          const int64_t* vis_count,   /* [n_vis] */
+                          codec_index** out);
+CODEC_API void codec_index_free(codec_index* ix);
+
+typedef struct {
+  int32_t n_nodes, bs;
+  int64_t total_tokens;     /* sum of node lengths (pool tokens) */
+  int64_t qset_nnz;         /* sum |I_n| */
+  int64_t path_nnz;
+} codec_index_info;
+CODEC_API int32_t codec_index_info_get(const codec_index* ix, codec_index_info* info);
+/* Copy out: node_off[n_nodes] (preorder kappa, forest.py:148-157),
+ * qset_ptr[n_nodes+1], qset_idx[qset_nnz] (ascending I_n, forest.py:236-237),
+ * qset_vis[qset_nnz] (visible count of that request in that node,
+ * forest.py:128-132), children_ptr[n_nodes+1], children_idx[n_nodes-1]. Any
+ * pointer may be NULL. */
+CODEC_API int32_t codec_index_read(const codec_index* ix, int64_t* node_off, int64_t* qset_ptr,
+                         int32_t* qset_idx, int64_t* qset_vis, int64_t* children_ptr,
+                         int32_t* children_idx);
+
+/* ======================================================================
+ * K1 -- cost model, task division and schedule (host, float64, operation
+ * order identical to the reference => bit-exact plans).
+ * ==================================================================== */
+typedef struct {
+  int32_t n_nq, n_n;
+  const int64_t* nq_knots;   /* [n_nq] strictly ascending */
+  const int64_t* n_knots;    /* [n_n]  strictly ascending */
+  const double* cost_ms;     /* [n_n][n_nq] row-major      */
+} codec_cost_table;
+
+/* estimate()            cost_model.py:68-84 */
+CODEC_API double codec_estimate(const codec_cost_table* t, int64_t n_q, int64_t n);
+/* slice_ranges()/canonical_division()   scheduler.py:81-92.
+ * Writes up to `cap` (start, stop) pairs; *count gets the slice count. */
+CODEC_API int32_t codec_slice_ranges(int64_t n, int64_t b, int64_t* start_stop, int64_t cap, int64_t* count);
+/* lower_bound()         scheduler.py:106-131 */
+CODEC_API int32_t codec_lower_bound(const codec_cost_table* t, int32_t n_tasks, const int64_t* task_nq,
+                          const int64_t* task_n, int32_t m, double tol, double* cost_l);
+/* division_caps()       scheduler.py:134-139 */
+CODEC_API int32_t codec_division_caps(const codec_cost_table* t, int32_t n_tasks, const int64_t* task_nq,
+                            const int64_t* task_n, double cost_l, int64_t* caps);
+/* greedy_assign()       scheduler.py:142-155 */
+CODEC_API int32_t codec_greedy_assign(int64_t n, const double* costs, int32_t m, int32_t* block_of,
+                            double* loads);
+
+typedef struct codec_plan codec_plan;
+/* divide_and_schedule() scheduler.py:187-222. on_overflow: 0 = fallback,
+ * 1 = raise SearchSpaceOverflow. */
+CODEC_API int32_t codec_divide_and_schedule(const codec_cost_table* t, int32_t n_tasks,
+                                  const int64_t* task_node, const int64_t* task_nq,
+                                  const int64_t* task_n, int32_t m, int64_t search_limit,
+                                  int32_t on_overflow, codec_plan** out);
+/* plan_uniform_bk()     scheduler.py:225-233. cost_l: NaN means None. */
+CODEC_API int32_t codec_plan_uniform(const codec_cost_table* t, int32_t n_tasks, const int64_t* task_node,
+                           const int64_t* task_nq, const int64_t* task_n, int32_t m, int64_t bk,
+                           double cost_l, codec_plan** out);
+CODEC_API void codec_plan_free(codec_plan* p);
+
+typedef struct {
+  int32_t n_tasks, n_subtasks, blocks, truncated;
+  double makespan_ms, cost_l_ms;   /* cost_l NaN == None */
+} codec_plan_info;
+CODEC_API int32_t codec_plan_info_get(const codec_plan* p, codec_plan_info* info);
+/* DivisionPlan fields (scheduler.py:26-78); any pointer may be NULL. */
+CODEC_API int32_t codec_plan_read(const codec_plan* p, int64_t* b_k, int32_t* sub_task, int64_t* sub_node,
+                        int64_t* sub_start, int64_t* sub_stop, double* sub_cost,
+                        int32_t* block_of, double* loads);
+
+/* ======================================================================
+ * Device task table -- the plan expanded for the GPU.  Replaces the job
+ * construction of _split_phase() (executor.py:145-206: row filter :156,
+ * per-row visible :187-190) and the per-request unit lists of
+ * _reduce_one() (executor.py:209-231), validated like _plan_slices()
+ * (executor.py:120-142).
+ *
+ * Each plan task owns a contiguous chunk of its node's query set (a
+ * node-level plan, tasks_from_forest(), is the one-chunk case). Each
+ * subtask x row tile becomes one "group"; group x local kv head is one CTA.
+ * ==================================================================== */
+typedef struct {
+  int32_t bs, h_q, h_kv, d;
+  int32_t head_begin, head_end;   /* local kv-head shard [begin, end) */
+  int32_t kv_dtype;               /* codec_dtype of q, k, v */
+  int32_t flags;                  /* CODEC_FLAG_* */
+  int64_t pool_tokens;            /* T: token stride of one head in the pool */
+} codec_dims;
+
+#define CODEC_FLAG_NO_TC      1   /* never use the tcgen05 shared-node kernel */
+#define CODEC_FLAG_FORCE_TC   2   /* tcgen05 kernel for every eligible group */
+#define CODEC_FLAG_NO_GEMV    4   /* generic kernel instead of the GEMV kernel */
+/* launch-time phase selection (profiling: time one kernel of the step alone) */
+#define CODEC_FLAG_SKIP_GENERIC 8
+#define CODEC_FLAG_SKIP_TC      16
+#define CODEC_FLAG_SKIP_GEMV    32
+#define CODEC_FLAG_SKIP_MERGE   64
+
+typedef struct codec_table codec_table;
+CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
+                          const int64_t* task_node, const int64_t* task_nq, int32_t n_sub,
+                          const int32_t* sub_task, const int64_t* sub_start,
+                          const int64_t* sub_stop, const int32_t* sub_block,
+                          codec_table** out);
+CODEC_API void codec_table_free(codec_table* t);
+
+typedef struct {
+  int32_t n_tc_groups, n_gemv_groups, n_gen_groups;   /* per kernel */
+  int32_t n_rows, n_slots, n_merge;                    /* rows, partial slots, merged requests */
+  int32_t gemv_rows;                                   /* q-row capacity of a GEMV group */
+  int32_t off_tc, off_gemv, off_gen, off_rows;         /* int32 offsets into the blob */
+  int32_t off_merge_req, off_merge_ptr, off_merge_slot;
+  int32_t h_local;                                     /* head_end - head_begin */
+  int64_t blob_len;                                    /* int32 elements */
+  int64_t workspace_bytes;                             /* partial (o, m, l) storage */
+} codec_table_info;
+CODEC_API int32_t codec_table_info_get(const codec_table* t, codec_table_info* info);
+/* Copy the int32 blob to host memory (caller uploads it to the device). */
+CODEC_API int32_t codec_table_copy(const codec_table* t, int32_t* blob);
+
+/* ======================================================================
+ * The decode-attention step.  Replaces execute()  executor.py:296-308
+ * (split phase + barrier + per-request LSE reduction + finalize), with
+ * _kernels.pac_kernel (_kernels.pyx:16-54) as the per-tile math.
+ *
+ *   q      [bs][h_q_local][d]            (q dtype = kv_dtype)
+ *   k, v   [h_local][pool_tokens][d]     head-major node pool, nodes at
+ *                                        their preorder offsets (kappa)
+ *   out    [bs][h_q_local][d]            float32 for BF16/F32, float64 for F64
+ *   workspace  >= info.workspace_bytes, 256-byte aligned
+ * All device pointers; asynchronous on `stream`.
+ * ==================================================================== */
+CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
+                               const int32_t* table_dev, const void* q, const void* k,
+                               const void* v, void* out, void* workspace, void* stream);
+
+/* ======================================================================
+ * Device primitives with the reference's argument meaning.
+ * ==================================================================== */
+/* pac_kernel()  _kernels.pyx:16-54 / attention.py:88-117.
+ * q [n_q][h_q][d], k/v [n][h_kv][d] (token-major, the reference layout),
+ * visible int64 [n_q] (device, each in 1..n; NULL = all n), scale (the
+ * reference passes 1/sqrt(d)); out [n_q][h_q][d], max_score / exp_sum
+ * [n_q][h_q]: float32 for F32/BF16 inputs, float64 for F64. */
+CODEC_API int32_t codec_pac(int32_t dtype, const void* q, const void* k, const void* v,
+                  const int64_t* visible, int64_t n_q, int64_t h_q, int64_t n, int64_t h_kv,
+                  int64_t d, double scale, void* out, void* max_score, void* exp_sum,
+                  void* stream);
+/* por()  attention.py:131-153, elementwise part (the whole-side-empty
+ * identity is resolved by the host wrapper). a/b/result (out, m, s) with
+ * out [count][d], m/s [count]; dtype F32 or F64. */
+CODEC_API int32_t codec_por(int32_t dtype, int64_t count, int64_t d, const void* a_out, const void* a_m,
+                  const void* a_s, const void* b_out, const void* b_m, const void* b_s,
+                  void* r_out, void* r_m, void* r_s, void* stream);
+
+/* Pack token-major node tensors [len][h_kv][d] into the head-major pool
+ * [h_local][pool_tokens][d] at token offset `tok0` (heads
+ * [head_begin, head_begin + h_local)). Device pointers, same dtype. */
+CODEC_API int32_t codec_pool_pack(int32_t dtype, const void* src, int64_t len, int64_t h_kv, int64_t d,
+                        int32_t head_begin, int32_t h_local, void* pool, int64_t pool_tokens,
+                        int64_t tok0, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CODEC_B200_H */

@@ -1,0 +1,30 @@
+// Layout of the int32 task-table blob shared by host_table.cpp (writer)
+// and the kernels (readers). See codec_table_build in codec_b200.h.
+#pragma once
+
+#include <cstdint>
+
+namespace codec {
+
+// group kinds (which kernel runs the group)
+constexpr int kKindTc = 0;       // tcgen05 shared-node kernel (bf16, d = 128)
+constexpr int kKindGemv = 1;     // CUDA-core warp-shuffle GEMV kernel
+constexpr int kKindGeneric = 2;  // any dtype / head dim (small or odd shapes)
+
+// a group record: 8 int32
+constexpr int kGroupInts = 8;
+constexpr int kGrpKvTok = 0;    // pool token index of the slice start
+constexpr int kGrpLen = 1;      // slice length (tokens)
+constexpr int kGrpRowBegin = 2; // first row record
+constexpr int kGrpNRows = 3;    // number of requests in the group
+constexpr int kGrpSub = 4;      // plan subtask (diagnostics)
+constexpr int kGrpNode = 5;     // forest node (diagnostics)
+
+// a row record: 4 int32 -- request, visible tokens within the slice,
+// partial slot (>= 0) or -1 - request for a direct write of the output
+constexpr int kRowInts = 4;
+
+// minimum query-head rows for a subtask to take the tensor-core kernel
+constexpr int kTcMinRows = 16;
+
+}  // namespace codec

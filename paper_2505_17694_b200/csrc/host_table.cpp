@@ -1,0 +1,294 @@
+// Device task table: a DivisionPlan expanded into GPU work groups.
+//
+// Host C++ restatement of the job construction of the reference
+// executor: plan/forest agreement (_plan_slices, executor.py:120-142),
+// per-subtask row filter `visible_count(r) > start` (:156), per-row
+// visible clip `min(visible, stop) - start` (:187-190), and each
+// request's partial list in path-then-slice order (_reduce_one,
+// executor.py:211-224). The result is one int32 blob (uploaded once and
+// reused across decode steps) plus counts/offsets (codec_table_info).
+//
+// Group = (subtask, row tile). A row tile is up to 128/g requests for the
+// tcgen05 kernel (one M=128 tile of query-head rows) or one request for
+// the GEMV / generic kernels. CTA = group x local kv head.
+#include <algorithm>
+#include <array>
+#include <map>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "device_table.h"
+
+using codec::fail;
+using codec::fail_str;
+
+namespace codec {
+const std::vector<int64_t>& ix_node_off(const codec_index* ix);
+const std::vector<int64_t>& ix_length(const codec_index* ix);
+const std::vector<int64_t>& ix_qset_ptr(const codec_index* ix);
+const std::vector<int32_t>& ix_qset_idx(const codec_index* ix);
+const std::vector<int64_t>& ix_qset_vis(const codec_index* ix);
+const std::vector<int64_t>& ix_path_ptr(const codec_index* ix);
+const std::vector<int32_t>& ix_path_idx(const codec_index* ix);
+int32_t ix_bs(const codec_index* ix);
+int32_t ix_n_nodes(const codec_index* ix);
+int64_t ix_total_tokens(const codec_index* ix);
+}  // namespace codec
+
+struct codec_table {
+  codec_table_info info{};
+  std::vector<int32_t> blob;
+};
+
+namespace {
+
+std::string py_list(const std::vector<int64_t>& v) {
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < v.size(); ++i) os << (i ? ", " : "") << v[i];
+  os << "]";
+  return os.str();
+}
+
+std::string py_ranges(const std::vector<std::pair<int64_t, int64_t>>& v) {
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < v.size(); ++i) os << (i ? ", " : "") << "(" << v[i].first << ", " << v[i].second << ")";
+  os << "]";
+  return os.str();
+}
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+}  // namespace
+
+extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
+                                     const int64_t* task_node, const int64_t* task_nq, int32_t n_sub,
+                                     const int32_t* sub_task, const int64_t* sub_start,
+                                     const int64_t* sub_stop, const int32_t* sub_block, codec_table** out) {
+  using namespace codec;
+  if (!ix || !dims || !out) return fail(CODEC_ERR_VALUE, "NULL argument");
+  *out = nullptr;
+  const int32_t n_nodes = ix_n_nodes(ix), bs = ix_bs(ix);
+  const auto& len = ix_length(ix);
+  const auto& off = ix_node_off(ix);
+  const auto& qptr = ix_qset_ptr(ix);
+  const auto& qidx = ix_qset_idx(ix);
+  const auto& qvis = ix_qset_vis(ix);
+  const auto& pptr = ix_path_ptr(ix);
+  const auto& pidx = ix_path_idx(ix);
+  if (dims->bs != bs) return fail(CODEC_ERR_DIMENSION_MISMATCH, "%d queries for %d requests", dims->bs, bs);
+  if (dims->h_kv < 1 || dims->h_q % dims->h_kv != 0)
+    return fail(CODEC_ERR_DIMENSION_MISMATCH, "h_q=%d must be a positive multiple of h_kv=%d", dims->h_q, dims->h_kv);
+  if (dims->head_begin < 0 || dims->head_end > dims->h_kv || dims->head_begin >= dims->head_end)
+    return fail(CODEC_ERR_VALUE, "kv head shard [%d, %d) outside 0..%d", dims->head_begin, dims->head_end, dims->h_kv);
+  if (dims->pool_tokens < ix_total_tokens(ix))
+    return fail(CODEC_ERR_VALUE, "pool holds %lld tokens, forest needs %lld", (long long)dims->pool_tokens,
+                (long long)ix_total_tokens(ix));
+  if (dims->pool_tokens >= (int64_t(1) << 31)) return fail(CODEC_ERR_UNSUPPORTED, "pool larger than 2^31 tokens");
+  const int32_t g = dims->h_q / dims->h_kv;
+  const int32_t d = dims->d;
+  for (int32_t j = 0; j < n_tasks; ++j)
+    if (task_node[j] < 1 || task_node[j] >= n_nodes)
+      return fail(CODEC_ERR_PLAN_FOREST_MISMATCH, "plan task %d names node %lld outside the forest", j,
+                  (long long)task_node[j]);
+  for (int32_t s = 0; s < n_sub; ++s)
+    if (sub_task[s] < 0 || sub_task[s] >= n_tasks)
+      return fail(CODEC_ERR_PLAN_FOREST_MISMATCH, "subtask %d names task %d of %d", s, sub_task[s], n_tasks);
+
+  // ---- plan <-> forest agreement (executor.py:120-142)
+  std::set<int64_t> have, want;
+  for (int32_t s = 0; s < n_sub; ++s) have.insert(task_node[sub_task[s]]);
+  for (int32_t n = 1; n < n_nodes; ++n)
+    if (qptr[n + 1] > qptr[n]) want.insert(n);
+  if (have != want)
+    return fail_str(CODEC_ERR_PLAN_FOREST_MISMATCH,
+                    "plan covers nodes " + py_list({have.begin(), have.end()}) + ", forest needs " +
+                        py_list({want.begin(), want.end()}));
+  {
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> per_task(n_tasks);
+    for (int32_t s = 0; s < n_sub; ++s) per_task[sub_task[s]].push_back({sub_start[s], sub_stop[s]});
+    for (int32_t j = 0; j < n_tasks; ++j) {
+      auto& r = per_task[j];
+      std::sort(r.begin(), r.end());
+      int64_t pos = 0, nl = len[task_node[j]];
+      bool ok = !r.empty();
+      for (auto& p : r) {
+        if (p.first != pos || p.second <= p.first) ok = false;
+        pos = p.second;
+      }
+      if (pos != nl) ok = false;
+      if (!ok)
+        return fail_str(CODEC_ERR_PLAN_FOREST_MISMATCH, "node " + std::to_string(task_node[j]) + " slices " +
+                                                            py_ranges(r) + " do not tile 0.." + std::to_string(nl));
+    }
+  }
+  // ---- task -> query-set chunk: tasks of a node split I_n in order
+  std::vector<int64_t> chunk_lo(n_tasks), chunk_hi(n_tasks);
+  {
+    std::map<int64_t, std::vector<int32_t>> by_node;
+    for (int32_t j = 0; j < n_tasks; ++j) by_node[task_node[j]].push_back(j);
+    for (auto& kv : by_node) {
+      int64_t n = kv.first, size = qptr[n + 1] - qptr[n], tot = 0;
+      for (int32_t j : kv.second) tot += task_nq[j];
+      int64_t hm = size > 0 ? tot / size : 0;
+      bool ok = size > 0 && hm >= 1 && hm * size == tot;
+      int64_t cur = 0;
+      for (int32_t j : kv.second) {
+        if (!ok || task_nq[j] % hm != 0) {
+          ok = false;
+          break;
+        }
+        chunk_lo[j] = cur;
+        cur += task_nq[j] / hm;
+        chunk_hi[j] = cur;
+      }
+      if (!ok || cur != size)
+        return fail(CODEC_ERR_PLAN_FOREST_MISMATCH, "tasks of node %lld do not partition its query set",
+                    (long long)n);
+    }
+  }
+
+  // ---- kernel eligibility
+  const bool tc_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && is_pow2(g) && g <= 128 &&
+                     !(dims->flags & CODEC_FLAG_NO_TC);
+  const bool gemv_ok = (dims->kv_dtype == CODEC_BF16 || dims->kv_dtype == CODEC_F32) &&
+                       (d == 64 || d == 128 || d == 256) && g <= 16 && !(dims->flags & CODEC_FLAG_NO_GEMV);
+  const int32_t tc_reqs = tc_ok ? 128 / g : 0;
+  const int32_t gemv_rows = g <= 4 ? 4 : (g <= 8 ? 8 : 16);
+
+  // ---- rows and slots
+  struct Grp {
+    int32_t kind, kv_tok, len, row_begin, n_rows, sub, node;
+    int64_t order_len;
+  };
+  std::vector<Grp> groups;
+  std::vector<int32_t> rows;  // 4 per row: req, vis_local, slot, pad
+  // per request: (path position, subtask, row index)
+  std::vector<std::vector<std::array<int64_t, 3>>> req_units(bs);
+  std::vector<std::vector<int32_t>> node_pathpos(bs);
+  auto path_pos = [&](int32_t r, int64_t n) -> int64_t {
+    for (int64_t i = pptr[r]; i < pptr[r + 1]; ++i)
+      if (pidx[i] == n) return i - pptr[r];
+    return -1;
+  };
+  for (int32_t s = 0; s < n_sub; ++s) {
+    int32_t j = sub_task[s];
+    int64_t n = task_node[j], start = sub_start[s], stop = sub_stop[s];
+    std::vector<std::pair<int32_t, int32_t>> live;  // (req, vis_local)
+    for (int64_t q = qptr[n] + chunk_lo[j]; q < qptr[n] + chunk_hi[j]; ++q) {
+      int64_t vis = qvis[q];
+      if (vis > start) live.push_back({qidx[q], (int32_t)(std::min(vis, stop) - start)});
+    }
+    if (live.empty()) continue;
+    int kind;
+    int32_t per;
+    if (tc_ok && ((int64_t)live.size() * g >= kTcMinRows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
+      kind = kKindTc;
+      per = tc_reqs;
+    } else if (gemv_ok) {
+      kind = kKindGemv;
+      per = 1;
+    } else {
+      kind = kKindGeneric;
+      per = 1;
+    }
+    for (size_t a = 0; a < live.size(); a += per) {
+      size_t b = std::min(live.size(), a + per);
+      Grp gr{kind, (int32_t)(off[n] + start), (int32_t)(stop - start), (int32_t)(rows.size() / 4),
+             (int32_t)(b - a), s, (int32_t)n, stop - start};
+      for (size_t i = a; i < b; ++i) {
+        int32_t r = live[i].first;
+        int64_t pp = path_pos(r, n);
+        if (pp < 0)
+          return fail(CODEC_ERR_INCOMPLETE_PARTIALS, "request %d not on a path through node %lld", r, (long long)n);
+        req_units[r].push_back({pp, (int64_t)s, (int64_t)(rows.size() / 4)});
+        rows.push_back(r);
+        rows.push_back(live[i].second);
+        rows.push_back(-1);
+        rows.push_back(0);
+      }
+      groups.push_back(gr);
+    }
+  }
+  // ---- slots: direct output for single-partial requests, else merged
+  std::vector<int32_t> merge_req, merge_ptr{0}, merge_slot;
+  int32_t n_slots = 0;
+  for (int32_t r = 0; r < bs; ++r) {
+    auto& u = req_units[r];
+    if (u.empty()) return fail(CODEC_ERR_NO_VISIBLE_TOKENS, "request %d has no visible tokens anywhere on its path", r);
+    std::sort(u.begin(), u.end());  // path-then-slice order
+    if (u.size() == 1) {
+      rows[4 * u[0][2] + 2] = -1 - r;
+      continue;
+    }
+    merge_req.push_back(r);
+    for (auto& e : u) {
+      rows[4 * e[2] + 2] = n_slots;
+      merge_slot.push_back(n_slots++);
+    }
+    merge_ptr.push_back((int32_t)merge_slot.size());
+  }
+  // ---- group order: TC, GEMV, generic; longest slices first within a kind
+  std::stable_sort(groups.begin(), groups.end(), [](const Grp& a, const Grp& b) {
+    if (a.kind != b.kind) return a.kind < b.kind;
+    return a.order_len > b.order_len;
+  });
+  (void)sub_block;
+
+  auto t = new codec_table();
+  codec_table_info& in = t->info;
+  in.h_local = dims->head_end - dims->head_begin;
+  in.gemv_rows = gemv_rows;
+  std::vector<int32_t>& blob = t->blob;
+  auto emit_groups = [&](int kind, int32_t& count, int32_t& offset) {
+    offset = (int32_t)blob.size();
+    count = 0;
+    for (auto& gr : groups)
+      if (gr.kind == kind) {
+        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.sub, gr.node, 0, 0};
+        blob.insert(blob.end(), rec, rec + kGroupInts);
+        ++count;
+      }
+  };
+  emit_groups(kKindTc, in.n_tc_groups, in.off_tc);
+  emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
+  emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
+  in.off_rows = (int32_t)blob.size();
+  in.n_rows = (int32_t)(rows.size() / 4);
+  blob.insert(blob.end(), rows.begin(), rows.end());
+  in.n_merge = (int32_t)merge_req.size();
+  in.off_merge_req = (int32_t)blob.size();
+  blob.insert(blob.end(), merge_req.begin(), merge_req.end());
+  in.off_merge_ptr = (int32_t)blob.size();
+  blob.insert(blob.end(), merge_ptr.begin(), merge_ptr.end());
+  in.off_merge_slot = (int32_t)blob.size();
+  blob.insert(blob.end(), merge_slot.begin(), merge_slot.end());
+  while (blob.size() % 4) blob.push_back(0);
+  in.blob_len = (int64_t)blob.size();
+  in.n_slots = n_slots;
+  const int64_t elem = dims->kv_dtype == CODEC_F64 ? 8 : 4;
+  const int64_t hq_local = (int64_t)in.h_local * g;
+  int64_t o_bytes = (int64_t)n_slots * hq_local * d * elem;
+  o_bytes = (o_bytes + 255) / 256 * 256;
+  in.workspace_bytes = o_bytes + (int64_t)n_slots * hq_local * 2 * elem + 256;
+  *out = t;
+  return CODEC_OK;
+}
+
+extern "C" void codec_table_free(codec_table* t) { delete t; }
+
+extern "C" int32_t codec_table_info_get(const codec_table* t, codec_table_info* info) {
+  if (!t || !info) return codec::fail(CODEC_ERR_VALUE, "NULL argument");
+  *info = t->info;
+  return CODEC_OK;
+}
+
+extern "C" int32_t codec_table_copy(const codec_table* t, int32_t* blob) {
+  if (!t || !blob) return codec::fail(CODEC_ERR_VALUE, "NULL argument");
+  std::copy(t->blob.begin(), t->blob.end(), blob);
+  return CODEC_OK;
+}

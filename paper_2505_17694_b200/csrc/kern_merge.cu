@@ -1,0 +1,83 @@
+// K4: per-request log-sum-exp merge of split partials.
+//
+// Replaces reduce_tree()/_reduce_one() + por() + finalize()
+// (executor.py:209-293, attention.py:131-161). For each request with two
+// or more partials (its path-then-slice list from the task table) and
+// each local query head:
+//     M = max_p m_p,  L = sum_p s_p e^(m_p - M),
+//     out = sum_p out_p s_p e^(m_p - M) / L
+// which equals the reference's balanced pairwise por() fold up to
+// rounding (the merge is associative/commutative in exact arithmetic,
+// test_attention.py:160-180) but takes one pass over the partials.
+// One warp per (request, query head); lanes cover the head dim.
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "device_table.h"
+#include "device_util.cuh"
+
+namespace codec {
+
+template <typename A, int DPL>
+__global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
+                                                    int off_slot, int n_merge, int hq_local, int d,
+                                                    const A* __restrict__ part_o, const A* __restrict__ part_ml,
+                                                    A* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x;
+  const int qh = blockIdx.y * 4 + warp;
+  if (i >= n_merge || qh >= hq_local) return;
+  const int req = table[off_req + i];
+  const int p0 = table[off_ptr + i], p1 = table[off_ptr + i + 1];
+  const int32_t* slots = table + off_slot;
+  A M = neg_inf<A>();
+  for (int p = p0; p < p1; ++p) {
+    const int64_t e = (int64_t)slots[p] * hq_local + qh;
+    if (part_ml[2 * e + 1] > 0) M = max(M, part_ml[2 * e]);
+  }
+  A acc[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) acc[j] = 0;
+  A L = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int64_t e = (int64_t)slots[p] * hq_local + qh;
+    const A s = part_ml[2 * e + 1];
+    if (!(s > 0)) continue;
+    const A w = s * exp_acc(part_ml[2 * e] - M);
+    L += w;
+    const A* po = part_o + e * d;
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+      const int x = lane + 32 * j;
+      if (x < d) acc[j] += w * po[x];
+    }
+  }
+  A* dst = out + ((int64_t)req * hq_local + qh) * d;
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) {
+    const int x = lane + 32 * j;
+    if (x < d) dst[x] = acc[j] / L;
+  }
+}
+
+int32_t cuda_status(cudaError_t e, const char* what);
+
+int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
+                     const void* part_o, const void* part_ml, void* out, cudaStream_t st) {
+  if (in.n_merge == 0) return CODEC_OK;
+  dim3 grid(in.n_merge, (hq_local + 3) / 4);
+#define CODEC_MERGE(A, DPL)                                                                                    \
+  merge_kernel<A, DPL><<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot,     \
+                                             in.n_merge, hq_local, d, (const A*)part_o, (const A*)part_ml,      \
+                                             (A*)out)
+  if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
+  if (dtype == CODEC_F64) {
+    if (d <= 128) CODEC_MERGE(double, 4); else CODEC_MERGE(double, 16);
+  } else {
+    if (d <= 128) CODEC_MERGE(float, 4); else CODEC_MERGE(float, 16);
+  }
+#undef CODEC_MERGE
+  return cuda_status(cudaGetLastError(), "merge launch");
+}
+
+}  // namespace codec

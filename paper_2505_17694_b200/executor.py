@@ -1,0 +1,148 @@
+"""The decode-attention step on the B200 (reference-compatible `execute`).
+
+`execute(forest, queries, plan, pool)` keeps the signature and error
+behaviour of prefixdec/executor.py:296-308 and returns [bs, h_q, d]. The
+reference runs the plan's subtasks on a host thread pool, barriers, and
+folds each request's partials with por(); here the plan is expanded once
+into a device task table (C++ codec_table_build: the row filter, the
+per-row visible clip and the path-then-slice partial lists of
+executor.py:145-231) and one call of codec_decode_attention runs
+    tcgen05 shared-node kernel | GEMV suffix kernel | generic kernel
+    -> LSE merge kernel
+on the current CUDA stream.
+
+`DecodeStep` is the prepared form (table + workspace uploaded once) that
+serving code reuses across decode steps until the next re-plan
+(DEFAULT_REPLAN_EVERY in scheduler.py), and that bench.py times.
+`BlockPool` is accepted for API compatibility: the GPU's CTAs are the
+blocks. `reduce_mode` "balanced" and "sequential" both map to the single
+pass max-then-sum merge (same result up to rounding, test_attention.py:
+160-180). The reference's simulated EventTrace is out of scope (CUDA
+events and ncu replace simulated time).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .attention import torch_dtype
+from .errors import DimensionMismatch
+from .forest import Forest, QueryBatch, dtype_code
+
+FLAG_NO_TC = 1
+FLAG_FORCE_TC = 2
+FLAG_NO_GEMV = 4
+
+
+@dataclass
+class BlockPool:
+    """API shim for prefixdec.executor.BlockPool (executor.py:35-44)."""
+
+    worker_count: int = 1
+    deterministic: bool = True
+
+    def __post_init__(self):
+        if self.worker_count < 1:
+            raise ValueError(f"worker_count must be >= 1, got {self.worker_count}")
+
+
+def _plan_arrays(plan):
+    tasks = plan.tasks
+    t_node = np.ascontiguousarray([t.node for t in tasks], dtype=np.int64)
+    t_nq = np.ascontiguousarray([t.n_q for t in tasks], dtype=np.int64)
+    s_task = np.ascontiguousarray([s.task_index for s in plan.subtasks], dtype=np.int32)
+    s_start = np.ascontiguousarray([s.start for s in plan.subtasks], dtype=np.int64)
+    s_stop = np.ascontiguousarray([s.stop for s in plan.subtasks], dtype=np.int64)
+    s_block = np.ascontiguousarray(plan.assignment.block_of, dtype=np.int32)
+    return t_node, t_nq, s_task, s_start, s_stop, s_block
+
+
+class DecodeStep:
+    """A plan expanded into a device task table for one forest, dtype and
+    kv-head shard. Call with device queries [bs, h_q_local, d] and the
+    head-major pools; returns [bs, h_q_local, d] (float32, or float64 for
+    float64 inputs)."""
+
+    def __init__(self, forest: Forest, plan, h_q: int, dtype="bfloat16", head_begin=0, head_end=None,
+                 device="cuda", flags=0):
+        import torch
+
+        self.forest = forest
+        self.h_q, self.h_kv, self.d = int(h_q), forest.h_kv, forest.d
+        self.head_begin = int(head_begin)
+        self.head_end = forest.h_kv if head_end is None else int(head_end)
+        self.g = self.h_q // self.h_kv
+        self.tdtype = torch_dtype(dtype)
+        self.device = torch.device(device)
+        self.dims = _lib.Dims(forest.bs, self.h_q, self.h_kv, self.d, self.head_begin, self.head_end,
+                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1))
+        t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
+        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        L = _lib.lib()
+        h = C.c_void_p()
+        _lib.check(L.codec_table_build(forest._index, C.byref(self.dims), len(t_node), P(t_node, C.c_int64),
+                                       P(t_nq, C.c_int64), len(s_task), P(s_task, C.c_int32),
+                                       P(s_start, C.c_int64), P(s_stop, C.c_int64), P(s_block, C.c_int32),
+                                       C.byref(h)))
+        try:
+            self.info = _lib.TableInfo()
+            _lib.check(L.codec_table_info_get(h, C.byref(self.info)))
+            blob = np.zeros(max(self.info.blob_len, 4), dtype=np.int32)
+            _lib.check(L.codec_table_copy(h, P(blob, C.c_int32)))
+        finally:
+            L.codec_table_free(h)
+        self.blob_host = blob
+        self.table = torch.from_numpy(blob).to(self.device)
+        self.workspace = torch.empty(max(int(self.info.workspace_bytes), 256), dtype=torch.uint8, device=self.device)
+        self.out_dtype = torch.float64 if self.tdtype == torch.float64 else torch.float32
+        self.hq_local = (self.head_end - self.head_begin) * self.g
+
+    @property
+    def launches(self) -> int:
+        """Kernels one call launches (for the bench's gpu_launches)."""
+        i = self.info
+        return int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) + int(bool(i.n_merge))
+
+    def __call__(self, q, k_pool, v_pool, out=None, stream=None):
+        import torch
+
+        if out is None:
+            out = torch.empty((self.forest.bs, self.hq_local, self.d), dtype=self.out_dtype, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().codec_decode_attention(
+            C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
+            C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(out.data_ptr()),
+            C.c_void_p(self.workspace.data_ptr()), C.c_void_p(st.cuda_stream)))
+        return out
+
+
+def execute(forest: Forest, queries: QueryBatch, plan, pool: BlockPool | None = None, trace=None,
+            reduce_mode: str = "balanced", flags: int = 0):
+    """Full decode-attention step (executor.py:296-308) on the GPU.
+    Returns a torch CUDA tensor [bs, h_q, d]."""
+    import torch
+
+    if queries.bs != forest.bs:
+        raise DimensionMismatch(f"{queries.bs} queries for {forest.bs} requests")
+    if queries.d != forest.d or queries.h_kv != forest.h_kv:
+        raise DimensionMismatch(
+            f"queries d={queries.d} h_kv={queries.h_kv} vs forest d={forest.d} h_kv={forest.h_kv}")
+    if reduce_mode not in ("balanced", "sequential"):
+        raise ValueError(f"mode must be balanced or sequential, got {reduce_mode!r}")
+    q = queries.queries
+    qdt = str(q.dtype).replace("torch.", "")
+    tdt = torch_dtype(qdt if qdt in ("float32", "float64", "bfloat16") else "float64")
+    key = ("step", id(plan), str(tdt), flags)
+    cache = forest._pools.setdefault("_steps", {})
+    step = cache.get(key)
+    if step is None or step[0] is not plan:
+        step = (plan, DecodeStep(forest, plan, queries.h_q, tdt, flags=flags))
+        cache[key] = step
+    step = step[1]
+    kp, vp = forest.device_pool(tdt)
+    qd = (q if isinstance(q, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(q)))
+    qd = qd.to(device=step.device, dtype=tdt).contiguous()
+    return step(qd, kp, vp)

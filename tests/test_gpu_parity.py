@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the golden vectors recorded from the reference. Needs a B200."""
+from __future__ import annotations
+
+import io
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_json, golden_npz, golden_table_text, rel_err
+from recipes import PAC_SHAPES, pac_inputs, random_forest_spec
+from oracle import attention as OA
+import paper_2505_17694_b200 as P
+from paper_2505_17694_b200 import workloads as W
+from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_TC, DecodeStep
+
+pytestmark = pytest.mark.gpu
+
+BF16_ABS, BF16_REL = 2e-3, 1e-2   # north-star tolerance for bf16 KV (BASELINE.json)
+
+
+@pytest.fixture(scope="module")
+def table():
+    return P.load_profile(io.StringIO(golden_table_text("a100_d128.csv")))
+
+
+def np_(t):
+    return t.detach().double().cpu().numpy()
+
+
+def oracle_forest(spec):
+    z = np.zeros((0, spec.h_kv, spec.d))
+    return OA.ForestData(spec.parent, [z] + [np.asarray(k, np.float64) for k in spec.keys[1:]],
+                         [z] + [np.asarray(v, np.float64) for v in spec.values[1:]], spec.paths, spec.visible)
+
+
+def build(spec, dtype=None):
+    specs = spec.node_specs()
+    q = spec.queries
+    if dtype is not None:
+        import torch
+        tdt = {"bfloat16": torch.bfloat16, "float32": torch.float32}[dtype]
+        specs = [(p, torch.from_numpy(np.ascontiguousarray(k)).to(tdt), torch.from_numpy(np.ascontiguousarray(v)).to(tdt), vis)
+                 for p, k, v, vis in specs]
+        q = torch.from_numpy(np.ascontiguousarray(q)).to(tdt)
+    qb = P.QueryBatch(q, spec.h_kv)
+    return P.build_forest(specs, spec.paths, qb), qb
+
+
+def upcast_spec(spec, dtype="bfloat16"):
+    """The spec's tensors rounded to `dtype` and back to float64: the
+    oracle then sees exactly the values the GPU sees."""
+    import torch
+    tdt = {"bfloat16": torch.bfloat16, "float32": torch.float32}[dtype]
+    r = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(tdt).double().numpy()
+    out = W.Spec(spec.h_q, spec.h_kv, spec.d, list(spec.parent), list(spec.length),
+                 [None] + [r(k) for k in spec.keys[1:]], [None] + [r(v) for v in spec.values[1:]],
+                 list(spec.paths), r(spec.queries), spec.visible)
+    return out
+
+
+def assert_bf16_close(out, ref):
+    out, ref = np.asarray(out, np.float64), np.asarray(ref, np.float64)
+    assert np.isfinite(out).all()
+    err = float(np.max(np.abs(out - ref)))
+    assert err <= BF16_ABS, err
+    assert rel_err(out, ref) <= BF16_REL, rel_err(out, ref)
+
+
+# ----------------------------------------------------------------- pac / por
+class TestPacGolden:
+    def test_known_answers(self, cuda_ok):
+        a = lambda *x: np.asarray(x, np.float64).reshape(-1, 1, 1)
+        p = P.pac(a(2.0), a(3.0), a(7.0))
+        assert (np_(p.out).item(), np_(p.max_score).item(), np_(p.exp_sum).item()) == (7.0, 6.0, 1.0)
+        p = P.pac(a(1.0), a(0.0, 0.0), a(2.0, 4.0))
+        assert np_(p.out).item() == pytest.approx(3.0, abs=1e-15)
+        p = P.pac(a(2.0), a(3.0, 5.0), a(7.0, 11.0))
+        assert np_(p.out).item() == pytest.approx(10.928055160152, rel=1e-12)
+        assert np_(p.max_score).item() == 10.0
+        assert np_(p.exp_sum).item() == pytest.approx(1.0183156388887, rel=1e-12)
+        d = 16
+        p = P.pac(np.ones((1, 1, d)), np.ones((1, 1, d)), np.ones((1, 1, d)))
+        assert np_(p.max_score).item() == pytest.approx(4.0, rel=1e-15)
+
+    def test_extreme_scores(self, cuda_ok):
+        a = lambda *x: np.asarray(x, np.float64).reshape(-1, 1, 1)
+        p = P.pac(np.ones((1, 1, 1)), a(500.0, -500.0, 250.0, -250.0, 0.0), a(1.0, 2.0, 3.0, 4.0, 5.0))
+        assert np.isfinite(np_(p.out)).all() and np_(p.out).item() == pytest.approx(1.0, rel=1e-8)
+        lo = P.pac(np.ones((1, 1, 1)), a(-500.0), a(2.0))
+        hi = P.pac(np.ones((1, 1, 1)), a(500.0), a(3.0))
+        m = P.por(lo, hi)
+        assert np_(m.out).item() == pytest.approx(3.0, rel=1e-12) and np_(m.max_score).item() == 500.0
+
+    @pytest.mark.parametrize("i", range(len(PAC_SHAPES)))
+    @pytest.mark.parametrize("masked", [False, True])
+    def test_float64_goldens(self, cuda_ok, i, masked):
+        z = golden_npz()
+        q, k, v, vis = pac_inputs(PAC_SHAPES[i], masked=masked)
+        p = P.pac(q, k, v, visible=vis)
+        tag = f"{i}_{int(masked)}"
+        assert rel_err(np_(p.out), z[f"pac_out_{tag}"]) <= 1e-12
+        assert rel_err(np_(p.max_score), z[f"pac_m_{tag}"]) <= 1e-12
+        assert rel_err(np_(p.exp_sum), z[f"pac_s_{tag}"]) <= 1e-12
+
+    @pytest.mark.parametrize("i", [1, 2, 4])
+    def test_float32(self, cuda_ok, i):
+        z = golden_npz()
+        q, k, v, vis = pac_inputs(PAC_SHAPES[i], dtype=np.float32, masked=True)
+        p = P.pac(q, k, v, visible=vis)
+        assert rel_err(np_(p.out), z[f"pac_out_{i}_1"]) <= 1e-4
+
+    def test_gqa_equals_expanded(self, cuda_ok):
+        rng = np.random.default_rng(1234)
+        h_kv, g, d, n = 2, 4, 8, 12
+        q = rng.standard_normal((3, h_kv * g, d))
+        k = rng.standard_normal((n, h_kv, d))
+        v = rng.standard_normal((n, h_kv, d))
+        kvmap = np.arange(h_kv * g) // g
+        a, b = P.pac(q, k, v), P.pac(q, k[:, kvmap, :], v[:, kvmap, :])
+        assert np.array_equal(np_(a.out), np_(b.out))
+
+    def test_errors(self, cuda_ok):
+        from paper_2505_17694_b200.errors import DimensionMismatch, EmptyVisibleSet, NoVisibleTokens, ShapeMismatch
+        a = lambda *x: np.asarray(x, np.float64).reshape(-1, 1, 1)
+        with pytest.raises(EmptyVisibleSet, match="1..2"):
+            P.pac(a(1.0), a(0.0, 0.0), a(1.0, 2.0), visible=[0])
+        with pytest.raises(DimensionMismatch, match="multiple"):
+            P.pac(np.zeros((1, 3, 4)), np.zeros((2, 2, 4)), np.zeros((2, 2, 4)))
+        with pytest.raises(ShapeMismatch, match="shapes differ"):
+            P.por(P.empty_partial(1, 1, 2), P.empty_partial(1, 1, 3))
+        with pytest.raises(NoVisibleTokens):
+            P.finalize(P.empty_partial(1, 1, 1))
+
+
+class TestPor:
+    def test_matches_concatenation(self, cuda_ok):
+        rng = np.random.default_rng(5)
+        k = rng.standard_normal((10, 2, 8))
+        v = rng.standard_normal((10, 2, 8))
+        q = rng.standard_normal((3, 4, 8))
+        whole = P.pac(q, k, v)
+        split = P.por(P.pac(q, k[:4], v[:4]), P.pac(q, k[4:], v[4:]))
+        assert rel_err(np_(split.out), np_(whole.out)) <= 1e-12
+        assert np.array_equal(np_(split.max_score), np_(whole.max_score))
+
+    def test_identity_and_elementwise_empty(self, cuda_ok):
+        rng = np.random.default_rng(6)
+        x = P.pac(rng.standard_normal((2, 2, 4)), rng.standard_normal((5, 2, 4)), rng.standard_normal((5, 2, 4)))
+        e = P.empty_partial(2, 2, 4)
+        for mgd in (P.por(x, e), P.por(e, x)):
+            assert np.array_equal(np_(mgd.out), np_(x.out))
+        y = x.copy()
+        y.exp_sum[0, 1] = 0.0
+        y.max_score[0, 1] = float("-inf")
+        y.out[0, 1] = 0.0
+        r = P.por(y, P.pac(rng.standard_normal((2, 2, 4)), rng.standard_normal((3, 2, 4)),
+                           rng.standard_normal((3, 2, 4))))
+        assert np.isfinite(np_(r.out)).all()
+
+
+# ----------------------------------------------------------------- execute
+class TestExecuteGolden:
+    """execute() on the reference's random forests vs the reference's own
+    execute/naive outputs (test_executor.py:104-110, acceptance :40-59)."""
+
+    def test_float64(self, cuda_ok, table):
+        z = golden_npz()
+        worst = 0.0
+        for doc in golden_json("forests.json")["forests"]:
+            spec = random_forest_spec(doc["seed"], with_masks=doc["masks"])
+            f, q = build(spec)
+            tasks = P.tasks_from_forest(f)
+            plan_u = P.plan_uniform_bk(tasks, table, 4, doc["bk"])
+            plan_a = P.divide_and_schedule(tasks, table, 4)
+            for plan, key in ((plan_u, "exec_u"), (plan_a, "exec_a")):
+                out = np_(P.execute(f, q, plan, P.BlockPool(4)))
+                worst = max(worst, rel_err(out, z[f"{key}_{doc['seed']}"]))
+                assert rel_err(out, z[f"naive_{doc['seed']}"]) <= 1e-10
+        assert worst <= 1e-10
+
+    def test_float32(self, cuda_ok, table):
+        z = golden_npz()
+        for doc in golden_json("forests.json")["forests"]:
+            spec = random_forest_spec(doc["seed"], with_masks=doc["masks"])
+            f, q = build(spec, "float32")
+            plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, doc["bk"])
+            out = np_(P.execute(f, q, plan))
+            assert rel_err(out, z[f"naive_{doc['seed']}"]) <= 1e-3
+            assert rel_err(out, z[f"exec32_{doc['seed']}"]) <= 1e-3
+
+    def test_float32_generic_kernel(self, cuda_ok, table):
+        z = golden_npz()
+        for doc in golden_json("forests.json")["forests"][:12]:
+            spec = random_forest_spec(doc["seed"], with_masks=doc["masks"])
+            f, q = build(spec, "float32")
+            plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, doc["bk"])
+            out = np_(P.execute(f, q, plan, flags=FLAG_NO_GEMV))
+            assert rel_err(out, z[f"naive_{doc['seed']}"]) <= 1e-3
+
+
+def d128_forest(seed, with_masks):
+    """random_forest recipe with d=128, g=4, h_kv=2: the head shape the
+    tensor-core and GEMV kernels specialise on."""
+    rng = np.random.default_rng(10_000 + seed)
+    spec = random_forest_spec(seed, with_masks=with_masks, max_bs=16)
+    h_kv, g, d = 2, 4, 128
+    sc = 1.0 / math.sqrt(d)
+    spec.h_q, spec.h_kv, spec.d = h_kv * g, h_kv, d
+    spec.keys = [None] + [rng.standard_normal((n, h_kv, d)) * sc for n in spec.length[1:]]
+    spec.values = [None] + [rng.standard_normal((n, h_kv, d)) * sc for n in spec.length[1:]]
+    spec.queries = rng.standard_normal((spec.bs, h_kv * g, d)) * sc
+    return spec
+
+
+class TestBf16Kernels:
+    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC])
+    def test_random_forests(self, cuda_ok, table, flags):
+        for seed in range(24):
+            spec = d128_forest(seed, with_masks=(seed % 2 == 1))
+            f, q = build(spec, "bfloat16")
+            plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, 1 + seed % 3)
+            out = np_(P.execute(f, q, plan, flags=flags))
+            ups = upcast_spec(spec)
+            ref = OA.naive_attention(ups.queries, oracle_forest(ups))
+            assert_bf16_close(out, ref)
+
+    def test_cfg1_float32(self, cuda_ok, table):
+        spec = W.make_config("cfg1", dtype=np.float32)
+        f, q = build(spec)
+        plan = P.divide_and_schedule(P.tasks_from_forest(f), table, 8)
+        out = np_(P.execute(f, q, plan))
+        ref = OA.naive_attention(np.asarray(spec.queries, np.float64), oracle_forest(spec))
+        assert rel_err(out, ref) <= 1e-3
+
+    def test_shared_root_device_plan(self, cuda_ok, table):
+        """cfg2 shape at reduced size: TC kernel on the split root, GEMV on
+        suffixes, LSE merge; device-level (row-chunk) plan."""
+        spec = W.two_level(4096, 128, 64, h_q=32, h_kv=8, d=128, seed=1, dtype=None)
+        f, q = build(spec, "bfloat16")
+        tasks = P.device_tasks(f, group_size=4)
+        plan = P.divide_and_schedule(tasks, table, 18)
+        step = DecodeStep(f, plan, 32, "bfloat16")
+        assert step.info.n_tc_groups > 0 and step.info.n_gemv_groups > 0
+        out = np_(P.execute(f, q, plan))
+        ups = upcast_spec(spec)
+        ref = OA.naive_attention(ups.queries, oracle_forest(ups))
+        assert_bf16_close(out, ref)
+
+    def test_repeatable_bitwise(self, cuda_ok, table):
+        spec = d128_forest(3, with_masks=True)
+        f, q = build(spec, "bfloat16")
+        plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, 2)
+        a = np_(P.execute(f, q, plan, flags=FLAG_FORCE_TC))
+        b = np_(P.execute(f, q, plan, flags=FLAG_FORCE_TC))
+        assert np.array_equal(a, b)
+
+    def test_plan_mismatch_errors(self, cuda_ok, table):
+        from paper_2505_17694_b200.errors import PlanForestMismatch
+        big = P.build_forest([(0, *[np.random.default_rng(0).standard_normal((8, 1, 8))] * 2),
+                              (1, *[np.random.default_rng(1).standard_normal((8, 1, 8))] * 2)], [(1, 2)])
+        small = P.build_forest([(0, *[np.random.default_rng(0).standard_normal((8, 1, 8))] * 2)], [(1,)])
+        q = P.QueryBatch(np.zeros((1, 1, 8)), 1)
+        plan = P.plan_uniform_bk(P.tasks_from_forest(small), table, 1, 1)
+        with pytest.raises(PlanForestMismatch, match="plan covers nodes"):
+            P.execute(big, q, plan)
+        donor = P.build_forest([(0, *[np.zeros((10, 1, 8))] * 2)], [(1,)])
+        target = P.build_forest([(0, *[np.zeros((12, 1, 8))] * 2)], [(1,)])
+        plan = P.plan_uniform_bk(P.tasks_from_forest(donor), table, 1, 2)
+        with pytest.raises(PlanForestMismatch, match="do not tile"):
+            P.execute(target, q, plan)
