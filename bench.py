@@ -56,41 +56,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region
+    (written by nvidia-smi itself via -f, so nothing is lost on stop)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index=0):
         self.proc = None
         self.path = Path("/tmp") / f"bench_clocks_{os.getpid()}.csv"
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={gpu_index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50", "-f", str(self.path)],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return None
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         rows = []
-        for line in self.path.read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                rows.append(parts)
+        if self.path.exists():
+            for line in self.path.read_text().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 7:
+                    rows.append(parts)
         if not rows:
-            return None
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[0]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[1]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(rows)}
 
@@ -203,7 +214,7 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     m = args.blocks or max(1, sms // h_local)
     t0 = time.perf_counter()
-    plan = P.divide_and_schedule(P.device_tasks(forest, g), table, m)
+    plan = P.divide_and_schedule(P.device_tasks(forest, g, rows_per_tile=256), table, m)
     plan_ms = (time.perf_counter() - t0) * 1e3
     step = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
                       flags=args.flags)
@@ -219,28 +230,38 @@ def main():
     work = P.device_work(forest, h_q, element_size=2, head_fraction=h_local / h_kv)
     stream = torch.cuda.current_stream(dev)
 
-    def timed(n, fn):
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(n):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / n
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+    def timed(n, fn, min_seconds=0.0):
+        """ms per call over n calls between barrier+sync on both sides, CUDA
+        events on the launching stream, max over ranks. With min_seconds,
+        the n-call window is repeated until that much wall time passed (so
+        the clock sampler sees the load) and the median window is used."""
+        windows = []
+        t_start = time.perf_counter()
+        while True:
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / n
+            if world > 1:
+                t = torch.tensor([ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            windows.append(ms)
+            if time.perf_counter() - t_start >= min_seconds or len(windows) >= 500:
+                break
+        return statistics.median(windows), len(windows)
 
     for _ in range(max(args.warmup, 3)):
         one_step(q_dev)
     torch.cuda.synchronize(dev)
     clocks = None if args.quick else ClockSampler(local_rank)
-    ms = timed(args.steps, lambda: one_step(q_dev))
+    ms, windows = timed(args.steps, lambda: one_step(q_dev), min_seconds=0 if args.quick else 2.0)
     clock_rec = clocks.stop() if clocks else None
 
     # per-kernel phases (same work, launched alone) for the roofline
@@ -254,7 +275,7 @@ def main():
                         flags=args.flags | fl)
         for _ in range(3):
             ph(q_dev, kp, vp, out=out)
-        phases[name] = timed(max(5, args.steps // 2), lambda: ph(q_dev, kp, vp, out=out))
+        phases[name] = timed(max(5, args.steps // 2), lambda: ph(q_dev, kp, vp, out=out))[0]
 
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     total_bytes = work["unique_kv_bytes"] * world
@@ -294,7 +315,7 @@ def main():
 
         for _ in range(3):
             e2e_step()
-        e2e_ms = timed(args.steps, e2e_step)
+        e2e_ms = timed(args.steps, e2e_step)[0]
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": q_host.numel() * q_host.element_size(),
                "d2h_bytes_per_step": out_host.numel() * out_host.element_size()}
@@ -308,7 +329,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms, "timed_windows": windows, "us_per_step": ms * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
             "config": {"workload": cfg["label"], "bs": cfg["batch"], "h_q": h_q, "h_kv": h_kv, "d": d,

@@ -156,7 +156,10 @@ CODEC_API int32_t codec_plan_read(const codec_plan* p, int64_t* b_k, int32_t* su
  *
  * Each plan task owns a contiguous chunk of its node's query set (a
  * node-level plan, tasks_from_forest(), is the one-chunk case). Each
- * subtask x row tile becomes one "group"; group x local kv head is one CTA.
+ * subtask x row tile becomes one "group". GEMV / generic groups run one CTA
+ * per (group, local kv head); tensor-core groups are LPT-packed (the
+ * reference's greedy rule, scheduler.py:142-155) onto sm_count/h_local
+ * persistent CTAs per head, which walk their group lists in order.
  * ==================================================================== */
 typedef struct {
   int32_t bs, h_q, h_kv, d;
@@ -164,6 +167,8 @@ typedef struct {
   int32_t kv_dtype;               /* codec_dtype of q, k, v */
   int32_t flags;                  /* CODEC_FLAG_* */
   int64_t pool_tokens;            /* T: token stride of one head in the pool */
+  int32_t sm_count;               /* SMs of the device (0 = 148); sizes the persistent TC grid */
+  int32_t reserved;
 } codec_dims;
 
 #define CODEC_FLAG_NO_TC      1   /* never use the tcgen05 shared-node kernel */
@@ -190,6 +195,7 @@ typedef struct {
   int32_t off_tc, off_gemv, off_gen, off_rows;         /* int32 offsets into the blob */
   int32_t off_merge_req, off_merge_ptr, off_merge_slot;
   int32_t h_local;                                     /* head_end - head_begin */
+  int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTAs per head, their group CSR */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

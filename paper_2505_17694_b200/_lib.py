@@ -62,7 +62,8 @@ class PlanInfo(C.Structure):
 
 class Dims(C.Structure):
     _fields_ = [("bs", I32), ("h_q", I32), ("h_kv", I32), ("d", I32), ("head_begin", I32),
-                ("head_end", I32), ("kv_dtype", I32), ("flags", I32), ("pool_tokens", I64)]
+                ("head_end", I32), ("kv_dtype", I32), ("flags", I32), ("pool_tokens", I64),
+                ("sm_count", I32), ("reserved", I32)]
 
 
 class TableInfo(C.Structure):
@@ -70,7 +71,8 @@ class TableInfo(C.Structure):
                 ("n_rows", I32), ("n_slots", I32), ("n_merge", I32), ("gemv_rows", I32),
                 ("off_tc", I32), ("off_gemv", I32), ("off_gen", I32), ("off_rows", I32),
                 ("off_merge_req", I32), ("off_merge_ptr", I32), ("off_merge_slot", I32),
-                ("h_local", I32), ("blob_len", I64), ("workspace_bytes", I64)]
+                ("h_local", I32), ("n_tc_blocks", I32), ("off_tc_block_ptr", I32),
+                ("blob_len", I64), ("workspace_bytes", I64)]
 
 
 _SIGS = {

@@ -26,5 +26,7 @@ constexpr int kRowInts = 4;
 
 // minimum query-head rows for a subtask to take the tensor-core kernel
 constexpr int kTcMinRows = 16;
+// query-head rows of one tensor-core group (two M=128 tiles)
+constexpr int kTcGroupRows = 256;
 
 }  // namespace codec

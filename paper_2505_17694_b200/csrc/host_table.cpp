@@ -157,7 +157,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
                      !(dims->flags & CODEC_FLAG_NO_TC);
   const bool gemv_ok = (dims->kv_dtype == CODEC_BF16 || dims->kv_dtype == CODEC_F32) &&
                        (d == 64 || d == 128 || d == 256) && g <= 16 && !(dims->flags & CODEC_FLAG_NO_GEMV);
-  const int32_t tc_reqs = tc_ok ? 128 / g : 0;
+  const int32_t tc_reqs = tc_ok ? std::max(1, kTcGroupRows / g) : 0;
   const int32_t gemv_rows = g <= 4 ? 4 : (g <= 8 ? 8 : 16);
 
   // ---- rows and slots
@@ -254,7 +254,51 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
         ++count;
       }
   };
-  emit_groups(kKindTc, in.n_tc_groups, in.off_tc);
+  // ---- tensor-core groups: LPT onto the persistent CTA slots of one head
+  // (cost = 64-token tiles, the unit the kernel iterates), same rule as
+  // greedy_assign (scheduler.py:142-155); each block keeps its groups in
+  // assignment order.
+  {
+    std::vector<Grp> tcg;
+    for (auto& gr : groups)
+      if (gr.kind == kKindTc) tcg.push_back(gr);
+    const int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
+    const int32_t h_local = dims->head_end - dims->head_begin;
+    int32_t m_tc = std::max(1, sms / h_local);
+    m_tc = std::min<int32_t>(m_tc, (int32_t)tcg.size());
+    std::vector<int64_t> cost(tcg.size());
+    for (size_t i = 0; i < tcg.size(); ++i) {
+      int64_t mv = 0;
+      for (int32_t k = 0; k < tcg[i].n_rows; ++k) mv = std::max<int64_t>(mv, rows[4 * (tcg[i].row_begin + k) + 1]);
+      cost[i] = (mv + 63) / 64;
+    }
+    std::vector<int32_t> order(tcg.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+    std::vector<int64_t> load(std::max(m_tc, 1), 0);
+    std::vector<std::vector<int32_t>> per_block(std::max(m_tc, 1));
+    for (int32_t i : order) {
+      int32_t best = 0;
+      for (int32_t b = 1; b < m_tc; ++b)
+        if (load[b] < load[best]) best = b;
+      load[best] += cost[i];
+      per_block[best].push_back(i);
+    }
+    in.off_tc = (int32_t)blob.size();
+    in.n_tc_groups = (int32_t)tcg.size();
+    std::vector<int32_t> block_ptr{0};
+    for (int32_t b = 0; b < m_tc; ++b) {
+      for (int32_t i : per_block[b]) {
+        const Grp& gr = tcg[i];
+        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.sub, gr.node, b, 0};
+        blob.insert(blob.end(), rec, rec + kGroupInts);
+      }
+      block_ptr.push_back(block_ptr.back() + (int32_t)per_block[b].size());
+    }
+    in.n_tc_blocks = tcg.empty() ? 0 : m_tc;
+    in.off_tc_block_ptr = (int32_t)blob.size();
+    blob.insert(blob.end(), block_ptr.begin(), block_ptr.end());
+  }
   emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
   emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
   in.off_rows = (int32_t)blob.size();

@@ -24,6 +24,7 @@
 #include "common.h"
 #include "device_table.h"
 #include "device_util.cuh"
+#include "tc_ptx.cuh"
 
 namespace codec {
 
@@ -152,10 +153,11 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
         float part[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          float a = 0.f;
+          float2 a = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int e = 0; e < C::EPT; ++e) a = fmaf(qf[r][e], kf[e], a);
-          part[r] = a;
+          for (int e = 0; e < C::EPT; e += 2)
+            a = tc::ffma2(make_float2(qf[r][e], qf[r][e + 1]), make_float2(kf[e], kf[e + 1]), a);
+          part[r] = a.x + a.y;
         }
         // reduce-scatter R partials over the TPT lanes of this token
 #pragma unroll
@@ -180,25 +182,30 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
       for (int u = 1; u < C::STEPS; ++u) mx = fmaxf(mx, sc[u]);
 #pragma unroll
       for (int b = C::TPT; b < 32; b <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, b));
-      const float m_new = fmaxf(m_run, mx);
-      const bool dead = m_new == neg_inf<float>();
-      const float alpha = dead ? 1.f : fast_exp2(m_run - m_new);
+      // lazy rescale: the exponent reference only moves when this chunk's
+      // max beats it by more than 2^8 (p <= 256 otherwise: exact enough in fp32)
+      const bool need = mx > m_run + 8.f;
+      const int src0 = ts * C::TPT;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = need ? fast_exp2(m_run - mx) : 1.f;  // 0 on the first chunk
+        l_run *= alpha;
+        m_run = need ? mx : m_run;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float a = __shfl_sync(0xffffffffu, alpha, src0 + (r << (C::LTPT - C::LR)));
+#pragma unroll
+          for (int e = 0; e < C::EPT; ++e) acc[r][e] *= a;
+        }
+      }
+      const bool dead = m_run == neg_inf<float>();
       float p[C::STEPS];
       float psum = 0.f;
 #pragma unroll
       for (int u = 0; u < C::STEPS; ++u) {
-        p[u] = dead ? 0.f : fast_exp2(sc[u] - m_new);
+        p[u] = dead ? 0.f : fast_exp2(sc[u] - m_run);
         psum += p[u];
       }
-      l_run = l_run * alpha + psum;
-      m_run = m_new;
-      const int src0 = ts * C::TPT;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float a = __shfl_sync(0xffffffffu, alpha, src0 + (r << (C::LTPT - C::LR)));
-#pragma unroll
-        for (int e = 0; e < C::EPT; ++e) acc[r][e] *= a;
-      }
+      l_run += psum;
 #pragma unroll
       for (int u = 0; u < C::STEPS; ++u) {
         const int lt = (warp * C::STEPS + u) * C::NTS + ts;
@@ -213,7 +220,12 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
         for (int r = 0; r < R; ++r) {
           const float pr = __shfl_sync(0xffffffffu, p[u], src0 + (r << (C::LTPT - C::LR)));
 #pragma unroll
-          for (int e = 0; e < C::EPT; ++e) acc[r][e] = fmaf(pr, vf[e], acc[r][e]);
+          for (int e = 0; e < C::EPT; e += 2) {
+            const float2 a = tc::ffma2(make_float2(pr, pr), make_float2(vf[e], vf[e + 1]),
+                                       make_float2(acc[r][e], acc[r][e + 1]));
+            acc[r][e] = a.x;
+            acc[r][e + 1] = a.y;
+          }
         }
       }
       __syncwarp();
@@ -228,8 +240,9 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
 #pragma unroll
         for (int e = 0; e < C::EPT; ++e) acc[r][e] += __shfl_xor_sync(0xffffffffu, acc[r][e], b);
     }
-    // stash per-warp (m, l, acc) in the (now idle) K ring
-    __syncwarp();
+    // stash per-warp (m, l, acc) in the K ring once every consumer warp is
+    // done reading it (named barrier over the 4 consumer warps)
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kGemvWarps) : "memory");
     float* wm = reinterpret_cast<float*>(smem) + warp * (R * (D + 2));
     if (ts == 0) {
 #pragma unroll

@@ -1,24 +1,35 @@
 // K2: shared-node split attention on the 5th-generation tensor cores.
 //
-// One CTA = (TC group, kv head): a KV slice [kv_tok, kv_tok + len) of a
-// shared node and up to 128 query-head rows (128/g requests of the node's
-// query set, each with its g query heads -- the GQA group becomes the M
-// dimension, so sharing turns the per-request GEMVs into one dense
-// contraction). Per 128-token tile j:
-//     S   = Q K_j^T              tcgen05.mma M128 N128 K128, S in TMEM
-//     P   = exp2(S*c - m)        softmax warps, online max/sum per row
-//     O  += P V_j                tcgen05.mma M128 N128 K128, O in TMEM
-// Math is the reference's pac_kernel (_kernels.pyx:25-54) per row; the
-// partial (O/l, m, l) feeds the same LSE merge as the other kernels.
+// Persistent CTA = (schedule block b, kv head h). It walks the TC groups
+// the balancer assigned to block b (LPT over the SM slots, host_table.cpp);
+// a group is a KV slice [kv_tok, kv_tok + len) of a shared node and up to
+// 256 query-head rows (256/g requests of the node's query set with their g
+// query heads: GQA packing turns the per-request GEMVs into one dense
+// contraction). The rows form two M=128 tiles, Q0 and Q1, that share every
+// K/V tile. Per 128-token KV tile t and Q tile i:
+//     S_i = Q_i K_t^T      tcgen05.mma SS, M128 N128 K128, fp32 in TMEM
+//     P_i = 2^(S_i c - m)  softmax warpgroup i (thread = row = TMEM lane),
+//                          written back over S_i as bf16 (tcgen05.st)
+//     O_i += P_i V_t       tcgen05.mma TS (A = P from TMEM), M128 N128 K128
+// Per row this is the reference's pac_kernel math (_kernels.pyx:25-54);
+// the partial (O/l, m, l) feeds the LSE merge (kern_merge.cu).
 //
-// Warp roles (192 threads): warp 0 = TMA producer (K and V rings, 2
-// stages each, SWIZZLE_128B boxes of 128 tokens x 64 dims), warp 1 = TMEM
-// allocator + single-thread MMA issuer, warps 2-5 = softmax / epilogue
-// (thread = one query row = one TMEM lane). S_{j+1} is issued as soon as
-// the softmax has pulled S_j into registers, so the QK^T of the next tile
-// overlaps the exponentials of this one. P goes through shared memory
-// (K-major SW128) as the A operand of the PV MMA; V is consumed MN-major
-// straight from its TMA layout.
+// Why this shape: the SS QK^T MMA already consumes SMEM bandwidth at its
+// peak (A and B from SMEM), so P never goes through SMEM (TS MMA) and the
+// 128-token tile halves the Q re-reads per token. The issue order
+//     PV_0(t) S_0(t+1) PV_1(t) S_1(t+1)
+// ping-pongs the two softmax warpgroups: while WG0 exponentiates S_0(t+1)
+// the tensor pipe runs PV_1(t) and S_1(t+1). In-order tcgen05 execution
+// makes S_i(t+1) (which overwrites P_i(t)) safe after PV_i(t), and the
+// commit behind S_i(t) guarantees PV_i(t-1) landed before softmax i reads
+// or rescales O_i.
+//
+// Warp roles (320 threads): warps 0-3 softmax of Q0, 4-7 softmax of Q1,
+// warp 8 TMA producer (K/V 2-stage rings of 128x64 SWIZZLE_128B boxes),
+// warp 9 TMEM allocator + single-thread MMA issuer. Softmax: packed f32x2
+// math, exponentials split between MUFU.EX2 and a degree-3 polynomial on
+// the FMA pipe, lazy O rescale (only when a row max grows by > 2^8),
+// masking only on a row's last tile.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -29,39 +40,71 @@
 
 namespace codec {
 
-constexpr int kTcThreads = 192;
-constexpr int kTcRows = 128;        // M
-constexpr int kTcTok = 128;         // tokens per tile (N of QK^T, K of PV)
-constexpr int kTcD = 128;           // head dim
-constexpr int kTcTile = 128 * 128 * 2;  // bytes of one bf16 128x128 tile
-constexpr int kTcKStages = 2;
-constexpr int kTcVStages = 2;
-constexpr int kOffQ = 0;
-constexpr int kOffP = kOffQ + kTcTile;
-constexpr int kOffK = kOffP + kTcTile;
-constexpr int kOffV = kOffK + kTcKStages * kTcTile;
-constexpr int kOffBar = kOffV + kTcVStages * kTcTile;
-constexpr int kTcSmem = kOffBar + 256 + 1024;  // + barriers + alignment slack
-constexpr uint32_t kTmemCols = 256;  // S: cols [0,128), O: cols [128,256)
+constexpr int kTcThreads = 320;
+constexpr int kTcBN = 128;                      // tokens per KV tile
+constexpr int kTcD = 128;                       // head dim
+constexpr int kTcStages = 2;                    // K and V ring depth
+constexpr int kTileBytes = 128 * 128 * 2;       // 32 KB: one 128x128 bf16 tile (Q, K or V)
+constexpr int kAtomBytes = kTileBytes / 2;      // 64-element-wide SW128 atom column
+constexpr int kOffQ = 0;                                 // Q0, Q1
+constexpr int kOffK = kOffQ + 2 * kTileBytes;            // K ring
+constexpr int kOffV = kOffK + kTcStages * kTileBytes;    // V ring
+constexpr int kOffBar = kOffV + kTcStages * kTileBytes;
+constexpr int kTcSmem = kOffBar + 512 + 1024;            // barriers + alignment slack
+constexpr uint32_t kTmemCols = 512;  // S0/P0 [0,128) S1/P1 [128,256) O0 [256,384) O1 [384,512)
+constexpr float kRescaleLog2 = 8.f;
 
 struct TcBars {
   uint64_t q_full;
-  uint64_t k_full[kTcKStages], k_empty[kTcKStages];
-  uint64_t v_full[kTcVStages], v_empty[kTcVStages];
-  uint64_t s_full, s_free, p_full, pv_done;
+  uint64_t k_full[kTcStages], k_empty[kTcStages];
+  uint64_t v_full[kTcStages], v_empty[kTcStages];
+  uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
   uint32_t tmem_slot;
 };
 
-// byte offset of 16-byte chunk `c` (0..15 along a 128-element row) of row
-// `r` in a K-major SWIZZLE_128B tile made of two 64-element atoms
-__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
-  const int atom = c >> 3, cc = c & 7;
-  return atom * (128 * 128) + r * 128 + ((cc ^ (r & 7)) << 4);
+// 16-byte chunk c (0..15 along a 128-element row) of row r in a K-major
+// SWIZZLE_128B 128x128 tile made of two 64-element atom columns
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return (c >> 3) * kAtomBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+// 2^x on the FMA/ALU pipes (Cody-Waite split, degree-3 minimax on
+// [-1/2, 1/2], rel. error 7.5e-5 -- below the bf16 rounding P gets anyway)
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round-to-nearest into the mantissa
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.05517153f, f, 0.24261101f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992808f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+struct GroupView {
+  int kv_tok, n_req, n_tiles;
+  const int32_t* rows;
+};
+
+__device__ __forceinline__ GroupView group_view(const int32_t* table, int off_groups, int off_rows, int gidx) {
+  const int32_t* grp = table + off_groups + gidx * kGroupInts;
+  GroupView v;
+  v.kv_tok = grp[kGrpKvTok];
+  v.n_req = grp[kGrpNRows];
+  v.rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
+  int max_vis = 0;
+  for (int i = 0; i < v.n_req; ++i) max_vis = max(max_vis, v.rows[i * kRowInts + 1]);
+  v.n_tiles = (max_vis + kTcBN - 1) / kTcBN;
+  return v;
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                  const int32_t* __restrict__ table, int off_groups, int off_rows,
+                  const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml) {
   extern __shared__ uint8_t smem_raw[];
@@ -71,35 +114,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   TcBars* bars = reinterpret_cast<TcBars*>(smem + kOffBar);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int32_t* grp = table + off_groups + blockIdx.x * kGroupInts;
-  const int kh = blockIdx.y;
-  const int kv_tok = grp[kGrpKvTok];
-  const int n_req = grp[kGrpNRows];
-  const int32_t* rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
-  // tiles needed = max visible over the group's rows
-  int max_vis = 0;
-  for (int i = 0; i < n_req; ++i) max_vis = max(max_vis, rows[i * kRowInts + 1]);
-  const int n_tiles = (max_vis + kTcTok - 1) / kTcTok;
-  const int row_base = kh * (int)pool_tokens + kv_tok;  // row of the 2D pool view
+  const int blk = blockIdx.x, kh = blockIdx.y;
+  const int g_begin = table[off_block_ptr + blk], g_end = table[off_block_ptr + blk + 1];
 
   if (tid == 0) {
-    mbar_init(&bars->q_full, 128);
-    for (int s = 0; s < kTcKStages; ++s) {
+    mbar_init(&bars->q_full, 256);
+    for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->k_empty[s], 1);
-    }
-    for (int s = 0; s < kTcVStages; ++s) {
       mbar_init(&bars->v_full[s], 1);
       mbar_init(&bars->v_empty[s], 1);
     }
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->s_free, 128);
-    mbar_init(&bars->p_full, 128);
-    mbar_init(&bars->pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_full[i], 128);
+      mbar_init(&bars->o_done[i], 1);
+      mbar_init(&bars->o_free[i], 128);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
-  if (warp == 0 && lane == 0) {
+  if (warp == 9) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
+  if (warp == 8 && lane == 0) {
     tc::prefetch_tmap(&tmk);
     tc::prefetch_tmap(&tmv);
   }
@@ -107,192 +142,239 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
-  const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+  if (warp == 8) {
+    // ================================================ TMA producer
     if (lane == 0) {
-      for (int j = 0; j < n_tiles; ++j) {
-        const int y = row_base + j * kTcTok;
-        const int ks = j % kTcKStages;
-        if (j >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((j / kTcKStages) - 1) & 1);
-        mbar_arrive_expect_tx(&bars->k_full[ks], kTcTile);
-        uint8_t* kd = smem + kOffK + ks * kTcTile;
-        tc::tma_load_2d(kd, &tmk, 0, y, &bars->k_full[ks]);
-        tc::tma_load_2d(kd + 128 * 128, &tmk, 64, y, &bars->k_full[ks]);
-        const int vs = j % kTcVStages;
-        if (j >= kTcVStages) mbar_wait(&bars->v_empty[vs], ((j / kTcVStages) - 1) & 1);
-        mbar_arrive_expect_tx(&bars->v_full[vs], kTcTile);
-        uint8_t* vd = smem + kOffV + vs * kTcTile;
-        tc::tma_load_2d(vd, &tmv, 0, y, &bars->v_full[vs]);
-        tc::tma_load_2d(vd + 128 * 128, &tmv, 64, y, &bars->v_full[vs]);
+      int t = 0;  // global KV tile counter (ring position)
+      for (int gi = g_begin; gi < g_end; ++gi) {
+        const GroupView gv = group_view(table, off_groups, off_rows, gi);
+        const int row0 = kh * (int)pool_tokens + gv.kv_tok;
+        for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+          const int s = t % kTcStages;
+          const int y = row0 + j * kTcBN;
+          if (t >= kTcStages) mbar_wait(&bars->k_empty[s], ((t / kTcStages) - 1) & 1);
+          mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
+          uint8_t* kd = smem + kOffK + s * kTileBytes;
+          tc::tma_load_2d(kd, &tmk, 0, y, &bars->k_full[s]);
+          tc::tma_load_2d(kd + kAtomBytes, &tmk, 64, y, &bars->k_full[s]);
+          if (t >= kTcStages) mbar_wait(&bars->v_empty[s], ((t / kTcStages) - 1) & 1);
+          mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
+          uint8_t* vd = smem + kOffV + s * kTileBytes;
+          tc::tma_load_2d(vd, &tmv, 0, y, &bars->v_full[s]);
+          tc::tma_load_2d(vd + kAtomBytes, &tmv, 64, y, &bars->v_full[s]);
+        }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
+  } else if (warp == 9) {
+    // ================================================ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc_s = tc::idesc_bf16(128, 128, false, false);
-      constexpr uint32_t idesc_o = tc::idesc_bf16(128, 128, false, true);
-      const uint32_t q_addr = sbase + kOffQ, p_addr = sbase + kOffP;
-      auto issue_s = [&](int j) {
-        const int ks = j % kTcKStages;
-        mbar_wait(&bars->k_full[ks], (j / kTcKStages) & 1);
-        tc::fence_after();
-        const uint32_t k_addr = sbase + kOffK + ks * kTcTile;
+      constexpr uint32_t idesc_s = tc::idesc_bf16(128, kTcBN, false, false);
+      constexpr uint32_t idesc_o = tc::idesc_bf16(128, kTcD, false, true);
+      int t = 0;  // global tile counter
+      int gq = 0;
+      auto issue_s = [&](int i, int tt) {
+        const int s = tt % kTcStages;
+        const uint32_t k_addr = sbase + kOffK + s * kTileBytes;
+        const uint32_t q_addr = sbase + kOffQ + i * kTileBytes;
 #pragma unroll
         for (int k = 0; k < kTcD / 16; ++k) {
-          const uint32_t koff = (k >> 2) * (128 * 128) + (k & 3) * 32;
-          tc::mma_f16_ss(tmem_s, tc::smem_desc(q_addr + koff, 16, 1024), tc::smem_desc(k_addr + koff, 16, 1024),
+          const uint32_t off = (k >> 2) * kAtomBytes + (k & 3) * 32;
+          tc::mma_f16_ss(tmem + i * 128, tc::smem_desc(q_addr + off, 16, 1024), tc::smem_desc(k_addr + off, 16, 1024),
                          idesc_s, k > 0 ? 1u : 0u);
         }
-        tc::commit(&bars->k_empty[ks]);
-        tc::commit(&bars->s_full);
+        tc::commit(&bars->s_full[i]);
+        if (i == 1) tc::commit(&bars->k_empty[s]);
       };
-      mbar_wait(&bars->q_full, 0);
-      if (n_tiles > 0) issue_s(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) {
-          mbar_wait(&bars->s_free, j & 1);  // softmax holds S_j in registers
-          issue_s(j + 1);
+      for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
+        const GroupView gv = group_view(table, off_groups, off_rows, gi);
+        if (gv.n_tiles == 0) {  // (cannot happen: every row sees >= 1 token) keep gq in step
+          --gq;
+          continue;
         }
-        const int vs = j % kTcVStages;
-        mbar_wait(&bars->v_full[vs], (j / kTcVStages) & 1);
-        mbar_wait(&bars->p_full, j & 1);
-        tc::fence_after();
-        const uint32_t v_addr = sbase + kOffV + vs * kTcTile;
+        mbar_wait(&bars->q_full, gq & 1);
+        {
+          const int s = t % kTcStages;
+          mbar_wait(&bars->k_full[s], (t / kTcStages) & 1);
+          tc::fence_after();
+          issue_s(0, t);
+          issue_s(1, t);
+        }
+        for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+          const int s = t % kTcStages;
+          const bool more = j + 1 < gv.n_tiles;
+          mbar_wait(&bars->v_full[s], (t / kTcStages) & 1);
+          if (more) mbar_wait(&bars->k_full[(t + 1) % kTcStages], ((t + 1) / kTcStages) & 1);
+          const uint32_t v_addr = sbase + kOffV + s * kTileBytes;
+          for (int i = 0; i < 2; ++i) {
+            mbar_wait(&bars->p_full[i], t & 1);                        // P_i(t) in TMEM
+            if (j == 0 && gq > 0) mbar_wait(&bars->o_free[i], (gq - 1) & 1);  // epilogue read O_i
+            tc::fence_after();
+            const uint32_t p_tmem = tmem + i * 128;
+            const uint32_t o_tmem = tmem + 256 + i * 128;
 #pragma unroll
-        for (int k = 0; k < kTcTok / 16; ++k) {
-          // A = P (K-major over tokens), B = V (MN-major: N = head dim)
-          const uint32_t aoff = (k >> 2) * (128 * 128) + (k & 3) * 32;
-          const uint32_t boff = k * 16 * 128;
-          tc::mma_f16_ss(tmem_o, tc::smem_desc(p_addr + aoff, 16, 1024),
-                         tc::smem_desc(v_addr + boff, 128 * 128, 1024), idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kTcBN / 16; ++k)
+              tc::mma_f16_ts(o_tmem, p_tmem + k * 8, tc::smem_desc(v_addr + k * 16 * 128, kAtomBytes, 1024),
+                             idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+            if (i == 1) tc::commit(&bars->v_empty[s]);
+            if (more) {
+              issue_s(i, t + 1);
+            } else {
+              tc::commit(&bars->o_done[i]);
+            }
+          }
         }
-        tc::commit(&bars->v_empty[vs]);
-        tc::commit(&bars->pv_done);
       }
     }
   } else {
-    // ------------------------------------------------ softmax / epilogue
-    const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-    const int r = quad * 32 + lane;        // query row == TMEM lane
+    // ================================================ softmax warpgroups
+    const int wg = warp >> 2;                 // Q tile
+    const int quad = warp & 3;                // TMEM lane quadrant
+    const int r = quad * 32 + lane;           // row in the Q tile == TMEM lane
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const int ridx = r / g;                // request slot within the group
-    const bool valid = ridx < n_req;
-    const int req = valid ? rows[ridx * kRowInts + 0] : 0;
-    const int vis = valid ? rows[ridx * kRowInts + 1] : 0;
-    const int slot = valid ? rows[ridx * kRowInts + 2] : 0;
-    const int qh = kh * g + (r % g);
-    // stage Q row r (K-major SW128)
-    {
-      uint8_t* qs = smem + kOffQ;
-      const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(qs + sw128_off(r, c)) = v;
-      }
-      tc::fence_proxy_async_smem();
-      mbar_arrive(&bars->q_full);
-    }
+    const uint32_t s_tmem = tmem + wg * 128 + lane_addr;
+    const uint32_t o_tmem = tmem + 256 + wg * 128 + lane_addr;
     const float cscale = 1.4426950408889634f * rsqrtf((float)kTcD);
-    float m_run = neg_inf<float>(), l_run = 0.f;
-    uint8_t* ps = smem + kOffP;
-    for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(&bars->s_full, j & 1);
-      tc::fence_after();
-      uint32_t sreg[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tmem_s + lane_addr + c * 32, sreg + c * 32);
-      tc::wait_ld();
-      tc::fence_before();
-      mbar_arrive(&bars->s_free);
-      const int lim = vis - j * kTcTok;  // tokens of this tile visible to the row
-      float mt = neg_inf<float>();
-#pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        float s = __uint_as_float(sreg[c]) * cscale;
-        s = (c < lim) ? s : neg_inf<float>();
-        sreg[c] = __float_as_uint(s);
-        mt = fmaxf(mt, s);
+    const float2 c2 = make_float2(cscale, cscale);
+    int t = 0, gq = 0;
+    for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      if (gv.n_tiles == 0) {
+        --gq;
+        continue;
       }
-      const float m_new = fmaxf(m_run, mt);
-      if (j > 0) {
-        mbar_wait(&bars->pv_done, (j - 1) & 1);  // P buffer free, O settled
+      const int grow = wg * 128 + r;          // row of the 256-row group
+      const int ridx = grow / g;
+      const bool valid = ridx < gv.n_req;
+      const int req = valid ? gv.rows[ridx * kRowInts + 0] : 0;
+      const int vis = valid ? gv.rows[ridx * kRowInts + 1] : 0;
+      const int slot = valid ? gv.rows[ridx * kRowInts + 2] : 0;
+      const int qh = kh * g + (grow % g);
+      {  // stage my Q row (K-major SW128); the previous group's S MMAs are complete
+        uint8_t* qs = smem + kOffQ + wg * kTileBytes;
+        const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const uint4 v = valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(qs + sw128(r, c)) = v;
+        }
+        tc::fence_proxy_async_smem();
+        mbar_arrive(&bars->q_full);
+      }
+      float m_used = 0.f;  // exponent reference (log2 units)
+      float2 l2 = make_float2(0.f, 0.f);
+      for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+        mbar_wait(&bars->s_full[wg], t & 1);   // also: PV_wg(t-1) has landed (commit order)
         tc::fence_after();
-        const bool need = valid && m_new > m_run;
-        if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
-          const float alpha = need ? fast_exp2(m_run - m_new) : 1.f;
-          l_run *= alpha;
+        const int lim = vis - j * kTcBN;
+        const bool full = __all_sync(0xffffffffu, !valid || lim >= kTcBN);
+        // pass 1: row max over the tile, 32 columns at a time (next load in flight)
+        uint32_t sa[32], sb[32];
+        float mx = neg_inf<float>();
+        tc::tmem_ld32(s_tmem, sa);
+        tc::wait_ld();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tc::tmem_ld32(tmem_o + lane_addr + c * 32, o);
-            tc::wait_ld();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* cur = (c & 1) ? sb : sa;
+          uint32_t* nxt = (c & 1) ? sa : sb;
+          if (c + 1 < 4) tc::tmem_ld32(s_tmem + (c + 1) * 32, nxt);
+          if (!full) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tc::tmem_st32(tmem_o + lane_addr + c * 32, o);
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= lim) cur[i] = 0xff800000u;  // -inf
           }
-          tc::wait_st();
-        }
-      }
-      m_run = valid ? m_new : m_run;
-      // P row -> bf16 K-major SW128
-      float psum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        uint32_t w[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          float p0 = valid ? fast_exp2(__uint_as_float(sreg[c * 8 + 2 * h]) - m_new) : 0.f;
-          float p1 = valid ? fast_exp2(__uint_as_float(sreg[c * 8 + 2 * h + 1]) - m_new) : 0.f;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          // accumulate l from the rounded values the MMA actually sees
-          float2 rb = __bfloat1622float2(b2);
-          psum += rb.x + rb.y;
-          w[h] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])));
+          tc::wait_ld();
         }
-        *reinterpret_cast<uint4*>(ps + sw128_off(r, c)) = make_uint4(w[0], w[1], w[2], w[3]);
+        const float mt = valid ? mx * cscale : 0.f;
+        if (j == 0) {
+          m_used = mt;
+        } else {
+          const bool need = mt > m_used + kRescaleLog2;
+          if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
+            const float alpha = need ? fast_exp2(m_used - mt) : 1.f;
+            l2.x *= alpha;
+            l2.y *= alpha;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              tc::tmem_ld32(o_tmem + c * 32, sa);
+              tc::wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) sa[i] = __float_as_uint(__uint_as_float(sa[i]) * alpha);
+              tc::tmem_st32(o_tmem + c * 32, sa);
+            }
+            if (need) m_used = mt;
+          }
+        }
+        // pass 2: P = 2^(S c - m) as bf16 pairs; chunk c (S columns 32c..32c+31)
+        // lands in P columns 16c..16c+15, i.e. over S columns already consumed
+        const float2 nm = make_float2(-m_used, -m_used);
+        tc::tmem_ld32(s_tmem, sa);
+        tc::wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t* cur = (c & 1) ? sb : sa;
+          uint32_t* nxt = (c & 1) ? sa : sb;
+          if (c + 1 < 4) tc::tmem_ld32(s_tmem + (c + 1) * 32, nxt);
+          if (!full) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= lim) cur[i] = 0xff800000u;
+          }
+          uint32_t pw[16];
+#pragma unroll
+          for (int w = 0; w < 16; ++w) {
+            const float2 x = tc::ffma2(make_float2(__uint_as_float(cur[2 * w]), __uint_as_float(cur[2 * w + 1])), c2, nm);
+            float2 p;
+            p.x = fast_exp2(x.x);  // MUFU
+            p.y = poly_exp2(x.y);  // FMA pipe
+            l2 = tc::fadd2(l2, p);
+            pw[w] = pack_bf16(p.x, p.y);
+          }
+          tc::wait_ld();  // the next chunk's load must land before its columns are overwritten
+          tc::tmem_st16(s_tmem + c * 16, pw);
+        }
+        tc::wait_st();
+        tc::fence_before();
+        mbar_arrive(&bars->p_full[wg]);
       }
-      l_run += psum;
-      tc::fence_proxy_async_smem();
-      tc::fence_before();
-      mbar_arrive(&bars->p_full);
-    }
-    // epilogue: O / l
-    if (n_tiles > 0) {
-      mbar_wait(&bars->pv_done, (n_tiles - 1) & 1);
+      // ---- epilogue: O / l once the group's last PV landed
+      const float l_run = l2.x + l2.y;
+      mbar_wait(&bars->o_done[wg], gq & 1);
       tc::fence_after();
-    }
-    float* dst;
-    if (slot < 0) {
-      dst = out + ((int64_t)req * hq_local + qh) * kTcD;
-    } else {
-      const int64_t ei = (int64_t)slot * hq_local + qh;
-      dst = part_o + ei * kTcD;
-      if (valid) {
-        part_ml[2 * ei] = m_run * 0.69314718055994530942f;
-        part_ml[2 * ei + 1] = l_run;
+      float* dst;
+      if (slot < 0) {
+        dst = out + ((int64_t)req * hq_local + qh) * kTcD;
+      } else {
+        const int64_t ei = (int64_t)slot * hq_local + qh;
+        dst = part_o + ei * kTcD;
+        if (valid) {
+          part_ml[2 * ei] = m_used * 0.69314718055994530942f;  // natural-log units
+          part_ml[2 * ei + 1] = l_run;
+        }
       }
-    }
-    const float inv = 1.f / l_run;
+      const float inv = 1.f / l_run;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tc::tmem_ld32(tmem_o + lane_addr + c * 32, o);
-      tc::wait_ld();
-      if (valid) {
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tc::tmem_ld32(o_tmem + c * 32, o);
+        tc::wait_ld();
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(dst + c * 32 + i) =
-              make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
-                          __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(dst + c * 32 + i) =
+                make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                            __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+        }
       }
+      tc::fence_before();
+      mbar_arrive(&bars->o_free[wg]);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, kTmemCols);
+  if (warp == 9) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 // ------------------------------------------------------------------ host
@@ -305,16 +387,16 @@ int32_t cuda_status(cudaError_t e, const char* what);
 static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
-    cudaDriverEntryPointQueryResult q;
+    cudaDriverEntryPointQueryResult qr;
     void* p = nullptr;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
-    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p)
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !p)
       return fail(CODEC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     fn = (EncodeTiledFn)p;
   }
   cuuint64_t dims[2] = {(cuuint64_t)kTcD, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kTcD * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, (cuuint32_t)kTcBN};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -323,19 +405,19 @@ static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows)
   return CODEC_OK;
 }
 
-int32_t launch_tc(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q, const void* k,
-                  const void* v, int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
+int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
+                  int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
                   cudaStream_t st) {
-  if (n_groups == 0) return CODEC_OK;
+  if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
   CUtensorMap mk, mv;
   CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens));
   CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens));
   cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   if (e != cudaSuccess) return cuda_status(e, "tc smem attribute");
-  dim3 grid(n_groups, h_local);
-  tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
-                                                   pool_tokens, g, h_local * g, (float*)out, (float*)part_o,
-                                                   (float*)part_ml);
+  dim3 grid(in.n_tc_blocks, h_local);
+  tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
+                                                   (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
+                                                   (float*)out, (float*)part_o, (float*)part_ml);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

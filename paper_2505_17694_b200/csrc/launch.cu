@@ -12,8 +12,8 @@
 #include "device_table.h"
 
 namespace codec {
-int32_t launch_tc(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q, const void* k,
-                  const void* v, int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
+int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
+                  int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
                   cudaStream_t st);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
                     const void* q, const void* k, const void* v, int64_t pool_tokens, int g, int h_local,
@@ -45,8 +45,7 @@ extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_ta
   void* part_o = workspace;
   void* part_ml = static_cast<uint8_t*>(workspace) + o_bytes;
   if (info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC))
-    CODEC_TRY(launch_tc(table_dev, info->n_tc_groups, info->off_tc, info->off_rows, q, k, v, dims->pool_tokens, g,
-                        h_local, out, part_o, part_ml, st));
+    CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));
   if (info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV))
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));

@@ -77,8 +77,9 @@ class DecodeStep:
         self.g = self.h_q // self.h_kv
         self.tdtype = torch_dtype(dtype)
         self.device = torch.device(device)
+        sm = torch.cuda.get_device_properties(self.device).multi_processor_count if torch.cuda.is_available() else 148
         self.dims = _lib.Dims(forest.bs, self.h_q, self.h_kv, self.d, self.head_begin, self.head_end,
-                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1))
+                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1), int(sm), 0)
         t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
         P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
         L = _lib.lib()

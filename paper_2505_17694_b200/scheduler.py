@@ -119,7 +119,7 @@ def tasks_from_forest(forest, head_multiplicity: int = 1) -> list:
             for node in forest.nodes[1:] if node.query_set]
 
 
-def device_tasks(forest, group_size: int, rows_per_tile: int = 128) -> list:
+def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
     """Node tasks split into consecutive query-set chunks of at most
     rows_per_tile // g requests (g = q heads per kv head), n_q counted in
     query-head rows (head_multiplicity = g). Each chunk is what one
