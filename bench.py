@@ -169,6 +169,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--blocks", type=int, default=0, help="planner m (0: SMs // local kv heads)")
     ap.add_argument("--quick", action="store_true", help="profiling run: no e2e / clocks / cpu baseline")
+    ap.add_argument("--serial", action="store_true", help="one stream: TC, GEMV and merge back to back")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -217,7 +218,10 @@ def main():
     plan = P.divide_and_schedule(P.device_tasks(forest, g, rows_per_tile=256), table, m)
     plan_ms = (time.perf_counter() - t0) * 1e3
     step = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
-                      flags=args.flags)
+                      flags=args.flags, concurrent=not args.serial)
+    tune_ms = {}
+    if not args.serial and not args.quick:
+        step, tune_ms = P.autotune_step(step, q_dev, kp, vp)
     out = torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32, device=dev)
     gathered = torch.empty((world, cfg["batch"], hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
 
@@ -272,7 +276,7 @@ def main():
         if not present:
             continue
         ph = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
-                        flags=args.flags | fl)
+                        flags=args.flags | fl, concurrent=False)
         for _ in range(3):
             ph(q_dev, kp, vp, out=out)
         phases[name] = timed(max(5, args.steps // 2), lambda: ph(q_dev, kp, vp, out=out))[0]
@@ -337,7 +341,10 @@ def main():
                        "parallelism": f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else ""),
                        "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
                        "planner": {"m": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,
-                                   "truncated": plan.search_truncated, "ms": plan_ms}},
+                                   "truncated": plan.search_truncated, "ms": plan_ms},
+                       "streams": "serial" if args.serial else "tc || gemv (aux stream)",
+                       "tc_sm_budget": step.tc_sm_budget, "tc_ctas": step.info.n_tc_blocks * h_local,
+                       "autotune_ms": tune_ms},
             "roofline": roof,
             "hbm_roofline_step": {"achieved": value / world, "peak": hbm, "unit": "GB/s",
                                   "frac": value / world / hbm, "frac_of_8tbs": value / world / 8000.0},

@@ -168,7 +168,8 @@ typedef struct {
   int32_t flags;                  /* CODEC_FLAG_* */
   int64_t pool_tokens;            /* T: token stride of one head in the pool */
   int32_t sm_count;               /* SMs of the device (0 = 148); sizes the persistent TC grid */
-  int32_t reserved;
+  int32_t tc_sm_budget;           /* SMs the TC kernel may occupy (0 = all); the rest stay free
+                                     for the GEMV kernel running concurrently on an aux stream */
 } codec_dims;
 
 #define CODEC_FLAG_NO_TC      1   /* never use the tcgen05 shared-node kernel */
@@ -196,6 +197,7 @@ typedef struct {
   int32_t off_merge_req, off_merge_ptr, off_merge_slot;
   int32_t h_local;                                     /* head_end - head_begin */
   int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTAs per head, their group CSR */
+  int32_t max_merge, reserved;                         /* most partials of one merged request */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;
@@ -215,6 +217,13 @@ CODEC_API int32_t codec_table_copy(const codec_table* t, int32_t* blob);
  *   workspace  >= info.workspace_bytes, 256-byte aligned
  * All device pointers; asynchronous on `stream`.
  * ==================================================================== */
+/* Same step with the GEMV / generic kernels forked onto `aux_stream`
+ * (event fork/join on `stream`) so they run concurrently with the
+ * tensor-core kernel; aux_stream NULL == codec_decode_attention. */
+CODEC_API int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
+                                            const int32_t* table_dev, const void* q, const void* k,
+                                            const void* v, void* out, void* workspace, void* stream,
+                                            void* aux_stream);
 CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
                                const int32_t* table_dev, const void* q, const void* k,
                                const void* v, void* out, void* workspace, void* stream);

@@ -63,7 +63,7 @@ class PlanInfo(C.Structure):
 class Dims(C.Structure):
     _fields_ = [("bs", I32), ("h_q", I32), ("h_kv", I32), ("d", I32), ("head_begin", I32),
                 ("head_end", I32), ("kv_dtype", I32), ("flags", I32), ("pool_tokens", I64),
-                ("sm_count", I32), ("reserved", I32)]
+                ("sm_count", I32), ("tc_sm_budget", I32)]
 
 
 class TableInfo(C.Structure):
@@ -72,6 +72,7 @@ class TableInfo(C.Structure):
                 ("off_tc", I32), ("off_gemv", I32), ("off_gen", I32), ("off_rows", I32),
                 ("off_merge_req", I32), ("off_merge_ptr", I32), ("off_merge_slot", I32),
                 ("h_local", I32), ("n_tc_blocks", I32), ("off_tc_block_ptr", I32),
+                ("max_merge", I32), ("reserved", I32),
                 ("blob_len", I64), ("workspace_bytes", I64)]
 
 
@@ -97,6 +98,7 @@ _SIGS = {
     "codec_table_info_get": (I32, [P, C.POINTER(TableInfo)]),
     "codec_table_copy": (I32, [P, PI32]),
     "codec_decode_attention": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P]),
+    "codec_decode_attention_ex": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P, P]),
     "codec_pac": (I32, [I32, P, P, P, P, I64, I64, I64, I64, I64, F64, P, P, P, P]),
     "codec_por": (I32, [I32, I64, I64, P, P, P, P, P, P, P, P, P, P]),
     "codec_pool_pack": (I32, [I32, P, I64, I64, I64, I32, I32, P, I64, I64, P]),

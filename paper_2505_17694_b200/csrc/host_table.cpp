@@ -216,7 +216,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   }
   // ---- slots: direct output for single-partial requests, else merged
   std::vector<int32_t> merge_req, merge_ptr{0}, merge_slot;
-  int32_t n_slots = 0;
+  int32_t n_slots = 0, max_merge = 0;
   for (int32_t r = 0; r < bs; ++r) {
     auto& u = req_units[r];
     if (u.empty()) return fail(CODEC_ERR_NO_VISIBLE_TOKENS, "request %d has no visible tokens anywhere on its path", r);
@@ -226,6 +226,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       continue;
     }
     merge_req.push_back(r);
+    max_merge = std::max<int32_t>(max_merge, (int32_t)u.size());
     for (auto& e : u) {
       rows[4 * e[2] + 2] = n_slots;
       merge_slot.push_back(n_slots++);
@@ -242,6 +243,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   auto t = new codec_table();
   codec_table_info& in = t->info;
   in.h_local = dims->head_end - dims->head_begin;
+  in.max_merge = max_merge;
   in.gemv_rows = gemv_rows;
   std::vector<int32_t>& blob = t->blob;
   auto emit_groups = [&](int kind, int32_t& count, int32_t& offset) {
@@ -262,7 +264,8 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     std::vector<Grp> tcg;
     for (auto& gr : groups)
       if (gr.kind == kKindTc) tcg.push_back(gr);
-    const int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
+    int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
+    if (dims->tc_sm_budget > 0) sms = std::min(sms, dims->tc_sm_budget);
     const int32_t h_local = dims->head_end - dims->head_begin;
     int32_t m_tc = std::max(1, sms / h_local);
     m_tc = std::min<int32_t>(m_tc, (int32_t)tcg.size());

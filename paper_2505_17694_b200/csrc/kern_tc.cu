@@ -24,11 +24,14 @@
 // commit behind S_i(t) guarantees PV_i(t-1) landed before softmax i reads
 // or rescales O_i.
 //
-// Warp roles (320 threads): warps 0-3 softmax of Q0, 4-7 softmax of Q1,
-// warp 8 TMA producer (K/V 2-stage rings of 128x64 SWIZZLE_128B boxes),
-// warp 9 TMEM allocator + single-thread MMA issuer. Softmax: packed f32x2
-// math, exponentials split between MUFU.EX2 and a degree-3 polynomial on
-// the FMA pipe, lazy O rescale (only when a row max grows by > 2^8),
+// Warp roles (576 threads): 16 softmax warps -- (Q tile, column half, TMEM
+// lane quadrant); a row's two 64-column halves exchange their max through
+// SMEM -- warp 16 TMA producer (K/V 2-stage rings of 128x64 SWIZZLE_128B
+// boxes), warp 17 TMEM allocator + single-thread MMA issuer. Two warps per
+// row keep two independent instruction streams per scheduler, which the
+// latency-bound exponential loop needs. Softmax: packed f32x2 math,
+// exponentials split between MUFU.EX2 (5/8) and a degree-3 polynomial on
+// the FMA pipe (3/8), lazy O rescale (only when a row max grows by > 2^8),
 // masking only on a row's last tile.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -40,24 +43,33 @@
 
 namespace codec {
 
-constexpr int kTcThreads = 320;
+constexpr int kTcSoftmaxWarps = 16;         // 2 Q tiles x 4 lane quadrants x 2 column halves
+constexpr int kTcProducerWarp = kTcSoftmaxWarps;
+constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
+constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 2);
 constexpr int kTcBN = 128;                      // tokens per KV tile
 constexpr int kTcD = 128;                       // head dim
-constexpr int kTcStages = 2;                    // K and V ring depth
+constexpr int kTcKStages = 3;                   // K ring depth (K is needed one MMA earlier than V)
+constexpr int kTcVStages = 2;                   // V ring depth
+constexpr int kTcPrefetch = 3;                  // tiles ahead the producer warms L2
 constexpr int kTileBytes = 128 * 128 * 2;       // 32 KB: one 128x128 bf16 tile (Q, K or V)
 constexpr int kAtomBytes = kTileBytes / 2;      // 64-element-wide SW128 atom column
 constexpr int kOffQ = 0;                                 // Q0, Q1
 constexpr int kOffK = kOffQ + 2 * kTileBytes;            // K ring
-constexpr int kOffV = kOffK + kTcStages * kTileBytes;    // V ring
-constexpr int kOffBar = kOffV + kTcStages * kTileBytes;
-constexpr int kTcSmem = kOffBar + 512 + 1024;            // barriers + alignment slack
+constexpr int kOffV = kOffK + kTcKStages * kTileBytes;   // V ring
+constexpr int kOffXch = kOffV + kTcVStages * kTileBytes; // row-max / row-sum exchange [2][2][128] f32
+constexpr int kOffBar = kOffXch + 2 * 2 * 128 * 4;
+// No alignment slack: the dynamic SMEM window starts 1024-aligned (behind the
+// driver's 1 KB reservation) and the kernel traps if it ever does not.
+constexpr int kTcSmem = kOffBar + 256;
+static_assert(kTcSmem <= 232448, "exceeds the 227 KB opt-in shared memory");
 constexpr uint32_t kTmemCols = 512;  // S0/P0 [0,128) S1/P1 [128,256) O0 [256,384) O1 [384,512)
 constexpr float kRescaleLog2 = 8.f;
 
 struct TcBars {
   uint64_t q_full;
-  uint64_t k_full[kTcStages], k_empty[kTcStages];
-  uint64_t v_full[kTcStages], v_empty[kTcStages];
+  uint64_t k_full[kTcKStages], k_empty[kTcKStages];
+  uint64_t v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
   uint32_t tmem_slot;
 };
@@ -78,6 +90,22 @@ __device__ __forceinline__ float poly_exp2(float x) {
   p = fmaf(p, f, 0.69326099f);
   p = fmaf(p, f, 0.99992808f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Two lanes of the same polynomial with packed f32x2 arithmetic
+// (FADD2/FFMA2): ~5 issue slots per exponential instead of ~8.
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = tc::fadd2(x, magic);
+  const float2 xi = tc::fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = tc::fadd2(x, make_float2(-xi.x, -xi.y));
+  float2 p = tc::ffma2(make_float2(0.05517153f, 0.05517153f), f, make_float2(0.24261101f, 0.24261101f));
+  p = tc::ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
+  p = tc::ffma2(p, f, make_float2(0.99992808f, 0.99992808f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -107,10 +135,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml) {
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw_u32 = smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + (((raw_u32 + 1023) & ~1023u) - raw_u32);
+  extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
+  if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
   TcBars* bars = reinterpret_cast<TcBars*>(smem + kOffBar);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -118,23 +145,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int g_begin = table[off_block_ptr + blk], g_end = table[off_block_ptr + blk + 1];
 
   if (tid == 0) {
-    mbar_init(&bars->q_full, 256);
-    for (int s = 0; s < kTcStages; ++s) {
+    mbar_init(&bars->q_full, 32 * kTcSoftmaxWarps);
+    for (int s = 0; s < kTcKStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->k_empty[s], 1);
+    }
+    for (int s = 0; s < kTcVStages; ++s) {
       mbar_init(&bars->v_full[s], 1);
       mbar_init(&bars->v_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->p_full[i], 128);
+      mbar_init(&bars->p_full[i], 256);
       mbar_init(&bars->o_done[i], 1);
-      mbar_init(&bars->o_free[i], 128);
+      mbar_init(&bars->o_free[i], 256);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
-  if (warp == 8 && lane == 0) {
+  if (warp == kTcMmaWarp) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
+  if (warp == kTcProducerWarp && lane == 0) {
     tc::prefetch_tmap(&tmk);
     tc::prefetch_tmap(&tmv);
   }
@@ -143,97 +172,137 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
 
-  if (warp == 8) {
-    // ================================================ TMA producer
-    if (lane == 0) {
-      int t = 0;  // global KV tile counter (ring position)
-      for (int gi = g_begin; gi < g_end; ++gi) {
-        const GroupView gv = group_view(table, off_groups, off_rows, gi);
-        const int row0 = kh * (int)pool_tokens + gv.kv_tok;
-        for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-          const int s = t % kTcStages;
-          const int y = row0 + j * kTcBN;
-          if (t >= kTcStages) mbar_wait(&bars->k_empty[s], ((t / kTcStages) - 1) & 1);
-          mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
-          uint8_t* kd = smem + kOffK + s * kTileBytes;
-          tc::tma_load_2d(kd, &tmk, 0, y, &bars->k_full[s]);
-          tc::tma_load_2d(kd + kAtomBytes, &tmk, 64, y, &bars->k_full[s]);
-          if (t >= kTcStages) mbar_wait(&bars->v_empty[s], ((t / kTcStages) - 1) & 1);
-          mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
-          uint8_t* vd = smem + kOffV + s * kTileBytes;
-          tc::tma_load_2d(vd, &tmv, 0, y, &bars->v_full[s]);
-          tc::tma_load_2d(vd + kAtomBytes, &tmv, 64, y, &bars->v_full[s]);
+  if (warp == kTcProducerWarp) {
+    // ================================================ TMA producer (whole warp, one lane issues)
+    int t = 0;  // global KV tile counter (ring position)
+    for (int gi = g_begin; gi < g_end; ++gi) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      const int row0 = kh * (int)pool_tokens + gv.kv_tok;
+      if (tc::elect_one()) {  // warm L2 with the group's first tiles
+        for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
+          tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN);
+          tc::tma_prefetch_2d(&tmk, 64, row0 + j * kTcBN);
+          tc::tma_prefetch_2d(&tmv, 0, row0 + j * kTcBN);
+          tc::tma_prefetch_2d(&tmv, 64, row0 + j * kTcBN);
         }
       }
+      __syncwarp();
+      for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+        const int ks = t % kTcKStages, vs = t % kTcVStages;
+        const int y = row0 + j * kTcBN;
+        if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
+        if (tc::elect_one()) {
+          mbar_arrive_expect_tx(&bars->k_full[ks], kTileBytes);
+          uint8_t* kd = smem + kOffK + ks * kTileBytes;
+          tc::tma_load_2d(kd, &tmk, 0, y, &bars->k_full[ks]);
+          tc::tma_load_2d(kd + kAtomBytes, &tmk, 64, y, &bars->k_full[ks]);
+          if (j + kTcPrefetch < gv.n_tiles) {
+            const int yp = y + kTcPrefetch * kTcBN;
+            tc::tma_prefetch_2d(&tmk, 0, yp);
+            tc::tma_prefetch_2d(&tmk, 64, yp);
+            tc::tma_prefetch_2d(&tmv, 0, yp);
+            tc::tma_prefetch_2d(&tmv, 64, yp);
+          }
+        }
+        __syncwarp();
+        if (t >= kTcVStages) mbar_wait(&bars->v_empty[vs], ((t / kTcVStages) - 1) & 1);
+        if (tc::elect_one()) {
+          mbar_arrive_expect_tx(&bars->v_full[vs], kTileBytes);
+          uint8_t* vd = smem + kOffV + vs * kTileBytes;
+          tc::tma_load_2d(vd, &tmv, 0, y, &bars->v_full[vs]);
+          tc::tma_load_2d(vd + kAtomBytes, &tmv, 64, y, &bars->v_full[vs]);
+        }
+        __syncwarp();
+      }
     }
-  } else if (warp == 9) {
+  } else if (warp == kTcMmaWarp) {
     // ================================================ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = tc::idesc_bf16(128, kTcBN, false, false);
-      constexpr uint32_t idesc_o = tc::idesc_bf16(128, kTcD, false, true);
-      int t = 0;  // global tile counter
-      int gq = 0;
-      auto issue_s = [&](int i, int tt) {
-        const int s = tt % kTcStages;
-        const uint32_t k_addr = sbase + kOffK + s * kTileBytes;
-        const uint32_t q_addr = sbase + kOffQ + i * kTileBytes;
+    // The whole warp runs the (warp-uniform) schedule so the descriptors stay
+    // in uniform registers; one elected lane issues each batch of MMAs.
+    // Descriptors are a base plus a compile-time start-address offset
+    // (the low 14 bits hold addr >> 4).
+    constexpr uint32_t idesc_s = tc::idesc_bf16(128, kTcBN, false, false);
+    constexpr uint32_t idesc_o = tc::idesc_bf16(128, kTcD, false, true);
+    const uint64_t dq = tc::smem_desc(sbase + kOffQ, 16, 1024);
+    const uint64_t dk = tc::smem_desc(sbase + kOffK, 16, 1024);
+    const uint64_t dv = tc::smem_desc(sbase + kOffV, kAtomBytes, 1024);
+    int t = 0;  // global tile counter
+    int gq = 0;
+    auto issue_s = [&](int i, int tt) {
+      const int s = tt % kTcKStages;
+      const uint64_t aq = dq + (uint64_t)((i * kTileBytes) >> 4);
+      const uint64_t bk = dk + (uint64_t)((s * kTileBytes) >> 4);
+      if (tc::elect_one()) {
 #pragma unroll
         for (int k = 0; k < kTcD / 16; ++k) {
-          const uint32_t off = (k >> 2) * kAtomBytes + (k & 3) * 32;
-          tc::mma_f16_ss(tmem + i * 128, tc::smem_desc(q_addr + off, 16, 1024), tc::smem_desc(k_addr + off, 16, 1024),
-                         idesc_s, k > 0 ? 1u : 0u);
+          const uint64_t off = (uint64_t)((((k >> 2) * kAtomBytes) + (k & 3) * 32) >> 4);
+          tc::mma_f16_ss(tmem + i * 128, aq + off, bk + off, idesc_s, k > 0 ? 1u : 0u);
         }
         tc::commit(&bars->s_full[i]);
         if (i == 1) tc::commit(&bars->k_empty[s]);
-      };
-      for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
-        const GroupView gv = group_view(table, off_groups, off_rows, gi);
-        if (gv.n_tiles == 0) {  // (cannot happen: every row sees >= 1 token) keep gq in step
-          --gq;
-          continue;
-        }
-        mbar_wait(&bars->q_full, gq & 1);
-        {
-          const int s = t % kTcStages;
-          mbar_wait(&bars->k_full[s], (t / kTcStages) & 1);
+      }
+      __syncwarp();
+    };
+    for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      if (gv.n_tiles == 0) {  // (cannot happen: every row sees >= 1 token) keep gq in step
+        --gq;
+        continue;
+      }
+      mbar_wait(&bars->q_full, gq & 1);
+      {
+        const int s = t % kTcKStages;
+        mbar_wait(&bars->k_full[s], (t / kTcKStages) & 1);
+        tc::fence_after();
+        issue_s(0, t);
+        issue_s(1, t);
+      }
+      for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+        const int s = t % kTcVStages;
+        const bool more = j + 1 < gv.n_tiles;
+        mbar_wait(&bars->v_full[s], (t / kTcVStages) & 1);
+        if (more) mbar_wait(&bars->k_full[(t + 1) % kTcKStages], ((t + 1) / kTcKStages) & 1);
+        const uint64_t bv = dv + (uint64_t)((s * kTileBytes) >> 4);
+        for (int i = 0; i < 2; ++i) {
+          mbar_wait(&bars->p_full[i], t & 1);                        // P_i(t) in TMEM
+          if (j == 0 && gq > 0) mbar_wait(&bars->o_free[i], (gq - 1) & 1);  // epilogue read O_i
           tc::fence_after();
-          issue_s(0, t);
-          issue_s(1, t);
-        }
-        for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-          const int s = t % kTcStages;
-          const bool more = j + 1 < gv.n_tiles;
-          mbar_wait(&bars->v_full[s], (t / kTcStages) & 1);
-          if (more) mbar_wait(&bars->k_full[(t + 1) % kTcStages], ((t + 1) / kTcStages) & 1);
-          const uint32_t v_addr = sbase + kOffV + s * kTileBytes;
-          for (int i = 0; i < 2; ++i) {
-            mbar_wait(&bars->p_full[i], t & 1);                        // P_i(t) in TMEM
-            if (j == 0 && gq > 0) mbar_wait(&bars->o_free[i], (gq - 1) & 1);  // epilogue read O_i
-            tc::fence_after();
-            const uint32_t p_tmem = tmem + i * 128;
-            const uint32_t o_tmem = tmem + 256 + i * 128;
+          const uint32_t p_tmem = tmem + i * 128;
+          const uint32_t o_tmem = tmem + 256 + i * 128;
+          if (tc::elect_one()) {
 #pragma unroll
             for (int k = 0; k < kTcBN / 16; ++k)
-              tc::mma_f16_ts(o_tmem, p_tmem + k * 8, tc::smem_desc(v_addr + k * 16 * 128, kAtomBytes, 1024),
+              // tokens [16k, 16k+16) of P: columns 64*(k/4) + 8*(k%4) (each
+              // column-half of the softmax packs its P over its own S columns)
+              tc::mma_f16_ts(o_tmem, p_tmem + (k >> 2) * 64 + (k & 3) * 8, bv + (uint64_t)((k * 16 * 128) >> 4),
                              idesc_o, (j > 0 || k > 0) ? 1u : 0u);
             if (i == 1) tc::commit(&bars->v_empty[s]);
-            if (more) {
-              issue_s(i, t + 1);
-            } else {
-              tc::commit(&bars->o_done[i]);
-            }
+            if (!more) tc::commit(&bars->o_done[i]);
           }
+          __syncwarp();
+          if (more) issue_s(i, t + 1);
         }
       }
     }
   } else {
-    // ================================================ softmax warpgroups
-    const int wg = warp >> 2;                 // Q tile
+    // ================================================ softmax warps
+    // warp = (Q tile wg, column half hf, lane quadrant quad); thread = one
+    // row of the Q tile (TMEM lane) over 64 of the tile's 128 columns. The
+    // two halves of a row meet through SMEM for the row max (named barrier
+    // per (wg, quad) pair) and, at the end of a group, for the row sum.
+    const int wg = warp >> 3;                 // Q tile
+    const int hf = (warp >> 2) & 1;           // column half
     const int quad = warp & 3;                // TMEM lane quadrant
     const int r = quad * 32 + lane;           // row in the Q tile == TMEM lane
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const uint32_t s_tmem = tmem + wg * 128 + lane_addr;
-    const uint32_t o_tmem = tmem + 256 + wg * 128 + lane_addr;
+    const uint32_t o_tmem = tmem + 256 + wg * 128 + lane_addr + hf * 64;
+    const uint32_t bar_id = 1 + wg * 4 + quad;  // pairs the two half-warps of these rows
+    // [wg][hf][128]; single-buffered: a pair barrier before every write keeps
+    // the partner's previous read ahead of the overwrite
+    float* xch = reinterpret_cast<float*>(smem + kOffXch);
+    auto xch_at = [&](int h) -> float* { return xch + (wg * 2 + h) * 128 + r; };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     const float cscale = 1.4426950408889634f * rsqrtf((float)kTcD);
     const float2 c2 = make_float2(cscale, cscale);
     int t = 0, gq = 0;
@@ -250,43 +319,46 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int vis = valid ? gv.rows[ridx * kRowInts + 1] : 0;
       const int slot = valid ? gv.rows[ridx * kRowInts + 2] : 0;
       const int qh = kh * g + (grow % g);
-      {  // stage my Q row (K-major SW128); the previous group's S MMAs are complete
+      {  // stage my half of the Q row (K-major SW128); the previous group's S MMAs are complete
         uint8_t* qs = smem + kOffQ + wg * kTileBytes;
         const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = hf * 8; c < hf * 8 + 8; ++c) {
           const uint4 v = valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(qs + sw128(r, c)) = v;
         }
         tc::fence_proxy_async_smem();
         mbar_arrive(&bars->q_full);
       }
-      float m_used = 0.f;  // exponent reference (log2 units)
+      float m_used = 0.f;  // exponent reference (log2 units), same in both halves
       float2 l2 = make_float2(0.f, 0.f);
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
         mbar_wait(&bars->s_full[wg], t & 1);   // also: PV_wg(t-1) has landed (commit order)
         tc::fence_after();
-        const int lim = vis - j * kTcBN;
-        const bool full = __all_sync(0xffffffffu, !valid || lim >= kTcBN);
-        // pass 1: row max over the tile, 32 columns at a time (next load in flight)
-        uint32_t sa[32], sb[32];
+        const int lim = vis - j * kTcBN - hf * 64;  // visible columns of my half
+        const bool full = __all_sync(0xffffffffu, !valid || lim >= 64);
+        const uint32_t my_s = s_tmem + hf * 64;
+        // pass 1: max over my 64 columns
         float mx = neg_inf<float>();
-        tc::tmem_ld32(s_tmem, sa);
-        tc::wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t* cur = (c & 1) ? sb : sa;
-          uint32_t* nxt = (c & 1) ? sa : sb;
-          if (c + 1 < 4) tc::tmem_ld32(s_tmem + (c + 1) * 32, nxt);
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32];
+          tc::tmem_ld32(my_s + c * 32, sr);
+          tc::wait_ld();
           if (!full) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= lim) cur[i] = 0xff800000u;  // -inf
+              if (c * 32 + i >= lim) sr[i] = 0xff800000u;  // -inf
           }
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])));
-          tc::wait_ld();
+          for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
         }
+        // meet the other half of the row (each half only ever writes P into
+        // its own S columns, so no ordering beyond this exchange is needed)
+        pair_sync();
+        *xch_at(hf) = mx;
+        pair_sync();
+        mx = fmaxf(mx, *xch_at(hf ^ 1));
         const float mt = valid ? mx * cscale : 0.f;
         if (j == 0) {
           m_used = mt;
@@ -297,66 +369,78 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             l2.x *= alpha;
             l2.y *= alpha;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              tc::tmem_ld32(o_tmem + c * 32, sa);
+            for (int c = 0; c < 2; ++c) {
+              uint32_t o[32];
+              tc::tmem_ld32(o_tmem + c * 32, o);
               tc::wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) sa[i] = __float_as_uint(__uint_as_float(sa[i]) * alpha);
-              tc::tmem_st32(o_tmem + c * 32, sa);
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tc::tmem_st32(o_tmem + c * 32, o);
             }
             if (need) m_used = mt;
           }
         }
-        // pass 2: P = 2^(S c - m) as bf16 pairs; chunk c (S columns 32c..32c+31)
-        // lands in P columns 16c..16c+15, i.e. over S columns already consumed
+        // pass 2: P = 2^(S c - m) as bf16 pairs; S columns 64hf + [32c, 32c+32)
+        // -> P columns 64hf + [16c, 16c+16), i.e. over my own consumed S
         const float2 nm = make_float2(-m_used, -m_used);
-        tc::tmem_ld32(s_tmem, sa);
-        tc::wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t* cur = (c & 1) ? sb : sa;
-          uint32_t* nxt = (c & 1) ? sa : sb;
-          if (c + 1 < 4) tc::tmem_ld32(s_tmem + (c + 1) * 32, nxt);
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32];
+          tc::tmem_ld32(my_s + c * 32, sr);
+          tc::wait_ld();
           if (!full) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= lim) cur[i] = 0xff800000u;
+              if (c * 32 + i >= lim) sr[i] = 0xff800000u;
           }
           uint32_t pw[16];
 #pragma unroll
-          for (int w = 0; w < 16; ++w) {
-            const float2 x = tc::ffma2(make_float2(__uint_as_float(cur[2 * w]), __uint_as_float(cur[2 * w + 1])), c2, nm);
-            float2 p;
-            p.x = fast_exp2(x.x);  // MUFU
-            p.y = poly_exp2(x.y);  // FMA pipe
-            l2 = tc::fadd2(l2, p);
-            pw[w] = pack_bf16(p.x, p.y);
+          for (int w = 0; w < 16; w += 4) {
+            // 8 scores: 5 exponentials on the MUFU, 3 on the FMA pipe (a packed pair + 1)
+            float2 x[4], p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              x[k] = tc::ffma2(make_float2(__uint_as_float(sr[2 * (w + k)]), __uint_as_float(sr[2 * (w + k) + 1])),
+                               c2, nm);
+            const float2 py = poly_exp2x2(make_float2(x[2].y, x[3].y));
+            p[0] = make_float2(fast_exp2(x[0].x), fast_exp2(x[0].y));
+            p[1] = make_float2(fast_exp2(x[1].x), poly_exp2(x[1].y));
+            p[2] = make_float2(fast_exp2(x[2].x), py.x);
+            p[3] = make_float2(fast_exp2(x[3].x), py.y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              l2 = tc::fadd2(l2, p[k]);
+              pw[w + k] = pack_bf16(p[k].x, p[k].y);
+            }
           }
-          tc::wait_ld();  // the next chunk's load must land before its columns are overwritten
-          tc::tmem_st16(s_tmem + c * 16, pw);
+          tc::tmem_st16(my_s + c * 16, pw);
         }
         tc::wait_st();
         tc::fence_before();
         mbar_arrive(&bars->p_full[wg]);
       }
       // ---- epilogue: O / l once the group's last PV landed
-      const float l_run = l2.x + l2.y;
+      float l_run = l2.x + l2.y;
+      pair_sync();
+      *xch_at(hf) = l_run;
+      pair_sync();
+      l_run += *xch_at(hf ^ 1);
       mbar_wait(&bars->o_done[wg], gq & 1);
       tc::fence_after();
       float* dst;
       if (slot < 0) {
-        dst = out + ((int64_t)req * hq_local + qh) * kTcD;
+        dst = out + ((int64_t)req * hq_local + qh) * kTcD + hf * 64;
       } else {
         const int64_t ei = (int64_t)slot * hq_local + qh;
-        dst = part_o + ei * kTcD;
-        if (valid) {
+        dst = part_o + ei * kTcD + hf * 64;
+        if (valid && hf == 0) {
           part_ml[2 * ei] = m_used * 0.69314718055994530942f;  // natural-log units
           part_ml[2 * ei + 1] = l_run;
         }
       }
       const float inv = 1.f / l_run;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t o[32];
         tc::tmem_ld32(o_tmem + c * 32, o);
         tc::wait_ld();
@@ -374,7 +458,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 9) tc::tmem_dealloc(tmem, kTmemCols);
+  if (warp == kTcMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
 // ------------------------------------------------------------------ host

@@ -23,13 +23,37 @@ int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st);
+int32_t cuda_status(cudaError_t e, const char* what);
 }  // namespace codec
 
 using namespace codec;
 
-extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
-                                          const int32_t* table_dev, const void* q, const void* k, const void* v,
-                                          void* out, void* workspace, void* stream) {
+namespace {
+// Per-thread, per-device fork/join events for the aux-stream variant.
+struct ForkJoin {
+  int device = -1;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+int32_t fork_join_events(ForkJoin*& out) {
+  thread_local ForkJoin slots[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return codec::cuda_status(e, "cudaGetDevice");
+  ForkJoin& fj = slots[dev & 15];
+  if (fj.device != dev) {
+    if (cudaEventCreateWithFlags(&fj.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&fj.join, cudaEventDisableTiming) != cudaSuccess)
+      return codec::fail(CODEC_ERR_CUDA, "event creation failed");
+    fj.device = dev;
+  }
+  out = &fj;
+  return CODEC_OK;
+}
+}  // namespace
+
+extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
+                                             const int32_t* table_dev, const void* q, const void* k, const void* v,
+                                             void* out, void* workspace, void* stream, void* aux_stream) {
   if (!dims || !info || !table_dev) return fail(CODEC_ERR_VALUE, "NULL argument");
   if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
     return fail(CODEC_ERR_VALUE, "workspace must be 256-byte aligned");
@@ -44,15 +68,35 @@ extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_ta
   o_bytes = (o_bytes + 255) / 256 * 256;
   void* part_o = workspace;
   void* part_ml = static_cast<uint8_t*>(workspace) + o_bytes;
-  if (info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC))
-    CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));
-  if (info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV))
+  const bool do_tc = info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC);
+  const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
+  const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
+  const bool fork = aux_stream != nullptr && do_tc && (do_gemv || do_gen);
+  cudaStream_t side = fork ? (cudaStream_t)aux_stream : st;
+  ForkJoin* fj = nullptr;
+  if (fork) {
+    CODEC_TRY(fork_join_events(fj));
+    if (cudaEventRecord(fj->fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fj->fork, 0) != cudaSuccess)
+      return fail(CODEC_ERR_CUDA, "fork failed");
+  }
+  if (do_tc) CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));
+  if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
-                          info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));
-  if (info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC))
+                          info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side));
+  if (do_gen)
     CODEC_TRY(launch_generic_groups(dims->kv_dtype, table_dev, info->n_gen_groups, info->off_gen, info->off_rows, q,
-                                    k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, st));
+                                    k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, side));
+  if (fork) {
+    if (cudaEventRecord(fj->join, side) != cudaSuccess || cudaStreamWaitEvent(st, fj->join, 0) != cudaSuccess)
+      return fail(CODEC_ERR_CUDA, "join failed");
+  }
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st));
   return CODEC_OK;
+}
+
+extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
+                                          const int32_t* table_dev, const void* q, const void* k, const void* v,
+                                          void* out, void* workspace, void* stream) {
+  return codec_decode_attention_ex(dims, info, table_dev, q, k, v, out, workspace, stream, nullptr);
 }

@@ -67,7 +67,7 @@ class DecodeStep:
     float64 inputs)."""
 
     def __init__(self, forest: Forest, plan, h_q: int, dtype="bfloat16", head_begin=0, head_end=None,
-                 device="cuda", flags=0):
+                 device="cuda", flags=0, tc_sm_budget=0, concurrent=True):
         import torch
 
         self.forest = forest
@@ -78,8 +78,13 @@ class DecodeStep:
         self.tdtype = torch_dtype(dtype)
         self.device = torch.device(device)
         sm = torch.cuda.get_device_properties(self.device).multi_processor_count if torch.cuda.is_available() else 148
+        self.plan, self.flags, self.tc_sm_budget = plan, int(flags), int(tc_sm_budget)
         self.dims = _lib.Dims(forest.bs, self.h_q, self.h_kv, self.d, self.head_begin, self.head_end,
-                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1), int(sm), 0)
+                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1), int(sm),
+                              int(tc_sm_budget))
+        # GEMV/generic kernels run on an aux stream, concurrently with the
+        # tensor-core kernel (event fork/join inside the library)
+        self.aux = torch.cuda.Stream(self.device) if concurrent and torch.cuda.is_available() else None
         t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
         P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
         L = _lib.lib()
@@ -113,11 +118,51 @@ class DecodeStep:
         if out is None:
             out = torch.empty((self.forest.bs, self.hq_local, self.d), dtype=self.out_dtype, device=self.device)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _lib.check(_lib.lib().codec_decode_attention(
+        _lib.check(_lib.lib().codec_decode_attention_ex(
             C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
             C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(out.data_ptr()),
-            C.c_void_p(self.workspace.data_ptr()), C.c_void_p(st.cuda_stream)))
+            C.c_void_p(self.workspace.data_ptr()), C.c_void_p(st.cuda_stream),
+            C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None))
         return out
+
+    def with_budget(self, tc_sm_budget: int) -> "DecodeStep":
+        return DecodeStep(self.forest, self.plan, self.h_q, self.tdtype, self.head_begin, self.head_end,
+                          self.device, self.flags, tc_sm_budget, self.aux is not None)
+
+
+def autotune_step(step: DecodeStep, q, k_pool, v_pool, budgets=None, iters=10):
+    """Pick the tensor-core SM budget (the SMs left to the concurrent GEMV
+    kernel) by timing one decode step per candidate with CUDA events --
+    done once per plan, like a cuDNN benchmark-mode choice. Returns
+    (best_step, {budget: ms})."""
+    import torch
+
+    if step.info.n_tc_groups == 0 or step.info.n_gemv_groups == 0:
+        return step, {}
+    sms = step.dims.sm_count
+    h_local = step.head_end - step.head_begin
+    budgets = budgets or sorted({sms, int(sms * 0.9), int(sms * 0.8), int(sms * 0.7), int(sms * 0.6)}, reverse=True)
+    out = torch.empty((step.forest.bs, step.hq_local, step.d), dtype=step.out_dtype, device=step.device)
+    times = {}
+    best, best_ms = step, None
+    for b in budgets:
+        if b < h_local:
+            continue
+        cand = step.with_budget(b)
+        for _ in range(3):
+            cand(q, k_pool, v_pool, out=out)
+        torch.cuda.synchronize(step.device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            cand(q, k_pool, v_pool, out=out)
+        e1.record()
+        torch.cuda.synchronize(step.device)
+        ms = e0.elapsed_time(e1) / iters
+        times[b] = ms
+        if best_ms is None or ms < best_ms:
+            best, best_ms = cand, ms
+    return best, times
 
 
 def execute(forest: Forest, queries: QueryBatch, plan, pool: BlockPool | None = None, trace=None,

@@ -270,3 +270,23 @@ class TestBf16Kernels:
         plan = P.plan_uniform_bk(P.tasks_from_forest(donor), table, 1, 2)
         with pytest.raises(PlanForestMismatch, match="do not tile"):
             P.execute(target, q, plan)
+
+
+class TestConcurrency:
+    def test_aux_stream_and_budgets_bitwise_equal(self, cuda_ok, table):
+        """TC on the main stream || GEMV on the aux stream, and different TC
+        SM budgets, change scheduling only -- results are bit-identical."""
+        spec = W.two_level(2048, 200, 96, h_q=32, h_kv=8, d=128, seed=4)
+        f, q = build(spec, "bfloat16")
+        plan = P.divide_and_schedule(P.device_tasks(f, group_size=4), table, 37)
+        kp, vp = f.device_pool("bfloat16")
+        qd = q.queries.cuda()
+        serial = DecodeStep(f, plan, 32, "bfloat16", concurrent=False)
+        base = np_(serial(qd, kp, vp))
+        for budget in (0, 120, 64):
+            conc = DecodeStep(f, plan, 32, "bfloat16", concurrent=True, tc_sm_budget=budget)
+            assert np.array_equal(np_(conc(qd, kp, vp)), base)
+        best, times = P.autotune_step(DecodeStep(f, plan, 32, "bfloat16"), qd, kp, vp, budgets=[148, 96], iters=2)
+        assert np.array_equal(np_(best(qd, kp, vp)), base)
+        ups = upcast_spec(spec)
+        assert_bf16_close(base, OA.naive_attention(ups.queries, oracle_forest(ups)))
