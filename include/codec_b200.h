@@ -180,6 +180,7 @@ typedef struct {
 #define CODEC_FLAG_SKIP_TC      16
 #define CODEC_FLAG_SKIP_GEMV    32
 #define CODEC_FLAG_SKIP_MERGE   64
+#define CODEC_FLAG_TRACE        128  /* record a clock64 timeline of TC CTA (0,0) (debug) */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
@@ -227,6 +228,12 @@ CODEC_API int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_
 CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
                                const int32_t* table_dev, const void* q, const void* k,
                                const void* v, void* out, void* workspace, void* stream);
+
+/* Copy the TC timeline recorded under CODEC_FLAG_TRACE: n <= 640 clock64
+ * values, trace[(event * 2 + q_tile) * 64 + tile], events: 0 MMA saw P,
+ * 1 MMA issued PV+next S, 2 softmax saw S, 3 softmax released P, 4 softmax
+ * finished the row-max exchange. Debug only. */
+CODEC_API int32_t codec_debug_trace(long long* host, int64_t n);
 
 /* ======================================================================
  * Device primitives with the reference's argument meaning.

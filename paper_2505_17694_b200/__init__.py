@@ -18,7 +18,7 @@ from .forest import (Forest, KvNode, QueryBatch, Violation, build_forest, forest
                      prefix_path, validate)
 from .metrics import TrafficReport, count_kv_reads, device_work, traffic_report, weighted_avg_sharing
 from .scheduler import (Assignment, DivisionPlan, Subtask, Task, canonical_division, device_tasks,
-                        divide_and_schedule, division_caps, greedy_assign, lower_bound, makespan,
+                        concat_plans, divide_and_schedule, division_caps, greedy_assign, lower_bound, makespan, plan_device,
                         plan_uniform_bk, slice_ranges, tasks_from_forest)
 
 __version__ = "0.1.0"

@@ -321,7 +321,9 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   const int64_t hq_local = (int64_t)in.h_local * g;
   int64_t o_bytes = (int64_t)n_slots * hq_local * d * elem;
   o_bytes = (o_bytes + 255) / 256 * 256;
-  in.workspace_bytes = o_bytes + (int64_t)n_slots * hq_local * 2 * elem + 256;
+  // partial outputs, partial (m, l), then 256 reserved bytes
+  int64_t ml_bytes = ((int64_t)n_slots * hq_local * 2 * elem + 255) / 256 * 256;
+  in.workspace_bytes = o_bytes + ml_bytes + 256;
   *out = t;
   return CODEC_OK;
 }

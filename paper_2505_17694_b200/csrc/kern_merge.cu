@@ -60,47 +60,53 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
   }
 }
 
-// d = 128, fp32 partials, <= 4 partials per request: every load of the
-// warp is issued before any math (float4 per lane), so one memory latency
-// covers the whole merge instead of one per partial.
+// d = 128, fp32 partials, <= 16 partials per request: the (m, l) pairs are
+// loaded first, then the output vectors four partials at a time with all
+// four loads in flight (float4 per lane), so the merge costs a few memory
+// latencies instead of one per partial.
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int hq_local,
                                                        const float* __restrict__ part_o,
                                                        const float* __restrict__ part_ml, float* __restrict__ out) {
+  constexpr int kMax = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const int qh = blockIdx.y * 4 + warp;
   if (i >= n_merge || qh >= hq_local) return;
   const int req = table[off_req + i];
-  const int p0 = table[off_ptr + i], np = min(table[off_ptr + i + 1] - p0, 4);
+  const int p0 = table[off_ptr + i], np = min(table[off_ptr + i + 1] - p0, kMax);
   const int32_t* slots = table + off_slot + p0;
-  float2 ml[4];
-  float4 o[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    if (p < np) {
-      const int64_t e = (int64_t)slots[p] * hq_local + qh;
-      ml[p] = __ldg(reinterpret_cast<const float2*>(part_ml) + e);
-      o[p] = __ldg(reinterpret_cast<const float4*>(part_o + e * 128) + lane);
-    } else {
-      ml[p] = make_float2(neg_inf<float>(), 0.f);
-      o[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  // lane p (< np) fetches partial p's (m, l); the max is a warp reduction
+  float2 mlp = make_float2(neg_inf<float>(), 0.f);
+  int64_t ep = 0;
+  if (lane < np) {
+    ep = (int64_t)slots[lane] * hq_local + qh;
+    mlp = __ldg(reinterpret_cast<const float2*>(part_ml) + ep);
   }
-  float M = neg_inf<float>();
-#pragma unroll
-  for (int p = 0; p < 4; ++p)
-    if (ml[p].y > 0) M = fmaxf(M, ml[p].x);
-  float L = 0.f;
+  float M = mlp.y > 0 ? mlp.x : neg_inf<float>();
+  M = warp_max(M);
+  const float wl = mlp.y > 0 ? mlp.y * __expf(mlp.x - M) : 0.f;
+  const float L = warp_sum(wl);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b = 0; b < np; b += 4) {
+    float4 o[4];
+    float w[4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const float w = ml[p].y > 0 ? ml[p].y * __expf(ml[p].x - M) : 0.f;
-    L += w;
-    acc.x += w * o[p].x;
-    acc.y += w * o[p].y;
-    acc.z += w * o[p].z;
-    acc.w += w * o[p].w;
+    for (int k = 0; k < 4; ++k) {
+      const int p = b + k;
+      w[k] = __shfl_sync(0xffffffffu, wl, p & 31);
+      const int64_t e = __shfl_sync(0xffffffffu, ep, p & 31);
+      o[k] = (p < np && w[k] > 0) ? __ldg(reinterpret_cast<const float4*>(part_o + e * 128) + lane)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float ww = (b + k < np) ? w[k] : 0.f;
+      acc.x += ww * o[k].x;
+      acc.y += ww * o[k].y;
+      acc.z += ww * o[k].z;
+      acc.w += ww * o[k].w;
+    }
   }
   const float inv = 1.f / L;
   reinterpret_cast<float4*>(out + ((int64_t)req * hq_local + qh) * 128)[lane] =
@@ -118,7 +124,7 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
                                              in.n_merge, hq_local, d, (const A*)part_o, (const A*)part_ml,      \
                                              (A*)out)
   if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
-  if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 4) {
+  if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 16) {
     merge128_kernel<<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot, in.n_merge,
                                           hq_local, (const float*)part_o, (const float*)part_ml, (float*)out);
     return cuda_status(cudaGetLastError(), "merge launch");

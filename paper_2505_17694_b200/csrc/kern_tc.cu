@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
-                  float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml) {
+                  float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
+                  long long* __restrict__ trace) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
@@ -142,6 +143,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int blk = blockIdx.x, kh = blockIdx.y;
+  // optional timeline of CTA (0, 0): trace[(event * 2 + q tile) * 64 + tile]
+  const bool tracing = trace != nullptr && blk == 0 && kh == 0;
+  auto stamp = [&](int ev, int i, int tt) {
+    if (tracing && tt < 64) trace[(ev * 2 + i) * 64 + tt] = clock64();
+  };
   const int g_begin = table[off_block_ptr + blk], g_end = table[off_block_ptr + blk + 1];
 
   if (tid == 0) {
@@ -267,6 +273,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(&bars->p_full[i], t & 1);                        // P_i(t) in TMEM
           if (j == 0 && gq > 0) mbar_wait(&bars->o_free[i], (gq - 1) & 1);  // epilogue read O_i
           tc::fence_after();
+          if (lane == 0) stamp(0, i, t);
           const uint32_t p_tmem = tmem + i * 128;
           const uint32_t o_tmem = tmem + 256 + i * 128;
           if (tc::elect_one()) {
@@ -281,6 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           __syncwarp();
           if (more) issue_s(i, t + 1);
+          if (lane == 0) stamp(1, i, t);
         }
       }
     }
@@ -335,6 +343,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
         mbar_wait(&bars->s_full[wg], t & 1);   // also: PV_wg(t-1) has landed (commit order)
         tc::fence_after();
+        if (tid == wg * 256) stamp(2, wg, t);
         const int lim = vis - j * kTcBN - hf * 64;  // visible columns of my half
         const bool full = __all_sync(0xffffffffu, !valid || lim >= 64);
         const uint32_t my_s = s_tmem + hf * 64;
@@ -359,6 +368,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         *xch_at(hf) = mx;
         pair_sync();
         mx = fmaxf(mx, *xch_at(hf ^ 1));
+        if (tid == wg * 256) stamp(4, wg, t);
         const float mt = valid ? mx * cscale : 0.f;
         if (j == 0) {
           m_used = mt;
@@ -417,6 +427,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         tc::wait_st();
         tc::fence_before();
+        if (tid == wg * 256) stamp(3, wg, t);
         mbar_arrive(&bars->p_full[wg]);
       }
       // ---- epilogue: O / l once the group's last PV landed
@@ -489,9 +500,15 @@ static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows)
   return CODEC_OK;
 }
 
+static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
+
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool trace) {
+  if (trace && !g_trace) {
+    if (cudaMalloc(&g_trace, 5 * 2 * 64 * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
+    cudaMemsetAsync(g_trace, 0, 5 * 2 * 64 * sizeof(long long), st);
+  }
   if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
   CUtensorMap mk, mv;
   CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens));
@@ -501,8 +518,15 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
   dim3 grid(in.n_tc_blocks, h_local);
   tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
-                                                   (float*)out, (float*)part_o, (float*)part_ml);
+                                                   (float*)out, (float*)part_o, (float*)part_ml,
+                                                   trace ? g_trace : nullptr);
   return cuda_status(cudaGetLastError(), "tc launch");
+}
+
+int32_t read_trace(long long* host, int64_t n) {
+  if (!g_trace) return fail(CODEC_ERR_VALUE, "no trace recorded");
+  if (n > 5 * 2 * 64) n = 5 * 2 * 64;
+  return cuda_status(cudaMemcpy(host, g_trace, n * sizeof(long long), cudaMemcpyDeviceToHost), "trace copy");
 }
 
 }  // namespace codec

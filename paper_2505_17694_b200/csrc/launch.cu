@@ -14,7 +14,8 @@
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st);
+                  cudaStream_t st, bool trace);
+int32_t read_trace(long long* host, int64_t n);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
                     const void* q, const void* k, const void* v, int64_t pool_tokens, int g, int h_local,
                     void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -79,7 +80,9 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
     if (cudaEventRecord(fj->fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fj->fork, 0) != cudaSuccess)
       return fail(CODEC_ERR_CUDA, "fork failed");
   }
-  if (do_tc) CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st));
+  if (do_tc)
+    CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
+                        (dims->flags & CODEC_FLAG_TRACE) != 0));
   if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side));
@@ -100,3 +103,5 @@ extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_ta
                                           void* out, void* workspace, void* stream) {
   return codec_decode_attention_ex(dims, info, table_dev, q, k, v, out, workspace, stream, nullptr);
 }
+
+extern "C" int32_t codec_debug_trace(long long* host, int64_t n) { return read_trace(host, n); }

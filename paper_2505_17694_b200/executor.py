@@ -102,7 +102,9 @@ class DecodeStep:
             L.codec_table_free(h)
         self.blob_host = blob
         self.table = torch.from_numpy(blob).to(self.device)
-        self.workspace = torch.empty(max(int(self.info.workspace_bytes), 256), dtype=torch.uint8, device=self.device)
+        # zeroed once: its last 256 bytes hold the persistent GEMV kernel's
+        # work counters, which every launch leaves at zero again
+        self.workspace = torch.zeros(max(int(self.info.workspace_bytes), 256), dtype=torch.uint8, device=self.device)
         self.out_dtype = torch.float64 if self.tdtype == torch.float64 else torch.float32
         self.hq_local = (self.head_end - self.head_begin) * self.g
 

@@ -136,6 +136,48 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
     return out
 
 
+TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
+
+
+def concat_plans(plans) -> DivisionPlan:
+    """One DivisionPlan from several plans over disjoint task lists (task
+    indices and block ids are offset; makespan = max)."""
+    tasks, subs, owner, loads, bk = [], [], [], [], []
+    t_off = b_off = 0
+    for p in plans:
+        tasks.extend(p.tasks)
+        bk.extend(p.b_k)
+        subs.extend(Subtask(st.task_index + t_off, st.node, st.start, st.stop, st.cost_ms) for st in p.subtasks)
+        owner.extend(b + b_off for b in p.assignment.block_of)
+        loads.extend(p.assignment.loads)
+        t_off += len(p.tasks)
+        b_off += p.blocks
+    return DivisionPlan(tasks=tuple(tasks), b_q=(1,) * len(tasks), b_k=tuple(bk), subtasks=tuple(subs),
+                        assignment=Assignment(tuple(owner), tuple(loads)), blocks=b_off,
+                        makespan_ms=max(p.makespan_ms for p in plans),
+                        cost_l_ms=plans[0].cost_l_ms, search_truncated=any(p.search_truncated for p in plans))
+
+
+def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
+                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT) -> DivisionPlan:
+    """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
+    head rows per chunk) are divided and LPT-scheduled with the reference
+    algorithm onto exactly the persistent tensor-core CTAs of one kv head
+    (m = budget // h_local), so slice counts match the CTA slots; unshared
+    nodes stay whole (their GEMV CTAs are hardware-scheduled and stream at
+    HBM speed regardless of order). Returns one plan over both."""
+    tasks = device_tasks(forest, group_size)
+    tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
+    gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
+    m_tc = max(1, (tc_sm_budget or sm_count) // max(1, h_local))
+    plans = []
+    if tc:
+        plans.append(divide_and_schedule(tc, table, m_tc, search_limit=search_limit))
+    if gv:  # one block per GEMV task: its makespan is the longest single task
+        plans.append(plan_uniform_bk(gv, table, len(gv), 1))
+    return concat_plans(plans)
+
+
 def lower_bound(tasks, table: CostTable, m: int, tol: float = 1e-4) -> float:
     """Eq. 4 bisection (scheduler.py:106-131)."""
     tasks, _, nq, n = _task_arrays(tasks)

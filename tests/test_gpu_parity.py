@@ -290,3 +290,14 @@ class TestConcurrency:
         assert np.array_equal(np_(best(qd, kp, vp)), base)
         ups = upcast_spec(spec)
         assert_bf16_close(base, OA.naive_attention(ups.queries, oracle_forest(ups)))
+
+    def test_repeat_launch_deterministic(self, cuda_ok, table):
+        """Back-to-back launches over the same workspace give identical outputs."""
+        spec = d128_forest(5, with_masks=True)
+        f, q = build(spec, "bfloat16")
+        plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, 2)
+        outs = [np_(P.execute(f, q, plan, flags=FLAG_NO_TC)) for _ in range(4)]
+        for o in outs[1:]:
+            assert np.array_equal(o, outs[0])
+        ups = upcast_spec(spec)
+        assert_bf16_close(outs[0], OA.naive_attention(ups.queries, oracle_forest(ups)))
