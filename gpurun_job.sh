@@ -1,10 +1,7 @@
-set -x
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"
-tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python tools/trace_tc.py > gpurun_out/trace.log 2>&1; tail -4 gpurun_out/trace.log
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_full.log 2>&1; echo "bench exit $?"
-timeout 600 python bench.py --serial --no-cpu-baseline > gpurun_out/bench_serial.log 2>&1; echo "bench serial exit $?"
-for f in gpurun_out/bench_full.log gpurun_out/bench_serial.log; do echo $f; python -c "
+timeout 100 python -m pytest tests -m gpu -x -q -k "tc or Tc or TC or smoke" 2>&1 | tail -2
+for fl in 0; do echo "== dbg $fl"; timeout 100 python tools/trace_tc.py $fl > gpurun_out/trace_$fl.log 2>&1; grep -A2 "period\|X (saw\|saw S -> S\|S freed -> m\|m settled ->" gpurun_out/trace_$fl.log | cut -c1-200; done
+timeout 200 python bench.py --serial --no-cpu-baseline > gpurun_out/bench_serial.log 2>&1; echo "bench serial exit $?"
+for f in gpurun_out/bench_serial.log; do echo $f; python -c "
 import json,sys
 for l in open('$f'):
   if l.startswith('{'):

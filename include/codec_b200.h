@@ -180,7 +180,9 @@ typedef struct {
 #define CODEC_FLAG_SKIP_TC      16
 #define CODEC_FLAG_SKIP_GEMV    32
 #define CODEC_FLAG_SKIP_MERGE   64
-#define CODEC_FLAG_TRACE        128  /* record a clock64 timeline of TC CTA (0,0) (debug) */
+#define CODEC_FLAG_TRACE        128  /* record a clock64 timeline of TC CTA pair (0,0) (debug) */
+#define CODEC_FLAG_DBG_NO_TMEM  256  /* TC softmax skips its TMEM S loads / P stores: timing only, wrong output (debug) */
+#define CODEC_FLAG_DBG_NO_EXP   512  /* TC softmax skips the exponentials: timing only, wrong output (debug) */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
@@ -229,7 +231,13 @@ CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_tab
                                const int32_t* table_dev, const void* q, const void* k,
                                const void* v, void* out, void* workspace, void* stream);
 
-/* Copy the TC timeline recorded under CODEC_FLAG_TRACE: n <= 640 clock64
+/* Debug builds only (compiled with -DCODEC_HANG_CHECK): a device pointer to
+ * host-mapped int32[8 + 8 * 1000]; a TC-kernel mbarrier wait that spins for
+ * ~2^20 polls appends (block.x, block.y, thread, barrier SMEM address,
+ * phase) there. Returns CODEC_ERR_VALUE in normal builds. */
+CODEC_API int32_t codec_debug_hang_buffer(void* dev_ptr);
+
+/* Copy the TC timeline recorded under CODEC_FLAG_TRACE: n <= 1792 clock64
  * values, trace[(event * 2 + q_tile) * 64 + tile], events: 0 MMA saw P,
  * 1 MMA issued PV+next S, 2 softmax saw S, 3 softmax released P, 4 softmax
  * finished the row-max exchange. Debug only. */

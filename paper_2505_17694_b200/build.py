@@ -27,7 +27,7 @@ OUT = PKG / "_codec_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden"]
-DEV_FLAGS = ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+DEV_FLAGS = ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"] + os.environ.get("CODEC_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -26,7 +26,10 @@ constexpr int kRowInts = 4;
 
 // minimum query-head rows for a subtask to take the tensor-core kernel
 constexpr int kTcMinRows = 16;
-// query-head rows of one tensor-core group (two M=128 tiles)
+// query-head rows of one tensor-core group (M = 256: one 128-row tile per
+// CTA of a cta_group::2 pair)
 constexpr int kTcGroupRows = 256;
+// SMs (CTAs) that run one tensor-core schedule block
+constexpr int kTcCtasPerBlock = 2;
 
 }  // namespace codec

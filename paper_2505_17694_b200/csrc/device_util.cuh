@@ -70,6 +70,35 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+#ifdef CODEC_HANG_CHECK
+// debug builds: a wait that spins for too long records (block, thread,
+// barrier SMEM address, phase) into host-mapped memory the host can read
+// while the kernel is stuck (tools/hang_probe.py)
+static __device__ int* g_hang_buf = nullptr;  // per translation unit (no -rdc)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    if (++spins == (1ll << 20) && g_hang_buf) {
+      const int slot = atomicAdd(g_hang_buf, 1);
+      if (slot < 1000) {
+        volatile int* rec = g_hang_buf + 8 + slot * 8;
+        rec[0] = blockIdx.x; rec[1] = blockIdx.y; rec[2] = threadIdx.x; rec[3] = (int)smem_u32(bar);
+        rec[4] = (int)phase; rec[5] = 1;
+        __threadfence_system();
+      }
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -79,6 +108,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#endif
 
 // 1D bulk async copy global -> shared, completion on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {

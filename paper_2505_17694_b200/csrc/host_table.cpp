@@ -267,7 +267,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
     if (dims->tc_sm_budget > 0) sms = std::min(sms, dims->tc_sm_budget);
     const int32_t h_local = dims->head_end - dims->head_begin;
-    int32_t m_tc = std::max(1, sms / h_local);
+    int32_t m_tc = std::max(1, sms / (h_local * kTcCtasPerBlock));
     m_tc = std::min<int32_t>(m_tc, (int32_t)tcg.size());
     std::vector<int64_t> cost(tcg.size());
     for (size_t i = 0; i < tcg.size(); ++i) {

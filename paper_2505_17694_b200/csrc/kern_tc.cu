@@ -1,38 +1,37 @@
-// K2: shared-node split attention on the 5th-generation tensor cores.
+// K2: shared-node split attention on the 5th-generation tensor cores,
+// one CTA PAIR (cta_group::2) per schedule block.
 //
-// Persistent CTA = (schedule block b, kv head h). It walks the TC groups
-// the balancer assigned to block b (LPT over the SM slots, host_table.cpp);
-// a group is a KV slice [kv_tok, kv_tok + len) of a shared node and up to
+// A group is a KV slice [kv_tok, kv_tok + len) of a shared node and up to
 // 256 query-head rows (256/g requests of the node's query set with their g
 // query heads: GQA packing turns the per-request GEMVs into one dense
-// contraction). The rows form two M=128 tiles, Q0 and Q1, that share every
-// K/V tile. Per 128-token KV tile t and Q tile i:
-//     S_i = Q_i K_t^T      tcgen05.mma SS, M128 N128 K128, fp32 in TMEM
-//     P_i = 2^(S_i c - m)  softmax warpgroup i (thread = row = TMEM lane),
-//                          written back over S_i as bf16 (tcgen05.st)
-//     O_i += P_i V_t       tcgen05.mma TS (A = P from TMEM), M128 N128 K128
+// contraction). The pair runs it as M=256 MMAs: CTA rank c owns rows
+// [128c, 128c+128) -- its S, P and O live in its own TMEM, its Q tile in
+// its own SMEM -- while each 128-token K/V tile is split between the two
+// CTAs' shared memories (K by tokens, V by head-dim columns) and read by
+// both through the pair's MMA. Per 128-token KV tile t:
+//     S(t) = Q K_t^T       tcgen05.mma.cta_group::2 SS, M256 N128 K128 -> S buffer t%2
+//     P(t) = 2^(S c - m)   one softmax thread per row (TMEM lane), bf16 -> P buffer t%2
+//     O   += P(t) V_t      tcgen05.mma.cta_group::2 TS (A = P in TMEM), M256 N128 K128
 // Per row this is the reference's pac_kernel math (_kernels.pyx:25-54);
 // the partial (O/l, m, l) feeds the LSE merge (kern_merge.cu).
 //
-// Why this shape: the SS QK^T MMA already consumes SMEM bandwidth at its
-// peak (A and B from SMEM), so P never goes through SMEM (TS MMA) and the
-// 128-token tile halves the Q re-reads per token. The issue order
-//     PV_0(t) S_0(t+1) PV_1(t) S_1(t+1)
-// ping-pongs the two softmax warpgroups: while WG0 exponentiates S_0(t+1)
-// the tensor pipe runs PV_1(t) and S_1(t+1). In-order tcgen05 execution
-// makes S_i(t+1) (which overwrites P_i(t)) safe after PV_i(t), and the
-// commit behind S_i(t) guarantees PV_i(t-1) landed before softmax i reads
-// or rescales O_i.
+// Pipeline (why it is shaped like this on B200): S and P are both double-
+// buffered in TMEM, so S(t+2) is issued as soon as the softmax has pulled
+// S(t) into registers -- the tensor pipe never waits for an exponential.
+// Two softmax warpgroups take alternate tiles (A even, B odd) with one
+// thread owning a whole 128-column row: no intra-row exchange, and while
+// one group waits on TMEM loads the other keeps MUFU/FMA busy. The row's
+// running max passes from group to group once per tile through SMEM and a
+// named-barrier arrive/sync pair; O is only touched by the lazy rescale
+// (row max grew by > 2^8), so the common path has no O traffic at all.
+// Cross-CTA signals are per-warp mbarrier arrivals on the leader with
+// release.cta semantics (~155 clk one way, tools/ubench_cluster.cu).
 //
-// Warp roles (576 threads): 16 softmax warps -- (Q tile, column half, TMEM
-// lane quadrant); a row's two 64-column halves exchange their max through
-// SMEM -- warp 16 TMA producer (K/V 2-stage rings of 128x64 SWIZZLE_128B
-// boxes), warp 17 TMEM allocator + single-thread MMA issuer. Two warps per
-// row keep two independent instruction streams per scheduler, which the
-// latency-bound exponential loop needs. Softmax: packed f32x2 math,
-// exponentials split between MUFU.EX2 (5/8) and a degree-3 polynomial on
-// the FMA pipe (3/8), lazy O rescale (only when a row max grows by > 2^8),
-// masking only on a row's last tile.
+// TMEM (512 columns per CTA): S0 [0,128) S1 [128,256) P0 [256,320)
+// P1 [320,384) O [384,512).
+// Warps: 0-3 softmax group A, 4-7 group B (lane quadrant = warp & 3),
+// 8 / 10 TMA producers of K / V (both CTAs load their halves; completion on
+// the leader's barriers), 9 TMEM allocator + MMA issuer (leader only).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,41 +42,46 @@
 
 namespace codec {
 
-constexpr int kTcSoftmaxWarps = 16;         // 2 Q tiles x 4 lane quadrants x 2 column halves
-constexpr int kTcProducerWarp = kTcSoftmaxWarps;
+constexpr int kTcSoftmaxWarps = 8;           // 2 groups x 4 lane quadrants
+constexpr int kTcProducerWarp = kTcSoftmaxWarps;       // K loads
 constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
-constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 2);
-constexpr int kTcBN = 128;                      // tokens per KV tile
-constexpr int kTcD = 128;                       // head dim
-constexpr int kTcKStages = 3;                   // K ring depth (K is needed one MMA earlier than V)
-constexpr int kTcVStages = 2;                   // V ring depth
-constexpr int kTcPrefetch = 3;                  // tiles ahead the producer warms L2
-constexpr int kTileBytes = 128 * 128 * 2;       // 32 KB: one 128x128 bf16 tile (Q, K or V)
-constexpr int kAtomBytes = kTileBytes / 2;      // 64-element-wide SW128 atom column
-constexpr int kOffQ = 0;                                 // Q0, Q1
-constexpr int kOffK = kOffQ + 2 * kTileBytes;            // K ring
-constexpr int kOffV = kOffK + kTcKStages * kTileBytes;   // V ring
-constexpr int kOffXch = kOffV + kTcVStages * kTileBytes; // row-max / row-sum exchange [2][2][128] f32
-constexpr int kOffBar = kOffXch + 2 * 2 * 128 * 4;
-// No alignment slack: the dynamic SMEM window starts 1024-aligned (behind the
-// driver's 1 KB reservation) and the kernel traps if it ever does not.
-constexpr int kTcSmem = kOffBar + 256;
+constexpr int kTcVProducerWarp = kTcSoftmaxWarps + 2;  // V loads (own warp: K must not queue behind V)
+constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 3);
+constexpr int kTcBN = 128;                   // tokens per KV tile
+constexpr int kTcD = 128;                    // head dim
+constexpr int kTcKStages = 4;
+constexpr int kTcVStages = 6;
+constexpr int kTcPrefetch = 4;               // tiles ahead the producer warms L2
+constexpr int kQBytes = 128 * 128 * 2;       // this CTA's 128-row Q tile (32 KB)
+constexpr int kQAtom = kQBytes / 2;          // Q atom column: 128 rows x 64 d (16 KB)
+constexpr int kHalfBytes = 64 * 128 * 2;     // this CTA's half of a K or V tile (16 KB)
+constexpr int kKAtom = kHalfBytes / 2;       // K-half atom column: 64 tokens x 64 d (8 KB)
+constexpr int kOffQ = 0;                     // Q0, Q1 (double-buffered across groups)
+constexpr int kOffK = kOffQ + 2 * kQBytes;
+constexpr int kOffV = kOffK + kTcKStages * kHalfBytes;
+constexpr int kOffMpub = kOffV + kTcVStages * kHalfBytes;  // [2 groups][128 rows] f32 published row max
+constexpr int kOffLx = kOffMpub + 2 * 128 * 4;             // [128 rows] float2 (l, m) at a group's end
+constexpr int kOffBar = kOffLx + 128 * 8;
+constexpr int kTcSmem = kOffBar + 512;
 static_assert(kTcSmem <= 232448, "exceeds the 227 KB opt-in shared memory");
-constexpr uint32_t kTmemCols = 512;  // S0/P0 [0,128) S1/P1 [128,256) O0 [256,384) O1 [384,512)
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr float kRescaleLog2 = 8.f;
+constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 
 struct TcBars {
-  uint64_t q_full;
   uint64_t k_full[kTcKStages], k_empty[kTcKStages];
   uint64_t v_full[kTcVStages], v_empty[kTcVStages];
-  uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
+  uint64_t q_full[2], s_full[2], s_free[2], p_full[2];
+  uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4] (parity waits stay within one phase)
+  uint64_t o_free;
   uint32_t tmem_slot;
 };
 
 // 16-byte chunk c (0..15 along a 128-element row) of row r in a K-major
-// SWIZZLE_128B 128x128 tile made of two 64-element atom columns
+// SWIZZLE_128B 128-row tile made of two 64-element atom columns
 __device__ __forceinline__ uint32_t sw128(int r, int c) {
-  return (c >> 3) * kAtomBytes + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+  return (c >> 3) * kQAtom + r * 128 + (((c & 7) ^ (r & 7)) << 4);
 }
 
 // 2^x on the FMA/ALU pipes (Cody-Waite split, degree-3 minimax on
@@ -92,8 +96,7 @@ __device__ __forceinline__ float poly_exp2(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Two lanes of the same polynomial with packed f32x2 arithmetic
-// (FADD2/FFMA2): ~5 issue slots per exponential instead of ~8.
+// Two lanes of the same polynomial with packed f32x2 arithmetic (FADD2/FFMA2)
 __device__ __forceinline__ float2 poly_exp2x2(float2 x) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
@@ -130,28 +133,72 @@ __device__ __forceinline__ GroupView group_view(const int32_t* table, int off_gr
   return v;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+// Walks the (group, tile) sequence of one schedule block; groups with no
+// tiles (cannot occur: every row sees >= 1 token) are skipped.
+struct TileCursor {
+  const int32_t* table;
+  int off_groups, off_rows, gi, g_end, n, j;
+  GroupView gv;
+  __device__ void open() {
+    while (gi < g_end) {
+      gv = group_view(table, off_groups, off_rows, gi);
+      if (gv.n_tiles > 0) return;
+      ++gi;
+    }
+  }
+  __device__ bool done() const { return gi >= g_end; }
+  __device__ void next() {
+    if (++j < gv.n_tiles) return;
+    j = 0;
+    ++n;
+    ++gi;
+    open();
+  }
+};
+
+
+#ifdef CODEC_HANG_CHECK
+// per-CTA progress words in host-mapped memory: [role * 2] = tile, [role * 2 + 1] = step
+#define PROG(role, tile, step)                                                                      \
+  do {                                                                                              \
+    if (g_hang_buf && (threadIdx.x & 31) == 0) {                                                  \
+      volatile int* pr = g_hang_buf + 8200 + (blockIdx.y * gridDim.x + blockIdx.x) * 8 + (role) * 2; \
+      pr[0] = (tile);                                                                               \
+      pr[1] = (step);                                                                               \
+    }                                                                                               \
+  } while (0)
+#else
+#define PROG(role, tile, step) \
+  do {                         \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     tc_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                   const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                  long long* __restrict__ trace) {
+                  long long* __restrict__ trace, int dbg_flags) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
   TcBars* bars = reinterpret_cast<TcBars*>(smem + kOffBar);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int blk = blockIdx.x, kh = blockIdx.y;
-  // optional timeline of CTA (0, 0): trace[(event * 2 + q tile) * 64 + tile]
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
+  const int blk = blockIdx.x >> 1, kh = blockIdx.y;
+  // optional timeline of pair (0, 0): trace[(event * 2 + rank) * 64 + tile]
   const bool tracing = trace != nullptr && blk == 0 && kh == 0;
-  auto stamp = [&](int ev, int i, int tt) {
-    if (tracing && tt < 64) trace[(ev * 2 + i) * 64 + tt] = clock64();
+  auto stamp = [&](int ev, int tt) {
+    if (tracing && tt < 64) trace[(ev * 2 + rank) * 64 + tt] = clock64();
   };
   const int g_begin = table[off_block_ptr + blk], g_end = table[off_block_ptr + blk + 1];
 
   if (tid == 0) {
-    mbar_init(&bars->q_full, 32 * kTcSoftmaxWarps);
     for (int s = 0; s < kTcKStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->k_empty[s], 1);
@@ -161,315 +208,410 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&bars->v_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->q_full[i], kGroupWarpArrivals);
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->p_full[i], 256);
-      mbar_init(&bars->o_done[i], 1);
-      mbar_init(&bars->o_free[i], 256);
+      mbar_init(&bars->s_free[i], kGroupWarpArrivals);
+      mbar_init(&bars->p_full[i], kGroupWarpArrivals);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&bars->pv_done[i], 1);
+    mbar_init(&bars->o_free, kGroupWarpArrivals);
     fence_barrier_init();
   }
-  if (warp == kTcMmaWarp) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
+  if (warp == kTcMmaWarp) tc::tmem_alloc_pair(&bars->tmem_slot, kTmemCols);
   if (warp == kTcProducerWarp && lane == 0) {
     tc::prefetch_tmap(&tmk);
     tc::prefetch_tmap(&tmv);
   }
   tc::fence_before();
-  __syncthreads();
+  tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
 
-  if (warp == kTcProducerWarp) {
-    // ================================================ TMA producer (whole warp, one lane issues)
-    int t = 0;  // global KV tile counter (ring position)
+  if (warp == kTcProducerWarp || warp == kTcVProducerWarp) {
+    // ================================================ TMA producers (both CTAs)
+    // K half: tokens [64 rank, 64 rank + 64) x all 128 d (two SW128 atom
+    // columns); V half: all 128 tokens x d [64 rank, 64 rank + 64). K and V
+    // stream from separate warps: the S MMAs run ahead of the PV MMAs, so a
+    // K load must never wait behind a V slot.
+    const bool is_k = warp == kTcProducerWarp;
+    int t = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       const int row0 = kh * (int)pool_tokens + gv.kv_tok;
-      if (tc::elect_one()) {  // warm L2 with the group's first tiles
+      if (is_k && tc::elect_one()) {
         for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
-          tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN);
-          tc::tma_prefetch_2d(&tmk, 64, row0 + j * kTcBN);
-          tc::tma_prefetch_2d(&tmv, 0, row0 + j * kTcBN);
-          tc::tma_prefetch_2d(&tmv, 64, row0 + j * kTcBN);
+          tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN + 64 * rank);
+          tc::tma_prefetch_2d(&tmk, 64, row0 + j * kTcBN + 64 * rank);
+          tc::tma_prefetch_2d(&tmv, 64 * rank, row0 + j * kTcBN);
         }
       }
       __syncwarp();
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-        const int ks = t % kTcKStages, vs = t % kTcVStages;
         const int y = row0 + j * kTcBN;
-        if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
-        if (tc::elect_one()) {
-          mbar_arrive_expect_tx(&bars->k_full[ks], kTileBytes);
-          uint8_t* kd = smem + kOffK + ks * kTileBytes;
-          tc::tma_load_2d(kd, &tmk, 0, y, &bars->k_full[ks]);
-          tc::tma_load_2d(kd + kAtomBytes, &tmk, 64, y, &bars->k_full[ks]);
-          if (j + kTcPrefetch < gv.n_tiles) {
-            const int yp = y + kTcPrefetch * kTcBN;
-            tc::tma_prefetch_2d(&tmk, 0, yp);
-            tc::tma_prefetch_2d(&tmk, 64, yp);
-            tc::tma_prefetch_2d(&tmv, 0, yp);
-            tc::tma_prefetch_2d(&tmv, 64, yp);
+        if (is_k) {
+          const int ks = t % kTcKStages;
+          PROG(3, t, 1);
+          if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
+          PROG(3, t, 2);
+          if (tc::elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
+            uint8_t* kd = smem + kOffK + ks * kHalfBytes;
+            tc::tma_load_2d_pair(kd, &tmk, 0, y + 64 * rank, &bars->k_full[ks]);
+            tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, y + 64 * rank, &bars->k_full[ks]);
+            if (j + kTcPrefetch < gv.n_tiles) {
+              const int yp = y + kTcPrefetch * kTcBN;
+              tc::tma_prefetch_2d(&tmk, 0, yp + 64 * rank);
+              tc::tma_prefetch_2d(&tmk, 64, yp + 64 * rank);
+              tc::tma_prefetch_2d(&tmv, 64 * rank, yp);
+            }
           }
-        }
-        __syncwarp();
-        if (t >= kTcVStages) mbar_wait(&bars->v_empty[vs], ((t / kTcVStages) - 1) & 1);
-        if (tc::elect_one()) {
-          mbar_arrive_expect_tx(&bars->v_full[vs], kTileBytes);
-          uint8_t* vd = smem + kOffV + vs * kTileBytes;
-          tc::tma_load_2d(vd, &tmv, 0, y, &bars->v_full[vs]);
-          tc::tma_load_2d(vd + kAtomBytes, &tmv, 64, y, &bars->v_full[vs]);
+        } else {
+          const int vs = t % kTcVStages;
+          if (t >= kTcVStages) mbar_wait(&bars->v_empty[vs], ((t / kTcVStages) - 1) & 1);
+          if (tc::elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&bars->v_full[vs], 2 * kHalfBytes);
+            tc::tma_load_2d_pair(smem + kOffV + vs * kHalfBytes, &tmv, 64 * rank, y, &bars->v_full[vs]);
+          }
         }
         __syncwarp();
       }
     }
   } else if (warp == kTcMmaWarp) {
-    // ================================================ MMA issuer
-    // The whole warp runs the (warp-uniform) schedule so the descriptors stay
-    // in uniform registers; one elected lane issues each batch of MMAs.
-    // Descriptors are a base plus a compile-time start-address offset
-    // (the low 14 bits hold addr >> 4).
-    constexpr uint32_t idesc_s = tc::idesc_bf16(128, kTcBN, false, false);
-    constexpr uint32_t idesc_o = tc::idesc_bf16(128, kTcD, false, true);
-    const uint64_t dq = tc::smem_desc(sbase + kOffQ, 16, 1024);
-    const uint64_t dk = tc::smem_desc(sbase + kOffK, 16, 1024);
-    const uint64_t dv = tc::smem_desc(sbase + kOffV, kAtomBytes, 1024);
-    int t = 0;  // global tile counter
-    int gq = 0;
-    auto issue_s = [&](int i, int tt) {
-      const int s = tt % kTcKStages;
-      const uint64_t aq = dq + (uint64_t)((i * kTileBytes) >> 4);
-      const uint64_t bk = dk + (uint64_t)((s * kTileBytes) >> 4);
-      if (tc::elect_one()) {
-#pragma unroll
-        for (int k = 0; k < kTcD / 16; ++k) {
-          const uint64_t off = (uint64_t)((((k >> 2) * kAtomBytes) + (k & 3) * 32) >> 4);
-          tc::mma_f16_ss(tmem + i * 128, aq + off, bk + off, idesc_s, k > 0 ? 1u : 0u);
-        }
-        tc::commit(&bars->s_full[i]);
-        if (i == 1) tc::commit(&bars->k_empty[s]);
-      }
-      __syncwarp();
-    };
-    for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
-      const GroupView gv = group_view(table, off_groups, off_rows, gi);
-      if (gv.n_tiles == 0) {  // (cannot happen: every row sees >= 1 token) keep gq in step
-        --gq;
-        continue;
-      }
-      mbar_wait(&bars->q_full, gq & 1);
-      {
-        const int s = t % kTcKStages;
-        mbar_wait(&bars->k_full[s], (t / kTcKStages) & 1);
+    // ================================================ MMA issuer (leader only)
+    if (leader) {
+      // S: A = Q tile (K-major SW128, 16 KB atom columns), B = K half
+      // (K-major SW128, 8 KB atom columns). PV: A = P (TMEM, 8 columns per
+      // 16 tokens), B = V half (MN-major SW128, one atom column).
+      constexpr uint32_t idesc_s = tc::idesc_bf16(256, kTcBN, false, false);
+      constexpr uint32_t idesc_o = tc::idesc_bf16(256, kTcD, false, true);
+      const uint64_t dq = tc::smem_desc(sbase + kOffQ, 16, 1024);
+      const uint64_t dk = tc::smem_desc(sbase + kOffK, 16, 1024);
+      const uint64_t dv = tc::smem_desc(sbase + kOffV, kHalfBytes, 1024);
+      TileCursor sc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
+      sc.open();
+      int ts = 0;  // next S tile (global)
+      auto issue_s = [&]() {
+        if (sc.done()) return;
+        const int s = ts % kTcKStages, b = ts & 1;
+        if (sc.j == 0) mbar_wait(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1);
+        mbar_wait(&bars->k_full[s], (ts / kTcKStages) & 1);  // (probed ready in the loop below)
         tc::fence_after();
-        issue_s(0, t);
-        issue_s(1, t);
-      }
-      for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-        const int s = t % kTcVStages;
-        const bool more = j + 1 < gv.n_tiles;
-        mbar_wait(&bars->v_full[s], (t / kTcVStages) & 1);
-        if (more) mbar_wait(&bars->k_full[(t + 1) % kTcKStages], ((t + 1) / kTcKStages) & 1);
-        const uint64_t bv = dv + (uint64_t)((s * kTileBytes) >> 4);
-        for (int i = 0; i < 2; ++i) {
-          mbar_wait(&bars->p_full[i], t & 1);                        // P_i(t) in TMEM
-          if (j == 0 && gq > 0) mbar_wait(&bars->o_free[i], (gq - 1) & 1);  // epilogue read O_i
-          tc::fence_after();
-          if (lane == 0) stamp(0, i, t);
-          const uint32_t p_tmem = tmem + i * 128;
-          const uint32_t o_tmem = tmem + 256 + i * 128;
-          if (tc::elect_one()) {
+        const uint64_t aq = dq + (uint64_t)(((sc.n & 1) * kQBytes) >> 4);
+        const uint64_t bk = dk + (uint64_t)((s * kHalfBytes) >> 4);
+        if (tc::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < kTcBN / 16; ++k)
-              // tokens [16k, 16k+16) of P: columns 64*(k/4) + 8*(k%4) (each
-              // column-half of the softmax packs its P over its own S columns)
-              tc::mma_f16_ts(o_tmem, p_tmem + (k >> 2) * 64 + (k & 3) * 8, bv + (uint64_t)((k * 16 * 128) >> 4),
-                             idesc_o, (j > 0 || k > 0) ? 1u : 0u);
-            if (i == 1) tc::commit(&bars->v_empty[s]);
-            if (!more) tc::commit(&bars->o_done[i]);
+          for (int k = 0; k < kTcD / 16; ++k) {
+            const uint64_t oa = (uint64_t)((((k >> 2) * kQAtom) + (k & 3) * 32) >> 4);
+            const uint64_t ob = (uint64_t)((((k >> 2) * kKAtom) + (k & 3) * 32) >> 4);
+            tc::mma2_f16_ss(tmem + kColS + b * 128, aq + oa, bk + ob, idesc_s, k > 0 ? 1u : 0u);
           }
-          __syncwarp();
-          if (more) issue_s(i, t + 1);
-          if (lane == 0) stamp(1, i, t);
+          tc::commit_pair(&bars->s_full[b]);
+          tc::commit_pair(&bars->k_empty[s]);
+        }
+        __syncwarp();
+        sc.next();
+        ++ts;
+      };
+      issue_s();
+      issue_s();
+      // Issue order S(k+2), PV(k-1), S(k+3), PV(k), ...: the order the
+      // softmax releases its inputs in steady state (it frees S(k) ~one
+      // exponential phase before P(k-1) of the other group is written), so
+      // blocking waits in this order never hold back the other stream.
+      // Deadlock-free: each wait depends only on MMAs issued earlier.
+      TileCursor pc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
+      pc.open();
+      auto issue_pv = [&](int tp) {
+        const int b = tp & 1, vs = tp % kTcVStages;
+        mbar_wait(&bars->p_full[b], (tp >> 1) & 1);  // P(tp) in both CTAs' TMEM
+        if (lane == 0) stamp(10, tp);
+        mbar_wait(&bars->v_full[vs], (tp / kTcVStages) & 1);
+        if (pc.j == 0 && pc.n > 0) mbar_wait(&bars->o_free, (pc.n - 1) & 1);  // epilogue read O
+        tc::fence_after();
+        if (lane == 0) stamp(0, tp);
+        const uint64_t bv = dv + (uint64_t)((vs * kHalfBytes) >> 4);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kTcBN / 16; ++k)
+            tc::mma2_f16_ts(tmem + kColO, tmem + kColP + b * 64 + k * 8, bv + (uint64_t)((k * 16 * 128) >> 4),
+                            idesc_o, (pc.j > 0 || k > 0) ? 1u : 0u);
+          tc::commit_pair(&bars->v_empty[vs]);
+          tc::commit_pair(&bars->pv_done[tp & 3]);
+        }
+        __syncwarp();
+        if (lane == 0) stamp(1, tp);
+        pc.next();
+      };
+      for (int k = 0; !pc.done(); ++k) {
+        if (!sc.done()) {
+          PROG(0, ts, 1);
+          mbar_wait(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1);  // both CTAs pulled S(ts-2) out of TMEM
+          if (lane == 0) stamp(8, ts);
+          PROG(0, ts, 2);
+          if (lane == 0) stamp(13, ts);
+          issue_s();
+          if (lane == 0) stamp(6, ts - 3);
+        }
+        if (k >= 1 && !pc.done()) {
+          PROG(0, k - 1, 4);
+          issue_pv(k - 1);
         }
       }
+      PROG(0, 9999, 7);
     }
   } else {
-    // ================================================ softmax warps
-    // warp = (Q tile wg, column half hf, lane quadrant quad); thread = one
-    // row of the Q tile (TMEM lane) over 64 of the tile's 128 columns. The
-    // two halves of a row meet through SMEM for the row max (named barrier
-    // per (wg, quad) pair) and, at the end of a group, for the row sum.
-    const int wg = warp >> 3;                 // Q tile
-    const int hf = (warp >> 2) & 1;           // column half
-    const int quad = warp & 3;                // TMEM lane quadrant
-    const int r = quad * 32 + lane;           // row in the Q tile == TMEM lane
+    // ================================================ softmax warpgroups
+    const int grp = warp >> 2;   // 0: even tiles, 1: odd tiles
+    const int quad = warp & 3;   // TMEM lane quadrant
+    const int r = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const uint32_t s_tmem = tmem + wg * 128 + lane_addr;
-    const uint32_t o_tmem = tmem + 256 + wg * 128 + lane_addr + hf * 64;
-    const uint32_t bar_id = 1 + wg * 4 + quad;  // pairs the two half-warps of these rows
-    // [wg][hf][128]; single-buffered: a pair barrier before every write keeps
-    // the partner's previous read ahead of the overwrite
-    float* xch = reinterpret_cast<float*>(smem + kOffXch);
-    auto xch_at = [&](int h) -> float* { return xch + (wg * 2 + h) * 128 + r; };
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    float* mpub = reinterpret_cast<float*>(smem + kOffMpub);
+    float2* lx = reinterpret_cast<float2*>(smem + kOffLx);
+    const int pub_mine = 1 + grp * 4 + quad, pub_other = 1 + (grp ^ 1) * 4 + quad;
     const float cscale = 1.4426950408889634f * rsqrtf((float)kTcD);
     const float2 c2 = make_float2(cscale, cscale);
-    int t = 0, gq = 0;
-    for (int gi = g_begin; gi < g_end; ++gi, ++gq) {
-      const GroupView gv = group_view(table, off_groups, off_rows, gi);
-      if (gv.n_tiles == 0) {
-        --gq;
-        continue;
+    const int grow = (int)rank * 128 + r;  // row of the 256-row group
+    // stage this thread's Q row of group gidx into SMEM Q buffer qb (K-major SW128)
+    auto stage_q = [&](int gidx, int qb) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gidx);
+      const int ridx = grow / g;
+      const bool valid = ridx < gv.n_req;
+      const int req = valid ? gv.rows[ridx * kRowInts] : 0;
+      const int qh = kh * g + (grow % g);
+      const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
+      uint8_t* qs = smem + kOffQ + qb * kQBytes;
+#pragma unroll
+      for (int h = 0; h < 16; h += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = valid ? __ldg(src + h + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(qs + sw128(r, h + c)) = v[c];
       }
-      const int grow = wg * 128 + r;          // row of the 256-row group
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(&bars->q_full[qb], 0);
+    };
+    auto next_group = [&](int gidx) {
+      for (++gidx; gidx < g_end; ++gidx)
+        if (group_view(table, off_groups, off_rows, gidx).n_tiles > 0) break;
+      return gidx;
+    };
+    int gi = g_begin;
+    while (gi < g_end && group_view(table, off_groups, off_rows, gi).n_tiles == 0) ++gi;
+    if (gi < g_end && grp == 0) stage_q(gi, 0);
+    // total tiles of the block (the last tile publishes no row max)
+    int t_total = 0;
+    for (int x = gi; x < g_end; ++x) t_total += group_view(table, off_groups, off_rows, x).n_tiles;
+    int t = 0, n = 0;
+    for (; gi < g_end; gi = next_group(gi), ++n) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
       const int ridx = grow / g;
       const bool valid = ridx < gv.n_req;
       const int req = valid ? gv.rows[ridx * kRowInts + 0] : 0;
       const int vis = valid ? gv.rows[ridx * kRowInts + 1] : 0;
       const int slot = valid ? gv.rows[ridx * kRowInts + 2] : 0;
       const int qh = kh * g + (grow % g);
-      {  // stage my half of the Q row (K-major SW128); the previous group's S MMAs are complete
-        uint8_t* qs = smem + kOffQ + wg * kTileBytes;
-        const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
-#pragma unroll
-        for (int c = hf * 8; c < hf * 8 + 8; ++c) {
-          const uint4 v = valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(qs + sw128(r, c)) = v;
-        }
-        tc::fence_proxy_async_smem();
-        mbar_arrive(&bars->q_full);
-      }
-      float m_used = 0.f;  // exponent reference (log2 units), same in both halves
-      float2 l2 = make_float2(0.f, 0.f);
+      float l = 0.f, my_m = 0.f;  // my tiles' row sum, relative to 2^my_m
+      bool have = false;          // processed a tile of this group
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-        mbar_wait(&bars->s_full[wg], t & 1);   // also: PV_wg(t-1) has landed (commit order)
+        if ((t & 1) != grp) continue;
+        const int b = t & 1;
+        if (quad == 0) PROG(1 + grp, t, 1);
+        mbar_wait(&bars->s_full[b], (t >> 1) & 1);
+        if (quad == 0) PROG(1 + grp, t, 2);
         tc::fence_after();
-        if (tid == wg * 256) stamp(2, wg, t);
-        const int lim = vis - j * kTcBN - hf * 64;  // visible columns of my half
-        const bool full = __all_sync(0xffffffffu, !valid || lim >= 64);
-        const uint32_t my_s = s_tmem + hf * 64;
-        // pass 1: max over my 64 columns
-        float mx = neg_inf<float>();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t sr[32];
-          tc::tmem_ld32(my_s + c * 32, sr);
-          tc::wait_ld();
-          if (!full) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= lim) sr[i] = 0xff800000u;  // -inf
-          }
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+        if (tid == grp * 128) stamp(2, t);
+        if (j == 0) {  // every S of the previous group is done: its Q buffer is free
+          const int gn = next_group(gi);
+          if (gn < g_end) stage_q(gn, (n + 1) & 1);
         }
-        // meet the other half of the row (each half only ever writes P into
-        // its own S columns, so no ordering beyond this exchange is needed)
-        pair_sync();
-        *xch_at(hf) = mx;
-        pair_sync();
-        mx = fmaxf(mx, *xch_at(hf ^ 1));
-        if (tid == wg * 256) stamp(4, wg, t);
-        const float mt = valid ? mx * cscale : 0.f;
-        if (j == 0) {
-          m_used = mt;
-        } else {
-          const bool need = mt > m_used + kRescaleLog2;
-          if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
-            const float alpha = need ? fast_exp2(m_used - mt) : 1.f;
-            l2.x *= alpha;
-            l2.y *= alpha;
+        uint32_t sr[128];
+        const uint32_t my_s = tmem + lane_addr + kColS + b * 128;
+        if (dbg_flags & 256) {  // timing experiment: no TMEM S traffic
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              uint32_t o[32];
-              tc::tmem_ld32(o_tmem + c * 32, o);
+          for (int i = 0; i < 128; ++i) sr[i] = __float_as_uint((float)((i * 37 + lane) & 15) * 0.1f);
+        } else {
+          tc::tmem_ld32(my_s, sr);
+          tc::tmem_ld32(my_s + 32, sr + 32);
+          tc::tmem_ld32(my_s + 64, sr + 64);
+          tc::tmem_ld32(my_s + 96, sr + 96);
+          tc::wait_ld();
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(&bars->s_free[b], 0);  // S buffer b may be overwritten
+        if (tid == grp * 128) stamp(4, t);
+        const int lim = vis - j * kTcBN;  // visible columns of this tile
+        if (!__all_sync(0xffffffffu, !valid || lim >= kTcBN)) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i >= lim) sr[i] = 0xff800000u;  // -inf
+        }
+        // row max as 8 independent 3-input chains (depth 8 instead of 64)
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = __uint_as_float(sr[k]);
+#pragma unroll
+        for (int i = 8; i < 120; i += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            m8[k] = fmaxf(m8[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], __uint_as_float(sr[120 + k]));
+        const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        const float mt = valid ? mx * cscale : 0.f;
+        // the row's exponent reference after tile t-1 (published by the other group)
+        float m_prev = mt;
+        if (quad == 0) PROG(1 + grp, t, 3);
+        if (t > 0) {
+          named_sync(pub_other, 64);
+          if (j > 0) m_prev = mpub[(grp ^ 1) * 128 + r];
+        }
+        float mr = m_prev;
+        if (j > 0) {
+          const bool need = mt > m_prev + kRescaleLog2;
+          if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
+            // PV(t-1) must have landed (PV(t) waits for our P). pv_done[x]
+            // completes for PV(x), PV(x+4), ...: PV(t-5) is done (this group
+            // waited for PV(t-4) at tile t-2) and PV(t+3) cannot be, so the
+            // parity wait is exact.
+            mbar_wait(&bars->pv_done[(t - 1) & 3], ((t - 1) >> 2) & 1);
+            tc::fence_after();
+            const float alpha = need ? fast_exp2(m_prev - mt) : 1.f;
+            const uint32_t my_o = tmem + lane_addr + kColO;
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              uint32_t o[16];
+              tc::tmem_ld16(my_o + c * 16, o);
               tc::wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tc::tmem_st32(o_tmem + c * 32, o);
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tc::tmem_st16(my_o + c * 16, o);
             }
-            if (need) m_used = mt;
+            tc::wait_st();
+            if (need) mr = mt;
           }
         }
-        // pass 2: P = 2^(S c - m) as bf16 pairs; S columns 64hf + [32c, 32c+32)
-        // -> P columns 64hf + [16c, 16c+16), i.e. over my own consumed S
-        const float2 nm = make_float2(-m_used, -m_used);
+        if (t + 1 < t_total) {
+          mpub[grp * 128 + r] = mr;
+          named_arrive(pub_mine, 64);
+        }
+        if (tid == grp * 128) stamp(5, t);
+        // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
+        // for at tile t-4; PV(t+2) cannot be)
+        if (quad == 0) PROG(1 + grp, t, 5);
+        if (t >= 2) mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+        if (quad == 0) PROG(1 + grp, t, 6);
+        if (tid == grp * 128) stamp(12, t);
+        // my row sum follows the reference
+        if (!have) {
+          my_m = mr;
+          have = true;
+        } else if (mr != my_m) {
+          l *= fast_exp2(my_m - mr);
+          my_m = mr;
+        }
+        tc::fence_after();
+        // P = 2^(S c - m) as bf16 pairs, 16 TMEM columns per 32 scores
+        const float2 nm = make_float2(-mr, -mr);
+        // four independent row-sum chains (a single fadd2 chain would be
+        // 64 dependent adds long)
+        float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const uint32_t my_p = tmem + lane_addr + kColP + b * 64;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t sr[32];
-          tc::tmem_ld32(my_s + c * 32, sr);
-          tc::wait_ld();
-          if (!full) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= lim) sr[i] = 0xff800000u;
-          }
+        for (int c = 0; c < 4; ++c) {
           uint32_t pw[16];
+          if (dbg_flags & 512) {  // timing experiment: no exponentials
+#pragma unroll
+            for (int w = 0; w < 16; ++w) pw[w] = sr[c * 32 + 2 * w] ^ sr[c * 32 + 2 * w + 1];
+          } else
 #pragma unroll
           for (int w = 0; w < 16; w += 4) {
-            // 8 scores: 5 exponentials on the MUFU, 3 on the FMA pipe (a packed pair + 1)
+            // 8 scores: 4 exponentials on the MUFU (16/clk/SM), 4 as two packed
+            // f32x2 polynomials on the FMA pipe -- the two pipes finish together
             float2 x[4], p[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              x[k] = tc::ffma2(make_float2(__uint_as_float(sr[2 * (w + k)]), __uint_as_float(sr[2 * (w + k) + 1])),
-                               c2, nm);
-            const float2 py = poly_exp2x2(make_float2(x[2].y, x[3].y));
+            for (int k = 0; k < 4; ++k) {
+              const int e = c * 32 + 2 * (w + k);
+              x[k] = tc::ffma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), c2, nm);
+            }
             p[0] = make_float2(fast_exp2(x[0].x), fast_exp2(x[0].y));
-            p[1] = make_float2(fast_exp2(x[1].x), poly_exp2(x[1].y));
-            p[2] = make_float2(fast_exp2(x[2].x), py.x);
-            p[3] = make_float2(fast_exp2(x[3].x), py.y);
+            p[1] = make_float2(fast_exp2(x[1].x), fast_exp2(x[1].y));
+            p[2] = poly_exp2x2(x[2]);
+            p[3] = poly_exp2x2(x[3]);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              l2 = tc::fadd2(l2, p[k]);
+              l2[k] = tc::fadd2(l2[k], p[k]);
               pw[w + k] = pack_bf16(p[k].x, p[k].y);
             }
           }
-          tc::tmem_st16(my_s + c * 16, pw);
+          if (!(dbg_flags & 256)) tc::tmem_st16(my_p + c * 16, pw);
+          else if (pw[0] == 12345u) sr[c] = pw[1];  // keep the math alive
+        }
+        {
+          const float2 la = tc::fadd2(l2[0], l2[1]), lb = tc::fadd2(l2[2], l2[3]);
+          l += (la.x + la.y) + (lb.x + lb.y);
         }
         tc::wait_st();
         tc::fence_before();
-        if (tid == wg * 256) stamp(3, wg, t);
-        mbar_arrive(&bars->p_full[wg]);
+        __syncwarp();
+        if (tid == grp * 128) stamp(3, t);
+        if (lane == 0 && quad == 3) stamp(7, t);
+        if (lane == 0) tc::mbar_arrive_cluster(&bars->p_full[b], 0);
       }
-      // ---- epilogue: O / l once the group's last PV landed
-      float l_run = l2.x + l2.y;
-      pair_sync();
-      *xch_at(hf) = l_run;
-      pair_sync();
-      l_run += *xch_at(hf ^ 1);
-      mbar_wait(&bars->o_done[wg], gq & 1);
-      tc::fence_after();
-      float* dst;
-      if (slot < 0) {
-        dst = out + ((int64_t)req * hq_local + qh) * kTcD + hf * 64;
+      // ---- epilogue: the group that ran the last tile writes O / l
+      // (both groups' 256 threads meet on a barrier alternating with the
+      // group parity, so one group's next epilogue never joins this one)
+      const int last = (t - 1) & 1, l_bar = 9 + (n & 1);
+      if (quad == 0) PROG(1 + grp, t, 7);
+      if (grp != last) {
+        lx[r] = make_float2(have ? l : 0.f, my_m);
+        named_arrive(l_bar, 256);
       } else {
-        const int64_t ei = (int64_t)slot * hq_local + qh;
-        dst = part_o + ei * kTcD + hf * 64;
-        if (valid && hf == 0) {
-          part_ml[2 * ei] = m_used * 0.69314718055994530942f;  // natural-log units
-          part_ml[2 * ei + 1] = l_run;
-        }
-      }
-      const float inv = 1.f / l_run;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t o[32];
-        tc::tmem_ld32(o_tmem + c * 32, o);
-        tc::wait_ld();
+        named_sync(l_bar, 256);
+        const float2 o2 = lx[r];
+        const float l_run = l + (o2.x > 0.f ? o2.x * fast_exp2(o2.y - my_m) : 0.f);
+        const int tl = t - 1;  // PV(tl) landed => the whole group landed (PV(tl-4) is done)
+        mbar_wait(&bars->pv_done[tl & 3], (tl >> 2) & 1);
+        tc::fence_after();
+        float* dst = nullptr;
         if (valid) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(dst + c * 32 + i) =
-                make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
-                            __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          if (slot < 0) {
+            dst = out + ((int64_t)req * hq_local + qh) * kTcD;
+          } else {
+            const int64_t ei = (int64_t)slot * hq_local + qh;
+            dst = part_o + ei * kTcD;
+            part_ml[2 * ei] = my_m * 0.69314718055994530942f;  // natural-log units
+            part_ml[2 * ei + 1] = l_run;
+          }
         }
+        const float inv = 1.f / l_run;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tc::tmem_ld32(tmem + lane_addr + kColO + c * 32, o);
+          tc::wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + c * 32 + i) =
+                  make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
+                              __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(&bars->o_free, 0);
       }
-      tc::fence_before();
-      mbar_arrive(&bars->o_free[wg]);
+      if (quad == 0) PROG(1 + grp, t, 8);
     }
   }
   tc::fence_before();
-  __syncthreads();
-  if (warp == kTcMmaWarp) tc::tmem_dealloc(tmem, kTmemCols);
+  tc::cluster_sync();  // the leader's MMAs into the peer's TMEM and all remote arrivals are done
+  tc::fence_after();
+  if (warp == kTcMmaWarp) tc::tmem_dealloc_pair(tmem, kTmemCols);
 }
 
 // ------------------------------------------------------------------ host
@@ -479,7 +621,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 int32_t cuda_status(cudaError_t e, const char* what);
 
-static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows) {
+// a [rows][128] bf16 pool viewed as SW128 boxes of 64 head-dim x box_rows tokens
+static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult qr;
@@ -491,7 +634,7 @@ static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows)
   }
   cuuint64_t dims[2] = {(cuuint64_t)kTcD, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kTcD * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)kTcBN};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -500,32 +643,43 @@ static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows)
   return CODEC_OK;
 }
 
+constexpr int kTraceLen = 14 * 2 * 64;
 static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
 
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, bool trace) {
+                  cudaStream_t st, int flags) {
+  const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
-    if (cudaMalloc(&g_trace, 5 * 2 * 64 * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
-    cudaMemsetAsync(g_trace, 0, 5 * 2 * 64 * sizeof(long long), st);
+    if (cudaMalloc(&g_trace, kTraceLen * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
+    cudaMemsetAsync(g_trace, 0, kTraceLen * sizeof(long long), st);
   }
   if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
   CUtensorMap mk, mv;
-  CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens));
-  CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens));
+  CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, 64));      // K half: 64 tokens
+  CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kTcBN));   // V half: 64 d columns
   cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   if (e != cudaSuccess) return cuda_status(e, "tc smem attribute");
-  dim3 grid(in.n_tc_blocks, h_local);
+  dim3 grid(kTcCtasPerBlock * in.n_tc_blocks, h_local);  // CTA pairs (__cluster_dims__)
   tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
-                                                   trace ? g_trace : nullptr);
+                                                   trace ? g_trace : nullptr, flags);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 
+#ifdef CODEC_HANG_CHECK
+int32_t set_hang_buffer(void* dev_ptr) {
+  int* p = static_cast<int*>(dev_ptr);
+  return cuda_status(cudaMemcpyToSymbol(g_hang_buf, &p, sizeof(p)), "hang buffer");
+}
+#else
+int32_t set_hang_buffer(void*) { return fail(CODEC_ERR_VALUE, "built without CODEC_HANG_CHECK"); }
+#endif
+
 int32_t read_trace(long long* host, int64_t n) {
   if (!g_trace) return fail(CODEC_ERR_VALUE, "no trace recorded");
-  if (n > 5 * 2 * 64) n = 5 * 2 * 64;
+  if (n > kTraceLen) n = kTraceLen;
   return cuda_status(cudaMemcpy(host, g_trace, n * sizeof(long long), cudaMemcpyDeviceToHost), "trace copy");
 }
 

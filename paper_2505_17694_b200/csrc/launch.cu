@@ -14,8 +14,9 @@
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, bool trace);
+                  cudaStream_t st, int flags);
 int32_t read_trace(long long* host, int64_t n);
+int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
                     const void* q, const void* k, const void* v, int64_t pool_tokens, int g, int h_local,
                     void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -82,7 +83,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   }
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
-                        (dims->flags & CODEC_FLAG_TRACE) != 0));
+                        dims->flags));
   if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side));
@@ -105,3 +106,6 @@ extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_ta
 }
 
 extern "C" int32_t codec_debug_trace(long long* host, int64_t n) { return read_trace(host, n); }
+
+// debug builds (CODEC_NVCC_EXTRA=-DCODEC_HANG_CHECK): where TC waits spin too long
+extern "C" CODEC_API int32_t codec_debug_hang_buffer(void* dev_ptr) { return set_hang_buffer(dev_ptr); }

@@ -137,6 +137,7 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
+TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 
 
 def concat_plans(plans) -> DivisionPlan:
@@ -163,13 +164,14 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
     head rows per chunk) are divided and LPT-scheduled with the reference
     algorithm onto exactly the persistent tensor-core CTAs of one kv head
-    (m = budget // h_local), so slice counts match the CTA slots; unshared
+    (m = budget // (2 h_local): one block is a CTA pair), so slice counts
+    match the CTA slots; unshared
     nodes stay whole (their GEMV CTAs are hardware-scheduled and stream at
     HBM speed regardless of order). Returns one plan over both."""
     tasks = device_tasks(forest, group_size)
     tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
     gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
-    m_tc = max(1, (tc_sm_budget or sm_count) // max(1, h_local))
+    m_tc = max(1, (tc_sm_budget or sm_count) // max(1, h_local * TC_CTAS_PER_BLOCK))
     plans = []
     if tc:
         plans.append(divide_and_schedule(tc, table, m_tc, search_limit=search_limit))
