@@ -1,6 +1,10 @@
-set -x
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 300 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -15 gpurun_out/pytest_gpu.log
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; tail -3 gpurun_out/smoke.log
-timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench exit $?"; tail -c 3000 gpurun_out/bench.log
+timeout 300 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python bench.py --serial --no-cpu-baseline --steps 10 > gpurun_out/bench_serial.log 2>&1; echo "bench exit $?"
+timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench.log 2>&1; echo "bench exit $?"
+for f in gpurun_out/bench_serial.log gpurun_out/bench.log; do python -c "
+import json,sys
+for l in open('$f'):
+  if l.startswith('{'):
+    d=json.loads(l); print('us/step %.1f GB/s %.0f'%(d['us_per_step'],d['value']), {k:round(v['ms']*1e3,1) for k,v in d['kernels'].items()}, d['clocks'], d['config'].get('tc_sm_budget'), d['config'].get('autotune_ms'))
+"; tail -2 $f | grep -i error; done

@@ -183,6 +183,8 @@ typedef struct {
 #define CODEC_FLAG_TRACE        128  /* record a clock64 timeline of TC CTA pair (0,0) (debug) */
 #define CODEC_FLAG_DBG_NO_TMEM  256  /* TC softmax skips its TMEM S loads / P stores: timing only, wrong output (debug) */
 #define CODEC_FLAG_DBG_NO_EXP   512  /* TC softmax skips the exponentials: timing only, wrong output (debug) */
+#define CODEC_FLAG_CTALOG       1024 /* record {smid, start ns, end ns, cta} per TC / GEMV CTA (debug) */
+#define CODEC_FLAG_GEMV_SIMT    2048 /* suffix groups on the CUDA-core GEMV kernel instead of the mma.sync one */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
@@ -199,7 +201,7 @@ typedef struct {
   int32_t off_tc, off_gemv, off_gen, off_rows;         /* int32 offsets into the blob */
   int32_t off_merge_req, off_merge_ptr, off_merge_slot;
   int32_t h_local;                                     /* head_end - head_begin */
-  int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTAs per head, their group CSR */
+  int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTA pairs, their (group, head) unit CSR */
   int32_t max_merge, reserved;                         /* most partials of one merged request */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
@@ -242,6 +244,10 @@ CODEC_API int32_t codec_debug_hang_buffer(void* dev_ptr);
  * 1 MMA issued PV+next S, 2 softmax saw S, 3 softmax released P, 4 softmax
  * finished the row-max exchange. Debug only. */
 CODEC_API int32_t codec_debug_trace(long long* host, int64_t n);
+/* Copy the CTA log recorded under CODEC_FLAG_CTALOG: 4 int64 per record,
+   TC CTAs at records [0, 4096), GEMV CTAs (blockIdx.y * gridDim.x +
+   blockIdx.x) from record 4096 (debug). */
+CODEC_API int32_t codec_debug_ctalog(long long* host, int64_t n);
 
 /* ======================================================================
  * Device primitives with the reference's argument meaning.

@@ -22,8 +22,9 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
-OBJ = ROOT / "build" / "obj"
-OUT = PKG / "_codec_b200.so"
+_TAG = os.environ.get("CODEC_BUILD_TAG", "")  # debug variants: build/obj_<tag>, _codec_b200_<tag>.so
+OBJ = ROOT / "build" / ("obj_" + _TAG if _TAG else "obj")
+OUT = PKG / ("_codec_b200_" + _TAG + ".so" if _TAG else "_codec_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden"]

@@ -17,8 +17,10 @@ constexpr int kGrpKvTok = 0;    // pool token index of the slice start
 constexpr int kGrpLen = 1;      // slice length (tokens)
 constexpr int kGrpRowBegin = 2; // first row record
 constexpr int kGrpNRows = 3;    // number of requests in the group
-constexpr int kGrpSub = 4;      // plan subtask (diagnostics)
+constexpr int kGrpMaxVis = 4;   // most visible tokens of any row (kernels size their tile loop by it)
 constexpr int kGrpNode = 5;     // forest node (diagnostics)
+constexpr int kGrpBlock = 6;    // TC: schedule block (CTA pair) of the unit
+constexpr int kGrpHead = 7;     // TC: local kv head of the unit
 
 // a row record: 4 int32 -- request, visible tokens within the slice,
 // partial slot (>= 0) or -1 - request for a direct write of the output
@@ -31,5 +33,9 @@ constexpr int kTcMinRows = 16;
 constexpr int kTcGroupRows = 256;
 // SMs (CTAs) that run one tensor-core schedule block
 constexpr int kTcCtasPerBlock = 2;
+
+// debug CTA log (CODEC_FLAG_CTALOG): TC records first, GEMV from this index
+constexpr int kCtaLogGemv = 4096;
+constexpr int kCtaLogLen = 4096 + 65536;
 
 }  // namespace codec

@@ -121,4 +121,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
 
 __device__ __forceinline__ bool elect_lane0() { return (threadIdx.x & 31) == 0; }
 
+
+// debug (CODEC_FLAG_CTALOG): one record per CTA {smid, start ns, end ns, cta}
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_log(long long* log, int idx, long long t0) {
+  if (log == nullptr || threadIdx.x != 0) return;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  long long* r = log + 4 * (int64_t)idx;
+  r[0] = sm;
+  r[1] = t0;
+  r[2] = global_ns();
+  r[3] = idx;
+}
+
 }  // namespace codec

@@ -162,7 +162,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
 
   // ---- rows and slots
   struct Grp {
-    int32_t kind, kv_tok, len, row_begin, n_rows, sub, node;
+    int32_t kind, kv_tok, len, row_begin, n_rows, max_vis, node;
     int64_t order_len;
   };
   std::vector<Grp> groups;
@@ -198,8 +198,10 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     }
     for (size_t a = 0; a < live.size(); a += per) {
       size_t b = std::min(live.size(), a + per);
+      int32_t max_vis = 0;
+      for (size_t i = a; i < b; ++i) max_vis = std::max(max_vis, live[i].second);
       Grp gr{kind, (int32_t)(off[n] + start), (int32_t)(stop - start), (int32_t)(rows.size() / 4),
-             (int32_t)(b - a), s, (int32_t)n, stop - start};
+             (int32_t)(b - a), max_vis, (int32_t)n, stop - start};
       for (size_t i = a; i < b; ++i) {
         int32_t r = live[i].first;
         int64_t pp = path_pos(r, n);
@@ -251,15 +253,17 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     count = 0;
     for (auto& gr : groups)
       if (gr.kind == kind) {
-        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.sub, gr.node, 0, 0};
+        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, 0, 0};
         blob.insert(blob.end(), rec, rec + kGroupInts);
         ++count;
       }
   };
-  // ---- tensor-core groups: LPT onto the persistent CTA slots of one head
-  // (cost = 64-token tiles, the unit the kernel iterates), same rule as
-  // greedy_assign (scheduler.py:142-155); each block keeps its groups in
-  // assignment order.
+  // ---- tensor-core units: one (group, local kv head) pair of the table is
+  // a unit; units are LPT-scheduled onto the persistent CTA pairs of the
+  // whole GPU (cost = 64-token tiles, the unit the kernel iterates), same
+  // rule as greedy_assign (scheduler.py:142-155) -- heads are not pinned
+  // to CTAs, so every SM of the budget gets work whatever h_local is.
+  // Each pair keeps its units in assignment order.
   {
     std::vector<Grp> tcg;
     for (auto& gr : groups)
@@ -267,33 +271,33 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
     if (dims->tc_sm_budget > 0) sms = std::min(sms, dims->tc_sm_budget);
     const int32_t h_local = dims->head_end - dims->head_begin;
-    int32_t m_tc = std::max(1, sms / (h_local * kTcCtasPerBlock));
-    m_tc = std::min<int32_t>(m_tc, (int32_t)tcg.size());
+    const int64_t n_units = (int64_t)tcg.size() * h_local;
+    int32_t m_tc = std::max(1, sms / kTcCtasPerBlock);
+    m_tc = (int32_t)std::min<int64_t>(m_tc, n_units);
     std::vector<int64_t> cost(tcg.size());
-    for (size_t i = 0; i < tcg.size(); ++i) {
-      int64_t mv = 0;
-      for (int32_t k = 0; k < tcg[i].n_rows; ++k) mv = std::max<int64_t>(mv, rows[4 * (tcg[i].row_begin + k) + 1]);
-      cost[i] = (mv + 63) / 64;
-    }
-    std::vector<int32_t> order(tcg.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cost[a] > cost[b]; });
+    for (size_t i = 0; i < tcg.size(); ++i) cost[i] = (tcg[i].max_vis + 63) / 64;
+    // units in (cost desc, group, head) order
+    std::vector<int64_t> order(n_units);
+    for (int64_t u = 0; u < n_units; ++u) order[u] = u;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return cost[a / h_local] > cost[b / h_local]; });
     std::vector<int64_t> load(std::max(m_tc, 1), 0);
-    std::vector<std::vector<int32_t>> per_block(std::max(m_tc, 1));
-    for (int32_t i : order) {
+    std::vector<std::vector<int64_t>> per_block(std::max(m_tc, 1));
+    for (int64_t u : order) {
       int32_t best = 0;
       for (int32_t b = 1; b < m_tc; ++b)
         if (load[b] < load[best]) best = b;
-      load[best] += cost[i];
-      per_block[best].push_back(i);
+      load[best] += cost[u / h_local];
+      per_block[best].push_back(u);
     }
     in.off_tc = (int32_t)blob.size();
-    in.n_tc_groups = (int32_t)tcg.size();
+    in.n_tc_groups = (int32_t)n_units;
     std::vector<int32_t> block_ptr{0};
     for (int32_t b = 0; b < m_tc; ++b) {
-      for (int32_t i : per_block[b]) {
-        const Grp& gr = tcg[i];
-        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.sub, gr.node, b, 0};
+      for (int64_t u : per_block[b]) {
+        const Grp& gr = tcg[u / h_local];
+        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, b,
+                                   (int32_t)(u % h_local)};
         blob.insert(blob.end(), rec, rec + kGroupInts);
       }
       block_ptr.push_back(block_ptr.back() + (int32_t)per_block[b].size());

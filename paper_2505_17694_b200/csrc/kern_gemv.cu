@@ -28,9 +28,9 @@
 
 namespace codec {
 
-constexpr int kGemvWarps = 4;                  // consumer warps
+constexpr int kGemvWarps = 2;                  // consumer warps (3 warps per CTA: one per SMSP next to a TC CTA)
 constexpr int kGemvThreads = 32 * (kGemvWarps + 1);
-constexpr int kGemvStages = 4;
+constexpr int kGemvStages = 3;                 // 48 KB ring: fits beside a TC CTA on one SM
 constexpr int kGemvStageBytes = 8192;          // K (and V) bytes per stage
 
 template <typename T, int D, int R>
@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
                                                                  int g, int hq_local, float qscale,
                                                                  float* __restrict__ out,
                                                                  float* __restrict__ part_o,
-                                                                 float* __restrict__ part_ml) {
+                                                                 float* __restrict__ part_ml,
+                                                                 long long* __restrict__ ctalog) {
+  const long long t_start = ctalog ? global_ns() : 0;
   using C = GemvCfg<T, D, R>;
   extern __shared__ __align__(128) uint8_t smem[];
   T* sk = reinterpret_cast<T*>(smem);                                  // [S][CT][D]
@@ -289,6 +291,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_pac_kernel(const int32_t* _
       }
     }
   }
+  if (ctalog) {
+    __syncthreads();
+    cta_log(ctalog, kCtaLogGemv + blockIdx.y * gridDim.x + blockIdx.x, t_start);
+  }
 }
 
 int32_t cuda_status(cudaError_t e, const char* what);
@@ -296,28 +302,30 @@ int32_t cuda_status(cudaError_t e, const char* what);
 template <typename T, int D, int R>
 int32_t launch_gemv_t(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                       const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
-                      void* part_o, void* part_ml, cudaStream_t st) {
+                      void* part_o, void* part_ml, cudaStream_t st, long long* ctalog) {
   const int smem = 2 * kGemvStages * kGemvStageBytes + 2 * kGemvStages * 8;
   static_assert(kGemvWarps * R * (D + 2) * 4 <= kGemvStages * kGemvStageBytes * 2, "stash must fit the ring");
   auto kern = gemv_pac_kernel<T, D, R>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_status(e, "gemv smem attribute");
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_status(e, "gemv carveout attribute");
   const float qscale = (float)(1.4426950408889634 / sqrt((double)D));
   dim3 grid(n_groups, h_local);
   kern<<<grid, kGemvThreads, smem, st>>>(table, off_groups, off_rows, (const T*)q, (const T*)k, (const T*)v,
                                         pool_tokens, g, h_local * g, qscale, (float*)out, (float*)part_o,
-                                        (float*)part_ml);
+                                        (float*)part_ml, ctalog);
   return cuda_status(cudaGetLastError(), "gemv launch");
 }
 
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
                     const void* q, const void* k, const void* v, int64_t pool_tokens, int g, int h_local,
-                    void* out, void* part_o, void* part_ml, cudaStream_t st) {
+                    void* out, void* part_o, void* part_ml, cudaStream_t st, long long* ctalog) {
   if (n_groups == 0) return CODEC_OK;
 #define CODEC_GEMV(T, D, R)                                                                                 \
   if (d == D && rows == R)                                                                                  \
   return launch_gemv_t<T, D, R>(table, n_groups, off_groups, off_rows, q, k, v, pool_tokens, g, h_local, out, \
-                                part_o, part_ml, st)
+                                part_o, part_ml, st, ctalog)
   if (dtype == CODEC_BF16) {
     CODEC_GEMV(__nv_bfloat16, 64, 4);
     CODEC_GEMV(__nv_bfloat16, 64, 8);

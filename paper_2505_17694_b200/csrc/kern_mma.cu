@@ -1,0 +1,288 @@
+// K3: unshared / lightly shared nodes (the per-request suffixes) on the
+// warp-level tensor cores (mma.sync m16n8k16 bf16 -> f32, HMMA in SASS).
+//
+// Same math as the reference's pac_kernel (_kernels.pyx:25-54) for the g
+// query heads of one request and one kv head over the request's visible
+// part of one node slice: scores q.k/sqrt(d), online softmax, normalised
+// output plus (m, s). One CTA = (GEMV group = one request's slice, one kv
+// head); rows = the g <= 8 query heads (GQA packing, padded to n = 8).
+//
+// Why tensor cores for a GEMV: the suffix path is HBM-bound, but it runs
+// concurrently with the persistent tcgen05 kernel on the same SMs, whose
+// softmax needs most of the issue slots. Turned on its side -- S^T = K Q^T
+// (m = 16 tokens, n = 8 heads, k = 16 of d) and O^T += V^T P^T (m = 16 of d,
+// n = 8 heads, k = 16 tokens) -- one request-head costs ~3.5 warp
+// instructions per token instead of ~40 on the CUDA cores (FFMA2 dots,
+// bf16 converts, shuffles). P^T reaches the B-fragment layout with two
+// movmatrix.trans per 16 tokens; no TMEM is used, so the kernel co-resides
+// with the tcgen05 kernel (which owns all 512 TMEM columns).
+//
+// Memory path: one producer lane streams the slice with 2D TMA boxes
+// (32 tokens x 64 d, SWIZZLE_128B) of the head-major pool into a 4-stage
+// ring (K and V, 16 KB per stage); the swizzle makes the ldmatrix reads
+// conflict-free. Two consumer warps take 16 tokens of each stage.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "device_table.h"
+#include "device_util.cuh"
+#include "tc_ptx.cuh"
+
+namespace codec {
+
+constexpr int kMmaWarps = 2;                       // consumer warps
+constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
+constexpr int kMmaStages = 4;
+constexpr int kMmaCT = 16 * kMmaWarps;             // tokens per stage
+constexpr int kMmaD = 128;
+constexpr int kMmaBox = kMmaCT * 128;              // one 64-d SW128 box of kMmaCT tokens (4 KB)
+constexpr int kMmaStageBytes = 4 * kMmaBox;        // K (2 boxes) + V (2 boxes)
+constexpr int kMmaSmem = kMmaStages * kMmaStageBytes + 1024 /* align */ + 2 * kMmaStages * 8;
+
+// byte offset of 16-byte chunk c (0..15 along d) of token row r in a K or V
+// stage (two 64-d SW128 boxes of kMmaCT rows)
+__device__ __forceinline__ uint32_t mma_sw(int r, int c) {
+  return (c >> 3) * kMmaBox + r * 128 + (((c & 7) ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void hmma(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kMmaThreads, 6)
+    mma_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                   const int32_t* __restrict__ table, int off_groups, int off_rows,
+                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
+                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
+                   long long* __restrict__ ctalog) {
+  const long long t_start = ctalog ? global_ns() : 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMmaStages * kMmaStageBytes);
+  uint64_t* empty = full + kMmaStages;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t* grp = table + off_groups + blockIdx.x * kGroupInts;
+  const int kh = blockIdx.y;
+  const int32_t* row = table + off_rows + grp[kGrpRowBegin] * kRowInts;
+  const int req = row[0], n_tok = row[1], slot = row[2];
+  const int nch = (n_tok + kMmaCT - 1) / kMmaCT;
+  const int row0 = kh * (int)pool_tokens + grp[kGrpKvTok];
+
+  if (tid == 0) {
+    for (int s = 0; s < kMmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kMmaWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kMmaWarps) {
+    // ---------------- producer: one lane streams K and V boxes
+    if (lane == 0) {
+      tc::prefetch_tmap(&tmk);
+      tc::prefetch_tmap(&tmv);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kMmaStages;
+        if (c >= kMmaStages) mbar_wait(&empty[s], ((c / kMmaStages) - 1) & 1);
+        uint8_t* st = smem + s * kMmaStageBytes;
+        const int y = row0 + c * kMmaCT;
+        mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
+        tc::tma_load_2d(st, &tmk, 0, y, &full[s]);
+        tc::tma_load_2d(st + kMmaBox, &tmk, 64, y, &full[s]);
+        tc::tma_load_2d(st + 2 * kMmaBox, &tmv, 0, y, &full[s]);
+        tc::tma_load_2d(st + 3 * kMmaBox, &tmv, 64, y, &full[s]);
+      }
+    }
+  } else {
+    // ---------------- consumers: 16 tokens of every stage each
+    const int gid = lane >> 2, tig = lane & 3;
+    const float cscale = 1.4426950408889634f * rsqrtf((float)kMmaD);
+    // B fragments of Q^T (k = d, n = query head gid of this kv head)
+    uint32_t qf[8][2];
+    {
+      const bool hv = gid < g;
+      const uint32_t* qp = reinterpret_cast<const uint32_t*>(q + ((int64_t)req * hq_local + kh * g + (hv ? gid : 0)) * kMmaD);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qf[ks][0] = hv ? __ldg(qp + ks * 8 + tig) : 0u;
+        qf[ks][1] = hv ? __ldg(qp + ks * 8 + 4 + tig) : 0u;
+      }
+    }
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m_run[2] = {neg_inf<float>(), neg_inf<float>()};  // heads 2 tig, 2 tig + 1 (log2 units)
+    float l_run[2] = {0.f, 0.f};                            // this lane's tokens only
+    const int mat = lane >> 3, rr = lane & 7;
+    const int tk_qk = 16 * warp + rr + ((mat & 1) << 3), ck_qk = mat >> 1;  // ldmatrix rows for S^T
+    const int tk_pv = 16 * warp + rr + ((mat >> 1) << 3), ck_pv = mat & 1;  // ldmatrix.trans rows for V^T
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % kMmaStages;
+      mbar_wait(&full[s], (c / kMmaStages) & 1);
+      const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + 2 * kMmaBox;
+      // S^T (16 tokens x 8 heads) = K Q^T
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t a[4];
+        ldsm_x4(kb + mma_sw(tk_qk, 2 * ks + ck_qk), a);
+        hmma(sc, a, qf[ks][0], qf[ks][1]);
+      }
+      // sc[0]: (token gid, head 2tig), [1]: (gid, 2tig+1), [2]: (gid+8, 2tig), [3]: (gid+8, 2tig+1)
+      const int t0 = c * kMmaCT + 16 * warp + gid;
+      const bool va = t0 < n_tok, vb8 = t0 + 8 < n_tok;
+      sc[0] = va ? sc[0] * cscale : neg_inf<float>();
+      sc[1] = va ? sc[1] * cscale : neg_inf<float>();
+      sc[2] = vb8 ? sc[2] * cscale : neg_inf<float>();
+      sc[3] = vb8 ? sc[3] * cscale : neg_inf<float>();
+      float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+      }
+      // lazy rescale: the exponent reference moves only when a head's max
+      // beats it by more than 2^8 (p <= 256 otherwise: exact enough in fp32)
+      const bool n0 = mx0 > m_run[0] + 8.f, n1 = mx1 > m_run[1] + 8.f;
+      if (__any_sync(0xffffffffu, n0 || n1)) {
+        const float a0 = n0 ? fast_exp2(m_run[0] - mx0) : 1.f;  // 0 on a head's first live tile
+        const float a1 = n1 ? fast_exp2(m_run[1] - mx1) : 1.f;
+        l_run[0] *= a0;
+        l_run[1] *= a1;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i][0] *= a0;
+          acc[i][2] *= a0;
+          acc[i][1] *= a1;
+          acc[i][3] *= a1;
+        }
+        if (n0) m_run[0] = mx0;
+        if (n1) m_run[1] = mx1;
+      }
+      const bool d0 = m_run[0] == neg_inf<float>(), d1 = m_run[1] == neg_inf<float>();
+      const float p0 = d0 ? 0.f : fast_exp2(sc[0] - m_run[0]);
+      const float p1 = d1 ? 0.f : fast_exp2(sc[1] - m_run[1]);
+      const float p2 = d0 ? 0.f : fast_exp2(sc[2] - m_run[0]);
+      const float p3 = d1 ? 0.f : fast_exp2(sc[3] - m_run[1]);
+      l_run[0] += p0 + p2;
+      l_run[1] += p1 + p3;
+      // P^T as the B fragment (k = token, n = head): transpose the two 8x8 halves
+      const uint32_t b0 = movm_t(pack2_bf16(p0, p1)), b1 = movm_t(pack2_bf16(p2, p3));
+      // O^T (128 d x 8 heads) += V^T P^T
+#pragma unroll
+      for (int dm = 0; dm < 8; ++dm) {
+        uint32_t a[4];
+        ldsm_x4_t(vb + mma_sw(tk_pv, 2 * dm + ck_pv), a);
+        hmma(acc[dm], a, b0, b1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // row sums over the lanes holding other tokens of the same heads
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], o);
+      l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], o);
+    }
+    // stash (m, l, O^T) per warp in the ring (every stage consumed by now:
+    // wait for the other consumer warp before overwriting)
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kMmaWarps) : "memory");
+    float* wm = reinterpret_cast<float*>(smem) + warp * (16 + 8 * kMmaD);  // m[8], l[8], O[8][128]
+    if (gid == 0) {
+      wm[2 * tig] = m_run[0];
+      wm[2 * tig + 1] = m_run[1];
+      wm[8 + 2 * tig] = l_run[0];
+      wm[8 + 2 * tig + 1] = l_run[1];
+    }
+#pragma unroll
+    for (int dm = 0; dm < 8; ++dm) {
+      const int dd = 16 * dm + gid;
+      wm[16 + (2 * tig) * kMmaD + dd] = acc[dm][0];
+      wm[16 + (2 * tig + 1) * kMmaD + dd] = acc[dm][1];
+      wm[16 + (2 * tig) * kMmaD + dd + 8] = acc[dm][2];
+      wm[16 + (2 * tig + 1) * kMmaD + dd + 8] = acc[dm][3];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kMmaWarps) : "memory");
+    const float* wb = reinterpret_cast<const float*>(smem);
+    for (int idx = tid; idx < g * kMmaD; idx += 32 * kMmaWarps) {
+      const int h = idx / kMmaD, e = idx % kMmaD;
+      float M = neg_inf<float>();
+#pragma unroll
+      for (int w = 0; w < kMmaWarps; ++w) M = fmaxf(M, wb[w * (16 + 8 * kMmaD) + h]);
+      float L = 0.f, O = 0.f;
+#pragma unroll
+      for (int w = 0; w < kMmaWarps; ++w) {
+        const float* x = wb + w * (16 + 8 * kMmaD);
+        if (x[h] == neg_inf<float>()) continue;
+        const float f = fast_exp2(x[h] - M);
+        L += x[8 + h] * f;
+        O += x[16 + h * kMmaD + e] * f;
+      }
+      const int qh = kh * g + h;
+      if (slot < 0) {
+        out[((int64_t)req * hq_local + qh) * kMmaD + e] = O / L;
+      } else {
+        const int64_t ei = (int64_t)slot * hq_local + qh;
+        part_o[ei * kMmaD + e] = O / L;
+        if (e == 0) {
+          part_ml[2 * ei] = M * 0.69314718055994530942f;  // natural-log units
+          part_ml[2 * ei + 1] = L;
+        }
+      }
+    }
+  }
+  if (ctalog) {
+    __syncthreads();
+    cta_log(ctalog, kCtaLogGemv + blockIdx.y * gridDim.x + blockIdx.x, t_start);
+  }
+}
+
+int32_t cuda_status(cudaError_t e, const char* what);
+int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows);
+
+int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
+                        const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
+                        void* part_o, void* part_ml, cudaStream_t st, long long* ctalog) {
+  if (n_groups == 0) return CODEC_OK;
+  if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
+  CUtensorMap mk, mv;
+  CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, kMmaCT));
+  CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kMmaCT));
+  cudaError_t e = cudaFuncSetAttribute(mma_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMmaSmem);
+  if (e != cudaSuccess) return cuda_status(e, "mma smem attribute");
+  e = cudaFuncSetAttribute(mma_pac_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_status(e, "mma carveout attribute");
+  dim3 grid(n_groups, h_local);
+  mma_pac_kernel<<<grid, kMmaThreads, kMmaSmem, st>>>(mk, mv, table, off_groups, off_rows,
+                                                      (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
+                                                      (float*)out, (float*)part_o, (float*)part_ml, ctalog);
+  return cuda_status(cudaGetLastError(), "mma gemv launch");
+}
+
+}  // namespace codec

@@ -46,7 +46,13 @@ constexpr int kTcSoftmaxWarps = 8;           // 2 groups x 4 lane quadrants
 constexpr int kTcProducerWarp = kTcSoftmaxWarps;       // K loads
 constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
 constexpr int kTcVProducerWarp = kTcSoftmaxWarps + 2;  // V loads (own warp: K must not queue behind V)
-constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 3);
+constexpr int kTcQWarp = kTcSoftmaxWarps + 3;          // gathers the next unit's Q rows into SMEM
+constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 4);
+// One CTA per SM owns the register file: 384 threads x 168 at launch, then
+// setmaxnreg hands the producer / MMA warpgroup's surplus to the softmax.
+// (No other kernel may share the SM: the hand-off corrupted the registers
+// of a co-resident CTA of another kernel in testing.)
+constexpr int kTcRegsSoftmax = 200, kTcRegsOther = 96;  // 256 x 200 + 128 x 96 <= 384 x 168
 constexpr int kTcBN = 128;                   // tokens per KV tile
 constexpr int kTcD = 128;                    // head dim
 constexpr int kTcKStages = 4;
@@ -72,7 +78,7 @@ constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 struct TcBars {
   uint64_t k_full[kTcKStages], k_empty[kTcKStages];
   uint64_t v_full[kTcVStages], v_empty[kTcVStages];
-  uint64_t q_full[2], s_full[2], s_free[2], p_full[2];
+  uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], p_full[2];
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4] (parity waits stay within one phase)
   uint64_t o_free;
   uint32_t tmem_slot;
@@ -117,7 +123,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 struct GroupView {
-  int kv_tok, n_req, n_tiles;
+  int kv_tok, n_req, n_tiles, kh;
   const int32_t* rows;
 };
 
@@ -126,10 +132,9 @@ __device__ __forceinline__ GroupView group_view(const int32_t* table, int off_gr
   GroupView v;
   v.kv_tok = grp[kGrpKvTok];
   v.n_req = grp[kGrpNRows];
+  v.kh = grp[kGrpHead];
   v.rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
-  int max_vis = 0;
-  for (int i = 0; i < v.n_req; ++i) max_vis = max(max_vis, v.rows[i * kRowInts + 1]);
-  v.n_tiles = (max_vis + kTcBN - 1) / kTcBN;
+  v.n_tiles = (grp[kGrpMaxVis] + kTcBN - 1) / kTcBN;
   return v;
 }
 
@@ -181,7 +186,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                   const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                  long long* __restrict__ trace, int dbg_flags) {
+                  long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog) {
+  const long long t_start = ctalog ? global_ns() : 0;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
@@ -190,9 +196,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = tc::cluster_rank();
   const bool leader = rank == 0;
-  const int blk = blockIdx.x >> 1, kh = blockIdx.y;
+  const int blk = blockIdx.x >> 1;
   // optional timeline of pair (0, 0): trace[(event * 2 + rank) * 64 + tile]
-  const bool tracing = trace != nullptr && blk == 0 && kh == 0;
+  const bool tracing = trace != nullptr && blk == 0;
   auto stamp = [&](int ev, int tt) {
     if (tracing && tt < 64) trace[(ev * 2 + rank) * 64 + tt] = clock64();
   };
@@ -208,7 +214,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_init(&bars->v_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->q_full[i], kGroupWarpArrivals);
+      mbar_init(&bars->q_full[i], 2);  // the Q warps of both CTAs
+      mbar_init(&bars->q_empty[i], 1);
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], kGroupWarpArrivals);
       mbar_init(&bars->p_full[i], kGroupWarpArrivals);
@@ -226,7 +233,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
-
+  if (warp >= kTcSoftmaxWarps) {
+  // producer / MMA warpgroup: hands registers to the softmax warpgroups
+#ifndef CODEC_NO_SETMAXNREG
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegsOther));
+#endif
   if (warp == kTcProducerWarp || warp == kTcVProducerWarp) {
     // ================================================ TMA producers (both CTAs)
     // K half: tokens [64 rank, 64 rank + 64) x all 128 d (two SW128 atom
@@ -237,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     int t = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
-      const int row0 = kh * (int)pool_tokens + gv.kv_tok;
+      const int row0 = gv.kh * (int)pool_tokens + gv.kv_tok;
       if (is_k && tc::elect_one()) {
         for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
           tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN + 64 * rank);
@@ -276,6 +287,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         __syncwarp();
       }
     }
+  } else if (warp == kTcQWarp) {
+    // ================================================ Q gather (both CTAs)
+    // this CTA's 128 query-head rows of each unit (row r = request r / g of
+    // the unit, q head kv_head * g + r % g) into Q buffer n % 2, K-major
+    // SW128; the buffer is reused once the unit two back issued its last S
+    const int nq_local = hq_local;
+    int n = 0;
+    for (int gi = g_begin; gi < g_end; ++gi) {
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      if (gv.n_tiles == 0) continue;
+      const int qb = n & 1;
+      if (n >= 2) mbar_wait(&bars->q_empty[qb], ((n - 2) >> 1) & 1);
+      uint8_t* qs = smem + kOffQ + qb * kQBytes;
+#pragma unroll 1
+      for (int i0 = 0; i0 < 64; i0 += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = (i0 + i) * 32 + lane, r = e >> 4, c = e & 15;
+          const int grow = (int)rank * 128 + r, ridx = grow / g;
+          v[i] = make_uint4(0, 0, 0, 0);
+          if (ridx < gv.n_req) {
+            const int req = __ldg(gv.rows + ridx * kRowInts);
+            const uint4* src = reinterpret_cast<const uint4*>(
+                q + ((int64_t)req * nq_local + gv.kh * g + (grow % g)) * kTcD);
+            v[i] = __ldg(src + c);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = (i0 + i) * 32 + lane;
+          *reinterpret_cast<uint4*>(qs + sw128(e >> 4, e & 15)) = v[i];
+        }
+      }
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(&bars->q_full[qb], 0);
+      ++n;
+    }
   } else if (warp == kTcMmaWarp) {
     // ================================================ MMA issuer (leader only)
     if (leader) {
@@ -307,6 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           tc::commit_pair(&bars->s_full[b]);
           tc::commit_pair(&bars->k_empty[s]);
+          if (sc.j + 1 == sc.gv.n_tiles) tc::commit_pair(&bars->q_empty[sc.n & 1]);  // unit's Q no longer read
         }
         __syncwarp();
         sc.next();
@@ -359,8 +410,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       PROG(0, 9999, 7);
     }
+    // Drain (both CTAs): tcgen05.commit arrivals land asynchronously, after
+    // the MMAs they track. Those nobody else waits for (the last S tiles'
+    // s_full / k_empty, the last PV tiles' v_empty, the last unit's
+    // q_empty, ...) must be seen here: once this CTA exits, a late arrival
+    // would hit the shared memory of whatever CTA the SM runs next.
+    {
+      int tiles = 0, units = 0;
+      for (int gi = g_begin; gi < g_end; ++gi) {
+        const int nt = group_view(table, off_groups, off_rows, gi).n_tiles;
+        tiles += nt;
+        units += nt > 0;
+      }
+      auto drain = [&](uint64_t* bar, int stages, int per_item) {
+        for (int s = 0; s < stages; ++s) {
+          const int n = per_item < 0 ? (units - s + stages - 1) / stages : (tiles - s + stages - 1) / stages;
+          if (n > 0) mbar_wait(&bar[s], (n - 1) & 1);
+        }
+      };
+      drain(bars->s_full, 2, 1);
+      drain(bars->k_empty, kTcKStages, 1);
+      drain(bars->v_empty, kTcVStages, 1);
+      drain(bars->pv_done, 4, 1);
+      drain(bars->q_empty, 2, -1);
+    }
+  }
   } else {
     // ================================================ softmax warpgroups
+#ifndef CODEC_NO_SETMAXNREG
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kTcRegsSoftmax));
+#endif
     const int grp = warp >> 2;   // 0: even tiles, 1: odd tiles
     const int quad = warp & 3;   // TMEM lane quadrant
     const int r = quad * 32 + lane;
@@ -371,27 +450,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const float cscale = 1.4426950408889634f * rsqrtf((float)kTcD);
     const float2 c2 = make_float2(cscale, cscale);
     const int grow = (int)rank * 128 + r;  // row of the 256-row group
-    // stage this thread's Q row of group gidx into SMEM Q buffer qb (K-major SW128)
-    auto stage_q = [&](int gidx, int qb) {
-      const GroupView gv = group_view(table, off_groups, off_rows, gidx);
-      const int ridx = grow / g;
-      const bool valid = ridx < gv.n_req;
-      const int req = valid ? gv.rows[ridx * kRowInts] : 0;
-      const int qh = kh * g + (grow % g);
-      const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + qh) * kTcD);
-      uint8_t* qs = smem + kOffQ + qb * kQBytes;
-#pragma unroll
-      for (int h = 0; h < 16; h += 8) {
-        uint4 v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = valid ? __ldg(src + h + c) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(qs + sw128(r, h + c)) = v[c];
-      }
-      tc::fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive_cluster(&bars->q_full[qb], 0);
-    };
     auto next_group = [&](int gidx) {
       for (++gidx; gidx < g_end; ++gidx)
         if (group_view(table, off_groups, off_rows, gidx).n_tiles > 0) break;
@@ -399,7 +457,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     };
     int gi = g_begin;
     while (gi < g_end && group_view(table, off_groups, off_rows, gi).n_tiles == 0) ++gi;
-    if (gi < g_end && grp == 0) stage_q(gi, 0);
     // total tiles of the block (the last tile publishes no row max)
     int t_total = 0;
     for (int x = gi; x < g_end; ++x) t_total += group_view(table, off_groups, off_rows, x).n_tiles;
@@ -411,7 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int req = valid ? gv.rows[ridx * kRowInts + 0] : 0;
       const int vis = valid ? gv.rows[ridx * kRowInts + 1] : 0;
       const int slot = valid ? gv.rows[ridx * kRowInts + 2] : 0;
-      const int qh = kh * g + (grow % g);
+      const int qh = gv.kh * g + (grow % g);
       float l = 0.f, my_m = 0.f;  // my tiles' row sum, relative to 2^my_m
       bool have = false;          // processed a tile of this group
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
@@ -422,10 +479,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (quad == 0) PROG(1 + grp, t, 2);
         tc::fence_after();
         if (tid == grp * 128) stamp(2, t);
-        if (j == 0) {  // every S of the previous group is done: its Q buffer is free
-          const int gn = next_group(gi);
-          if (gn < g_end) stage_q(gn, (n + 1) & 1);
-        }
         uint32_t sr[128];
         const uint32_t my_s = tmem + lane_addr + kColS + b * 128;
         if (dbg_flags & 256) {  // timing experiment: no TMEM S traffic
@@ -529,8 +582,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           } else
 #pragma unroll
           for (int w = 0; w < 16; w += 4) {
-            // 8 scores: 4 exponentials on the MUFU (16/clk/SM), 4 as two packed
-            // f32x2 polynomials on the FMA pipe -- the two pipes finish together
+            // 8 scores: 6 exponentials on the MUFU (16/clk/SM), 2 as a packed
+            // f32x2 polynomial on the FMA pipe: the MUFU share that keeps both
+            // the XU pipe and the issue slots below saturation
             float2 x[4], p[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -539,7 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             }
             p[0] = make_float2(fast_exp2(x[0].x), fast_exp2(x[0].y));
             p[1] = make_float2(fast_exp2(x[1].x), fast_exp2(x[1].y));
-            p[2] = poly_exp2x2(x[2]);
+            p[2] = make_float2(fast_exp2(x[2].x), fast_exp2(x[2].y));
             p[3] = poly_exp2x2(x[3]);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -612,6 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   tc::cluster_sync();  // the leader's MMAs into the peer's TMEM and all remote arrivals are done
   tc::fence_after();
   if (warp == kTcMmaWarp) tc::tmem_dealloc_pair(tmem, kTmemCols);
+  cta_log(ctalog, blockIdx.x, t_start);
 }
 
 // ------------------------------------------------------------------ host
@@ -622,7 +677,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 int32_t cuda_status(cudaError_t e, const char* what);
 
 // a [rows][128] bf16 pool viewed as SW128 boxes of 64 head-dim x box_rows tokens
-static int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows) {
+int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult qr;
@@ -648,7 +703,7 @@ static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one 
 
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags) {
+                  cudaStream_t st, int flags, long long* ctalog) {
   const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
     if (cudaMalloc(&g_trace, kTraceLen * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
@@ -660,11 +715,14 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
   CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kTcBN));   // V half: 64 d columns
   cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   if (e != cudaSuccess) return cuda_status(e, "tc smem attribute");
-  dim3 grid(kTcCtasPerBlock * in.n_tc_blocks, h_local);  // CTA pairs (__cluster_dims__)
+  // the full 228 KB carveout: a GEMV CTA must fit in what the TC CTA leaves
+  e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return cuda_status(e, "tc carveout attribute");
+  dim3 grid(kTcCtasPerBlock * in.n_tc_blocks, 1);  // CTA pairs (__cluster_dims__); heads come from the units
   tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
-                                                   trace ? g_trace : nullptr, flags);
+                                                   trace ? g_trace : nullptr, flags, ctalog);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

@@ -14,12 +14,15 @@
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags);
+                  cudaStream_t st, int flags, long long* ctalog);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
                     const void* q, const void* k, const void* v, int64_t pool_tokens, int g, int h_local,
-                    void* out, void* part_o, void* part_ml, cudaStream_t st);
+                    void* out, void* part_o, void* part_ml, cudaStream_t st, long long* ctalog);
+int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
+                        const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
+                        void* part_o, void* part_ml, cudaStream_t st, long long* ctalog);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -53,6 +56,16 @@ int32_t fork_join_events(ForkJoin*& out) {
 }
 }  // namespace
 
+namespace {
+long long* g_ctalog = nullptr;  // debug CTA log (CODEC_FLAG_CTALOG), one per process
+}
+
+extern "C" int32_t codec_debug_ctalog(long long* host, int64_t n) {
+  if (!g_ctalog) return fail(CODEC_ERR_VALUE, "no CTA log recorded");
+  if (n > 4 * (int64_t)kCtaLogLen) n = 4 * (int64_t)kCtaLogLen;
+  return codec::cuda_status(cudaMemcpy(host, g_ctalog, n * sizeof(long long), cudaMemcpyDeviceToHost), "ctalog copy");
+}
+
 extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
                                              const int32_t* table_dev, const void* q, const void* k, const void* v,
                                              void* out, void* workspace, void* stream, void* aux_stream) {
@@ -73,8 +86,22 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool do_tc = info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC);
   const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
   const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
-  const bool fork = aux_stream != nullptr && do_tc && (do_gemv || do_gen);
+  // The mma.sync suffix kernel must not share SMs with the TC kernel: the
+  // TC CTA's setmaxnreg register hand-off corrupts the registers of a
+  // co-resident CTA of another kernel (observed on B200: wrong O in the
+  // suffix partials, tools/determinism.py). It runs after the TC kernel.
+  const bool mma_gemv = do_gemv && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
+                        !(dims->flags & CODEC_FLAG_GEMV_SIMT);
+  const bool fork = aux_stream != nullptr && do_tc && ((do_gemv && !mma_gemv) || do_gen);
   cudaStream_t side = fork ? (cudaStream_t)aux_stream : st;
+  long long* ctalog = nullptr;
+  if (dims->flags & CODEC_FLAG_CTALOG) {
+    if (!g_ctalog && cudaMalloc(&g_ctalog, 4 * sizeof(long long) * kCtaLogLen) != cudaSuccess)
+      return fail(CODEC_ERR_CUDA, "ctalog alloc");
+    if (cudaMemsetAsync(g_ctalog, 0, 4 * sizeof(long long) * kCtaLogLen, st) != cudaSuccess)
+      return fail(CODEC_ERR_CUDA, "ctalog clear");
+    ctalog = g_ctalog;
+  }
   ForkJoin* fj = nullptr;
   if (fork) {
     CODEC_TRY(fork_join_events(fj));
@@ -83,10 +110,14 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   }
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
-                        dims->flags));
-  if (do_gemv)
+                        dims->flags, ctalog));
+  if (mma_gemv)
+    CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
+                              dims->pool_tokens, g, h_local, out, part_o, part_ml, st, ctalog));
+  else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
-                          info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side));
+                          info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
+                          ctalog));
   if (do_gen)
     CODEC_TRY(launch_generic_groups(dims->kv_dtype, table_dev, info->n_gen_groups, info->off_gen, info->off_rows, q,
                                     k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, side));

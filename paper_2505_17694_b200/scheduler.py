@@ -160,18 +160,21 @@ def concat_plans(plans) -> DivisionPlan:
 
 
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
-                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT) -> DivisionPlan:
+                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT,
+                units_per_pair: int = 4) -> DivisionPlan:
     """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
     head rows per chunk) are divided and LPT-scheduled with the reference
-    algorithm onto exactly the persistent tensor-core CTAs of one kv head
-    (m = budget // (2 h_local): one block is a CTA pair), so slice counts
-    match the CTA slots; unshared
+    algorithm onto m = ceil(units_per_pair * pairs / h_local) blocks, where
+    pairs = budget // 2 persistent tensor-core CTA pairs serve every local
+    kv head: the table builder then LPT-packs the (slice, head) units onto
+    the pairs (host_table.cpp), ~units_per_pair units per pair. Unshared
     nodes stay whole (their GEMV CTAs are hardware-scheduled and stream at
     HBM speed regardless of order). Returns one plan over both."""
     tasks = device_tasks(forest, group_size)
     tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
     gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
-    m_tc = max(1, (tc_sm_budget or sm_count) // max(1, h_local * TC_CTAS_PER_BLOCK))
+    pairs = max(1, (tc_sm_budget or sm_count) // TC_CTAS_PER_BLOCK)
+    m_tc = max(1, -(-units_per_pair * pairs // max(1, h_local)))
     plans = []
     if tc:
         plans.append(divide_and_schedule(tc, table, m_tc, search_limit=search_limit))

@@ -1,0 +1,57 @@
+"""Debug: per-CTA timeline (SM, start, end) of one cfg2 decode step with the
+TC and GEMV kernels on concurrent streams -- shows whether GEMV CTAs
+co-reside with the persistent TC CTAs.
+
+    python tools/ctalog.py [budget] [flags]
+"""
+import ctypes as C
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2505_17694_b200 as P  # noqa: E402
+from paper_2505_17694_b200 import _lib, workloads as W  # noqa: E402
+from paper_2505_17694_b200.executor import DecodeStep  # noqa: E402
+
+budget = int(sys.argv[1]) if len(sys.argv) > 1 else 148
+extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+dev = torch.device("cuda")
+spec = W.two_level(32768, 512, 256, h_q=32, h_kv=8, d=128, tensors=False)
+f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+T = f.total_tokens
+kp = (torch.randn((8, T, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
+vp = (torch.randn((8, T, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
+q = (torch.randn((256, 32, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
+plan = P.plan_device(f, 4, P.load_default_profile(), 8, 148, budget)
+step = DecodeStep(f, plan, 32, "bfloat16", flags=1024 | extra, tc_sm_budget=budget, concurrent=True)
+for _ in range(3):
+    step(q, kp, vp)
+torch.cuda.synchronize()
+n = 4 * (4096 + 65536)
+buf = (C.c_longlong * n)()
+_lib.check(_lib.lib().codec_debug_ctalog(buf, n))
+a = np.array(buf, dtype=np.int64).reshape(-1, 4)
+tc = a[:4096][a[:4096, 2] > 0]
+gv = a[4096:][a[4096:, 2] > 0]
+t0 = min(tc[:, 1].min() if len(tc) else 1 << 62, gv[:, 1].min() if len(gv) else 1 << 62)
+us = lambda x: (x - t0) / 1e3
+print(f"TC CTAs {len(tc)}: start {us(tc[:,1]).min():.1f}-{us(tc[:,1]).max():.1f} us, "
+      f"end {us(tc[:,2]).min():.1f}-{us(tc[:,2]).max():.1f} us, SMs {len(set(tc[:,0]))}")
+if len(gv):
+    print(f"GEMV CTAs {len(gv)}: start {us(gv[:,1]).min():.1f}-{us(gv[:,1]).max():.1f} us, "
+          f"end max {us(gv[:,2]).max():.1f} us, SMs {len(set(gv[:,0]))}, "
+          f"dur median {np.median(gv[:,2]-gv[:,1])/1e3:.2f} us")
+    tc_end = tc[:, 2].max() if len(tc) else t0
+    during = gv[gv[:, 1] < tc_end]
+    print(f"GEMV CTAs started while TC ran: {len(during)} on {len(set(during[:,0]))} SMs; "
+          f"SMs shared with a TC CTA: {len(set(during[:,0]) & set(tc[:,0]))}")
+    # GEMV concurrency over time
+    for t in np.linspace(0, us(max(gv[:, 2].max(), tc[:, 2].max() if len(tc) else 0)), 12):
+        tt = t0 + t * 1e3
+        live = ((gv[:, 1] <= tt) & (gv[:, 2] > tt)).sum()
+        tlive = ((tc[:, 1] <= tt) & (tc[:, 2] > tt)).sum() if len(tc) else 0
+        print(f"  t={t:7.1f} us  TC live {tlive:4d}  GEMV live {live:4d}")
