@@ -1,8 +1,8 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 120 python tools/ctalog.py 148 4096 > gpurun_out/ctalog_fused.log 2>&1; echo "ctalog exit $?"
 timeout 300 python bench.py --serial --no-cpu-baseline --steps 10 > gpurun_out/bench_serial.log 2>&1; echo "bench exit $?"
-timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench.log 2>&1; echo "bench exit $?"
-for f in gpurun_out/bench_serial.log gpurun_out/bench.log; do python -c "
+for f in gpurun_out/bench_serial.log; do python -c "
 import json,sys
 for l in open('$f'):
   if l.startswith('{'):

@@ -17,9 +17,10 @@
 // movmatrix.trans per 16 tokens; no TMEM is used, so the kernel co-resides
 // with the tcgen05 kernel (which owns all 512 TMEM columns).
 //
-// Memory path: one producer lane streams the slice with 2D TMA boxes
-// (32 tokens x 64 d, SWIZZLE_128B) of the head-major pool into a 4-stage
-// ring (K and V, 16 KB per stage); the swizzle makes the ldmatrix reads
+// Memory path: one producer lane streams the slice with 3D TMA boxes of
+// 32 whole token rows (8 KB, SWIZZLE_128B; one op each for K and V: the
+// TMA unit's per-op cost, not bytes, limits small boxes) of the head-major
+// pool into a 4-stage ring; the swizzle makes the ldmatrix reads
 // conflict-free. Two consumer warps take 16 tokens of each stage.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -27,6 +28,7 @@
 #include "common.h"
 #include "device_table.h"
 #include "device_util.cuh"
+#include "mma_sync.cuh"
 #include "tc_ptx.cuh"
 
 namespace codec {
@@ -36,41 +38,15 @@ constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
 constexpr int kMmaStages = 4;
 constexpr int kMmaCT = 16 * kMmaWarps;             // tokens per stage
 constexpr int kMmaD = 128;
-constexpr int kMmaBox = kMmaCT * 128;              // one 64-d SW128 box of kMmaCT tokens (4 KB)
-constexpr int kMmaStageBytes = 4 * kMmaBox;        // K (2 boxes) + V (2 boxes)
+constexpr int kMmaBox = kMmaCT * 256;              // one box: kMmaCT whole token rows (8 KB)
+constexpr int kMmaStageBytes = 2 * kMmaBox;        // K box + V box
 constexpr int kMmaSmem = kMmaStages * kMmaStageBytes + 1024 /* align */ + 2 * kMmaStages * 8;
 
-// byte offset of 16-byte chunk c (0..15 along d) of token row r in a K or V
-// stage (two 64-d SW128 boxes of kMmaCT rows)
+// byte offset of 16-byte chunk c (0..15 along d) of token row r in a
+// [rows][2][64] SW128 box (line = 2 r + half, chunk XOR line % 8)
 __device__ __forceinline__ uint32_t mma_sw(int r, int c) {
-  return (c >> 3) * kMmaBox + r * 128 + (((c & 7) ^ (r & 7)) << 4);
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* a) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* a) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void hmma(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
-  uint32_t y;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
+  const int line = 2 * r + (c >> 3);
+  return line * 128 + (((c & 7) ^ (line & 7)) << 4);
 }
 
 __global__ void __launch_bounds__(kMmaThreads, 6)
@@ -113,10 +89,8 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         uint8_t* st = smem + s * kMmaStageBytes;
         const int y = row0 + c * kMmaCT;
         mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
-        tc::tma_load_2d(st, &tmk, 0, y, &full[s]);
-        tc::tma_load_2d(st + kMmaBox, &tmk, 64, y, &full[s]);
-        tc::tma_load_2d(st + 2 * kMmaBox, &tmv, 0, y, &full[s]);
-        tc::tma_load_2d(st + 3 * kMmaBox, &tmv, 64, y, &full[s]);
+        tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
+        tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
       }
     }
   } else {
@@ -145,7 +119,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
     for (int c = 0; c < nch; ++c) {
       const int s = c % kMmaStages;
       mbar_wait(&full[s], (c / kMmaStages) & 1);
-      const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + 2 * kMmaBox;
+      const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + kMmaBox;
       // S^T (16 tokens x 8 heads) = K Q^T
       float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -264,7 +238,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
 }
 
 int32_t cuda_status(cudaError_t e, const char* what);
-int32_t encode_pool_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows);
+int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows);
 
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
@@ -272,8 +246,8 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
-  CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, kMmaCT));
-  CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kMmaCT));
+  CODEC_TRY(encode_pool_rows_map(&mk, k, (int64_t)h_local * pool_tokens, kMmaCT));
+  CODEC_TRY(encode_pool_rows_map(&mv, v, (int64_t)h_local * pool_tokens, kMmaCT));
   cudaError_t e = cudaFuncSetAttribute(mma_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMmaSmem);
   if (e != cudaSuccess) return cuda_status(e, "mma smem attribute");
   e = cudaFuncSetAttribute(mma_pac_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

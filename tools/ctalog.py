@@ -55,3 +55,21 @@ if len(gv):
         live = ((gv[:, 1] <= tt) & (gv[:, 2] > tt)).sum()
         tlive = ((tc[:, 1] <= tt) & (tc[:, 2] > tt)).sum() if len(tc) else 0
         print(f"  t={t:7.1f} us  TC live {tlive:4d}  GEMV live {live:4d}")
+
+# fused kernel: per CTA {TC work drained, suffix warp 0 done, suffix warp 1 done, start}
+fz = a[2048:4096]
+fz = fz[fz[:, 3] > 0]
+if len(fz):
+    print(f"fused: TC done {us(fz[:,0]).min():.1f}-{np.median(us(fz[:,0])):.1f}-{us(fz[:,0]).max():.1f} us (min-med-max); "
+          f"suffix w0 done {us(fz[:,1]).min():.1f}-{np.median(us(fz[:,1])):.1f}-{us(fz[:,1]).max():.1f}; "
+          f"w1 {us(fz[:,2]).min():.1f}-{np.median(us(fz[:,2])):.1f}-{us(fz[:,2]).max():.1f}")
+
+# TC units per pair (table)
+info = step.info
+blob = step.blob_host
+bp = blob[info.off_tc_block_ptr: info.off_tc_block_ptr + info.n_tc_blocks + 1]
+units = np.diff(bp)
+recs = blob[info.off_tc: info.off_tc + 8 * info.n_tc_groups].reshape(-1, 8)
+tiles = [int(sum((recs[j, 4] + 127) // 128 for j in range(bp[b], bp[b + 1]))) for b in range(info.n_tc_blocks)]
+print("TC pairs", info.n_tc_blocks, "units/pair", np.bincount(units).tolist(), "tiles/pair min/med/max",
+      min(tiles), int(np.median(tiles)), max(tiles), "sfx slots", info.n_sfx_slots)
