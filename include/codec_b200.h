@@ -188,6 +188,7 @@ typedef struct {
 #define CODEC_FLAG_FUSE_SUFFIX  4096 /* experimental: suffix groups on the TC kernel's suffix warps (mma.sync)
                                         instead of their own kernel after it (slower on cfg2 so far) */
 #define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* fused TC kernel skips its shared-node units: timing only, wrong output (debug) */
+#define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
@@ -254,6 +255,11 @@ CODEC_API int32_t codec_debug_trace(long long* host, int64_t n);
    TC CTAs at records [0, 4096), GEMV CTAs (blockIdx.y * gridDim.x +
    blockIdx.x) from record 4096 (debug). */
 CODEC_API int32_t codec_debug_ctalog(long long* host, int64_t n);
+/* Per-kernel device times of the calls made with CODEC_FLAG_KERNEL_EVENTS
+   since the last read (profiling; process-global, not reentrant): ms[3 i
+   + k] = call i's TC kernel, suffix + generic kernels, merge kernel.
+   Synchronizes on the recorded events, then clears the ring. */
+CODEC_API int32_t codec_kernel_times(float* ms, int32_t max_calls, int32_t* n_calls);
 
 /* ======================================================================
  * Device primitives with the reference's argument meaning.

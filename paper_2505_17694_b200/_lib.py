@@ -102,6 +102,7 @@ _SIGS = {
     "codec_decode_attention_ex": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P, P]),
     "codec_debug_trace": (I32, [P, I64]),
     "codec_debug_ctalog": (I32, [P, I64]),
+    "codec_kernel_times": (I32, [P, I32, P]),
     "codec_debug_hang_buffer": (I32, [P]),
     "codec_pac": (I32, [I32, P, P, P, P, I64, I64, I64, I64, I64, F64, P, P, P, P]),
     "codec_por": (I32, [I32, I64, I64, P, P, P, P, P, P, P, P, P, P]),

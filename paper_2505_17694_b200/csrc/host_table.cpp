@@ -285,11 +285,18 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     if (!fuse) m_tc = (int32_t)std::min<int64_t>(m_tc, n_units);  // fused: every pair runs suffix work
     std::vector<int64_t> cost(tcg.size());
     for (size_t i = 0; i < tcg.size(); ++i) cost[i] = (tcg[i].max_vis + 63) / 64;
-    // units in (cost desc, group, head) order
+    // units in (cost desc, KV slice, head) order: the row chunks of one
+    // (slice, head) -- they read the same K/V tiles -- land on consecutive
+    // pairs of the same LPT round and run concurrently, so their tiles are
+    // read from HBM once and from L2 by the others
     std::vector<int64_t> order(n_units);
     for (int64_t u = 0; u < n_units; ++u) order[u] = u;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return cost[a / h_local] > cost[b / h_local]; });
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      const Grp &ga = tcg[a / h_local], &gb = tcg[b / h_local];
+      if (cost[a / h_local] != cost[b / h_local]) return cost[a / h_local] > cost[b / h_local];
+      if (ga.kv_tok != gb.kv_tok) return ga.kv_tok < gb.kv_tok;
+      return a % h_local < b % h_local;
+    });
     std::vector<int64_t> load(std::max(m_tc, 1), 0);
     std::vector<std::vector<int64_t>> per_block(std::max(m_tc, 1));
     for (int64_t u : order) {

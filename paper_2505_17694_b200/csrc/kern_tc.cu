@@ -65,9 +65,9 @@ constexpr int kSfxStage = 2 * kSfxBox;       // K box + V box
 
 // Two builds of the kernel. Plain: 12 warps (softmax x 8, K / MMA / V / Q),
 // 384 x 168 registers at launch, setmaxnreg 200 / 96, K and V rings of 4
-// and 6 half-tiles. Fused (CODEC_FLAG_FUSE_SUFFIX): + a suffix warpgroup
+// and 5 half-tiles. Fused (CODEC_FLAG_FUSE_SUFFIX): + a suffix warpgroup
 // running the GEMV groups on mma.sync (sfx_run), 512 x 128 at launch,
-// setmaxnreg 176 / 64 / 96 (per SMSP 2 x 176 + 64 + 96 = 512), 3 + 3
+// setmaxnreg 176 / 64 / 96 (per SMSP 2 x 176 + 64 + 96 = 512), 3 + 2
 // half-tile rings to make room for the suffix rings. Either way one CTA
 // owns its SM: the setmaxnreg hand-off corrupted the registers of a
 // co-resident CTA of another kernel in testing.
@@ -75,7 +75,7 @@ template <bool F>
 struct TcCfg {
   static constexpr int Threads = 32 * (kTcSoftmaxWarps + (F ? 8 : 4));
   static constexpr int RegsSoftmax = F ? 176 : 200, RegsOther = F ? 64 : 96, RegsSfx = 96;
-  static constexpr int KStages = F ? 3 : 4, VStages = F ? 3 : 6;
+  static constexpr int KStages = F ? 3 : 4, VStages = F ? 2 : 5;
   static constexpr int OffQ = 0;             // Q0, Q1 (double-buffered across units)
   static constexpr int OffK = OffQ + 2 * kQBytes;
   static constexpr int OffV = OffK + KStages * kHalfBytes;
@@ -96,6 +96,7 @@ struct TcBars {
   uint64_t k_full[KS], k_empty[KS];
   uint64_t v_full[VS], v_empty[VS];
   uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], p_full[2];
+  uint64_t epi_done[2];  // unit n's epilogue no longer uses Q buffer n % 2 as staging
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4] (parity waits stay within one phase)
   uint64_t o_free;
   uint64_t sfx_full[kTcSfxWarps][kSfxStages];
@@ -489,6 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 2);  // the Q warps of both CTAs
       mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->epi_done[i], 4);  // the epilogue group's 4 warps (this CTA)
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], kGroupWarpArrivals);
       mbar_init(&bars->p_full[i], kGroupWarpArrivals);
@@ -587,8 +589,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       if (gv.n_tiles == 0) continue;
+      if (n == 0) {  // the first unit's Q is gathered by the softmax warps (lower latency)
+        ++n;
+        continue;
+      }
       const int qb = n & 1;
-      if (n >= 2) mbar_wait(&bars->q_empty[qb], ((n - 2) >> 1) & 1);
+      if (n >= 2) {
+        mbar_wait(&bars->q_empty[qb], ((n - 2) >> 1) & 1);
+        mbar_wait(&bars->epi_done[qb], ((n - 2) >> 1) & 1);  // staging of unit n - 2's O
+      }
       uint8_t* qs = smem + kOffQ + qb * kQBytes;
 #pragma unroll 1
       for (int i0 = 0; i0 < 64; i0 += 8) {
@@ -653,13 +662,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         sc.next();
         ++ts;
       };
-      issue_s();
-      issue_s();
-      // Issue order S(k+2), PV(k-1), S(k+3), PV(k), ...: the order the
-      // softmax releases its inputs in steady state (it frees S(k) ~one
-      // exponential phase before P(k-1) of the other group is written), so
-      // blocking waits in this order never hold back the other stream.
-      // Deadlock-free: each wait depends only on MMAs issued earlier.
+      // Polling scheduler: issue S(ts) or PV(tp), whichever is ready, S
+      // first. A fixed order would deadlock at short units: PV(tl) (ending
+      // unit n) would queue behind S(tl + 3), whose Q (unit n + 2) waits
+      // for unit n's epilogue, which waits for PV(tl). Parity probes are
+      // exact: each barrier's next phase depends on an MMA not yet issued.
       TileCursor pc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
       pc.open();
       auto issue_pv = [&](int tp) {
@@ -683,20 +690,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         if (lane == 0) stamp(1, tp);
         pc.next();
       };
-      for (int k = 0; !pc.done(); ++k) {
-        if (!sc.done()) {
-          PROG(0, ts, 1);
-          mbar_wait(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1);  // both CTAs pulled S(ts-2) out of TMEM
+      auto s_ready = [&]() {
+        if (ts >= 2 && !tc::mbar_ready(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1)) return false;
+        if (sc.j == 0 && !tc::mbar_ready(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1)) return false;
+        return tc::mbar_ready(&bars->k_full[ts % kTcKStages], (ts / kTcKStages) & 1);
+      };
+      auto pv_ready = [&](int tp) {
+        if (!tc::mbar_ready(&bars->p_full[tp & 1], (tp >> 1) & 1)) return false;
+        if (!tc::mbar_ready(&bars->v_full[tp % kTcVStages], (tp / kTcVStages) & 1)) return false;
+        return pc.j != 0 || pc.n == 0 || tc::mbar_ready(&bars->o_free, (pc.n - 1) & 1);
+      };
+      int tp = 0;
+      while (!pc.done()) {
+        if (!sc.done() && s_ready()) {
           if (lane == 0) stamp(8, ts);
-          PROG(0, ts, 2);
           if (lane == 0) stamp(13, ts);
           issue_s();
           if (lane == 0) stamp(6, ts - 3);
+          continue;
         }
-        if (k >= 1 && !pc.done()) {
-          PROG(0, k - 1, 4);
-          issue_pv(k - 1);
+        if (tp < ts && pv_ready(tp)) {
+          if (lane == 0) stamp(10, tp);
+          issue_pv(tp);
+          ++tp;
+          continue;
         }
+        __nanosleep(20);
       }
       PROG(0, 9999, 7);
     }
@@ -723,6 +742,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
     };
     int gi = g_begin;
     while (gi < g_end && group_view(table, off_groups, off_rows, gi).n_tiles == 0) ++gi;
+    if (gi < g_end && grp == 0) {
+      // first unit's Q: one row per thread of group A, all 16 loads in flight
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      const int ridx = grow / g;
+      const bool valid = ridx < gv.n_req;
+      const int req = valid ? __ldg(gv.rows + ridx * kRowInts) : 0;
+      const uint4* src = reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + gv.kh * g + (grow % g)) * kTcD);
+      uint4 v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = valid ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      uint8_t* qs = smem + kOffQ;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) *reinterpret_cast<uint4*>(qs + sw128(r, c)) = v[c];
+      tc::fence_proxy_async_smem();
+      named_sync(11, 128);
+      if (tid == 0) tc::mbar_arrive_cluster(&bars->q_full[0], 0);
+    }
     // total tiles of the block (the last tile publishes no row max)
     int t_total = 0;
     for (int x = gi; x < g_end; ++x) t_total += group_view(table, off_groups, off_rows, x).n_tiles;
@@ -741,6 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         if ((t & 1) != grp) continue;
         const int b = t & 1;
         if (quad == 0) PROG(1 + grp, t, 1);
+        if (tid == grp * 128) stamp(14, t);
         mbar_wait(&bars->s_full[b], (t >> 1) & 1);
         if (quad == 0) PROG(1 + grp, t, 2);
         tc::fence_after();
@@ -881,49 +918,79 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         if (lane == 0 && quad == 3) stamp(7, t);
         if (lane == 0) tc::mbar_arrive_cluster(&bars->p_full[b], 0);
       }
-      // ---- epilogue: the group that ran the last tile writes O / l
-      // (both groups' 256 threads meet on a barrier alternating with the
-      // group parity, so one group's next epilogue never joins this one)
-      const int last = (t - 1) & 1, l_bar = 9 + (n & 1);
+      // ---- epilogue: the group that ran the unit's last tile reads all of
+      // O out of TMEM into registers, releases the accumulator (o_free: the
+      // next unit's first PV may start) and only then writes to global
+      // memory. (Both groups waiting for the last PV would deadlock: it is
+      // issued after S(tl + 3), which needs the other group's next tile.)
+      // The l / m barrier alternates with the unit parity so one epilogue
+      // never joins the next.
+      const int tl = t - 1, last = tl & 1, l_bar = 9 + (n & 1);
       if (quad == 0) PROG(1 + grp, t, 7);
       if (grp != last) {
         lx[r] = make_float2(have ? l : 0.f, my_m);
         named_arrive(l_bar, 256);
       } else {
         named_sync(l_bar, 256);
+        if (tid == grp * 128) stamp(16, tl);
         const float2 o2 = lx[r];
         const float l_run = l + (o2.x > 0.f ? o2.x * fast_exp2(o2.y - my_m) : 0.f);
-        const int tl = t - 1;  // PV(tl) landed => the whole group landed (PV(tl-4) is done)
+        // PV(tl) landed => the whole unit landed (PV(tl - 4) is done)
         mbar_wait(&bars->pv_done[tl & 3], (tl >> 2) & 1);
         tc::fence_after();
-        float* dst = nullptr;
-        if (valid) {
-          if (slot < 0) {
-            dst = out + ((int64_t)req * hq_local + qh) * kTcD;
-          } else {
-            const int64_t ei = (int64_t)slot * hq_local + qh;
-            dst = part_o + ei * kTcD;
-            part_ml[2 * ei] = my_m * 0.69314718055994530942f;  // natural-log units
-            part_ml[2 * ei + 1] = l_run;
-          }
-        }
-        const float inv = 1.f / l_run;
+        uint32_t o[128];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tc::tmem_ld32(tmem + lane_addr + kColO + c * 32, o);
-          tc::wait_ld();
-          if (valid) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              *reinterpret_cast<float4*>(dst + c * 32 + i) =
-                  make_float4(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv,
-                              __uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          }
-        }
+        for (int c = 0; c < 4; ++c) tc::tmem_ld32(tmem + lane_addr + kColO + c * 32, o + c * 32);
+        tc::wait_ld();
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(&bars->o_free, 0);
+        if (tid == grp * 128) stamp(15, tl);
+        // Write O through this unit's Q buffer (its S MMAs are complete) as a
+        // staging area, 64 rows per pass: thread-per-row global stores touch
+        // 32 lines per instruction; from SMEM each row goes out as one fully
+        // coalesced 512-byte warp store. Chunk c of staging row x lives at
+        // c ^ (x % 32): conflict-free both ways.
+        {
+          float4* stg = reinterpret_cast<float4*>(smem + kOffQ + (n & 1) * kQBytes);
+          long long* rdst = reinterpret_cast<long long*>(smem + kOffMpub + grp * 512);  // this group's free mpub half
+          float* dst = nullptr;
+          const float inv = 1.f / l_run;
+          if (valid) {
+            if (slot < 0) {
+              dst = out + ((int64_t)req * hq_local + qh) * kTcD;
+            } else {
+              const int64_t ei = (int64_t)slot * hq_local + qh;
+              dst = part_o + ei * kTcD;
+              part_ml[2 * ei] = my_m * 0.69314718055994530942f;  // natural-log units
+              part_ml[2 * ei + 1] = l_run;
+            }
+          }
+          const int wq = warp & 3;
+#pragma unroll 1
+          for (int pass = 0; pass < 2; ++pass) {
+            if ((quad >> 1) == pass) {
+              const int x = (quad & 1) * 32 + lane;  // staging row
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                stg[x * 32 + (c ^ lane)] =
+                    make_float4(__uint_as_float(o[4 * c]) * inv, __uint_as_float(o[4 * c + 1]) * inv,
+                                __uint_as_float(o[4 * c + 2]) * inv, __uint_as_float(o[4 * c + 3]) * inv);
+              rdst[x] = reinterpret_cast<long long>(dst);
+            }
+            named_sync(12, 128);
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+              const int x = wq * 16 + i;
+              float* d = reinterpret_cast<float*>(rdst[x]);
+              if (d) reinterpret_cast<float4*>(d)[lane] = stg[x * 32 + (lane ^ (x & 31))];
+            }
+            named_sync(12, 128);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->epi_done[n & 1]);
+          if (tid == grp * 128) stamp(9, tl);
+        }
       }
       if (quad == 0) PROG(1 + grp, t, 8);
     }
@@ -1021,7 +1088,7 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
   return CODEC_OK;
 }
 
-constexpr int kTraceLen = 14 * 2 * 64;
+constexpr int kTraceLen = 17 * 2 * 64;
 static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
 
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,

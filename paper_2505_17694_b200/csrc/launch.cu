@@ -60,6 +60,39 @@ namespace {
 long long* g_ctalog = nullptr;  // debug CTA log (CODEC_FLAG_CTALOG), one per process
 }
 
+// Profiling (CODEC_FLAG_KERNEL_EVENTS): CUDA events around each kernel of a
+// call on the caller's stream, so a benchmark can time every kernel inside
+// its own timed region. Process-global ring; not for concurrent callers.
+constexpr int kEvCalls = 512;
+struct KernelEvents {
+  cudaEvent_t ev[kEvCalls][4] = {};
+  int n = 0;
+};
+KernelEvents g_kev;
+int32_t kev_record(int slot, cudaStream_t st) {
+  if (g_kev.n >= kEvCalls) return CODEC_OK;  // ring full: drop
+  cudaEvent_t& e = g_kev.ev[g_kev.n][slot];
+  if (!e && cudaEventCreate(&e) != cudaSuccess) return fail(CODEC_ERR_CUDA, "event create");
+  if (cudaEventRecord(e, st) != cudaSuccess) return fail(CODEC_ERR_CUDA, "event record");
+  return CODEC_OK;
+}
+
+extern "C" int32_t codec_kernel_times(float* ms, int32_t max_calls, int32_t* n_calls) {
+  if (!ms || !n_calls) return fail(CODEC_ERR_VALUE, "NULL argument");
+  const int n = g_kev.n < max_calls ? g_kev.n : max_calls;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < 3; ++k) {
+      float t = 0.f;
+      if (cudaEventSynchronize(g_kev.ev[i][k + 1]) != cudaSuccess ||
+          cudaEventElapsedTime(&t, g_kev.ev[i][k], g_kev.ev[i][k + 1]) != cudaSuccess)
+        return fail(CODEC_ERR_CUDA, "event read");
+      ms[3 * i + k] = t;
+    }
+  *n_calls = n;
+  g_kev.n = 0;
+  return CODEC_OK;
+}
+
 extern "C" int32_t codec_debug_ctalog(long long* host, int64_t n) {
   if (!g_ctalog) return fail(CODEC_ERR_VALUE, "no CTA log recorded");
   if (n > 4 * (int64_t)kCtaLogLen) n = 4 * (int64_t)kCtaLogLen;
@@ -109,9 +142,12 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
     if (cudaEventRecord(fj->fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fj->fork, 0) != cudaSuccess)
       return fail(CODEC_ERR_CUDA, "fork failed");
   }
+  const bool kev = (dims->flags & CODEC_FLAG_KERNEL_EVENTS) && !fork;
+  if (kev) CODEC_TRY(kev_record(0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
                         dims->flags, ctalog));
+  if (kev) CODEC_TRY(kev_record(1, st));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, st, ctalog));
@@ -119,6 +155,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
                           ctalog));
+  if (kev) CODEC_TRY(kev_record(2, st));
   if (do_gen)
     CODEC_TRY(launch_generic_groups(dims->kv_dtype, table_dev, info->n_gen_groups, info->off_gen, info->off_rows, q,
                                     k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, side));
@@ -128,6 +165,10 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   }
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st));
+  if (kev) {
+    CODEC_TRY(kev_record(3, st));
+    ++g_kev.n;
+  }
   return CODEC_OK;
 }
 

@@ -16,9 +16,9 @@ plan = P.plan_device(f, 4, P.load_default_profile(), 8)
 step = DecodeStep(f, plan, 32, 'bfloat16', flags=128 | 8 | 32 | 64 | int(sys.argv[1] if len(sys.argv) > 1 else 0), concurrent=False)
 for _ in range(3): step(q, kp, vp)
 torch.cuda.synchronize()
-buf = (C.c_longlong * 1792)()
-_lib.check(_lib.lib().codec_debug_trace(buf, 1792))
-a = np.array(buf, dtype=np.int64).reshape(14, 2, 64)
+buf = (C.c_longlong * 2176)()
+_lib.check(_lib.lib().codec_debug_trace(buf, 2176))
+a = np.array(buf, dtype=np.int64).reshape(17, 2, 64)
 t0 = a[a > 0].min()
 a = np.where(a > 0, a - t0, -1)
 # a[event, cta rank, tile]: 0 MMA saw P(t), 1 MMA issued PV(t), 2 softmax saw S(t),
@@ -46,3 +46,12 @@ print('S(ts): s_free seen - last s_free release:', a[8, 0, 2:n] - np.maximum(a[4
 print('S(ts) issue duration:', a[6, 0, :n - 2] - a[13, 0, 2:n])
 print('PV issue(t-2) -> softmax P-buffer wait done (t):', a[12, 0, 2:n] - a[1, 0, :n - 2])
 print('softmax m settled -> P-buffer wait done:', a[12, 0, :n] - a[5, 0, :n])
+
+np.set_printoptions(linewidth=250)
+print('ready(t) -> saw S(t):', (a[2, 0, :n] - a[14, 0, :n]).tolist())
+print('rel P(t-2) [same group] -> ready(t):', (a[14, 0, 2:n] - a[3, 0, :n - 2]).tolist())
+ep = np.nonzero(a[15, 0] > 0)[0]
+for t in ep:
+    print(f'unit ends at tile {t}: epi start {a[16,0,t]-a[3,0,t]} after rel P(last); epi took {a[15,0,t]-a[16,0,t]}; '
+          f'staging+copy {a[9,0,t]-a[15,0,t]}; next ready {a[14,0,t+2]-a[9,0,t] if t+2<64 else None}; '
+          f'next PV issue (MMA saw P) {a[0,0,t+1]-a[15,0,t] if t+1<64 else None}')
