@@ -385,20 +385,67 @@ def main():
 
     e2e = None
     if not args.quick:
-        out_host = torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32).pin_memory()
-        qd2 = torch.empty_like(q_dev)
+        # Serving-style pipeline through the public API: every step uploads
+        # its queries from pinned host memory and reads its output back;
+        # step k's copies run on their own streams, overlapping the compute
+        # of steps k - 1 / k + 1 (double-buffered device q / out).
+        s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        qbuf = [torch.empty_like(q_dev) for _ in range(2)]
+        obuf = [torch.empty_like(out) for _ in range(2)]
+        ohost = [torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
+        gath2 = [torch.empty_like(gathered) for _ in range(2)] if world > 1 else None
+        st8 = {"k": 0}
 
         def e2e_step():
-            qd2.copy_(q_host, non_blocking=True)
-            one_step(qd2)
-            out_host.copy_(out, non_blocking=True)
+            k = st8["k"]
+            sl = k & 1
+            st8["k"] += 1
+            with torch.cuda.stream(s_h2d):
+                if k >= 2:
+                    s_h2d.wait_event(ev["comp"][sl])
+                qbuf[sl].copy_(q_host, non_blocking=True)
+                ev["h2d"][sl].record(s_h2d)
+            stream.wait_event(ev["h2d"][sl])
+            if k >= 2:
+                stream.wait_event(ev["d2h"][sl])
+            step(qbuf[sl], kp, vp, out=obuf[sl], stream=stream)
+            res = obuf[sl]
+            if world > 1:
+                dist.all_gather_into_tensor(gath2[sl], obuf[sl])
+            ev["comp"][sl].record(stream)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev["comp"][sl])
+                ohost[sl].copy_(res, non_blocking=True)
+                ev["d2h"][sl].record(s_d2h)
 
-        for _ in range(3):
-            e2e_step()
-        e2e_ms = timed(args.steps, e2e_step)[0]
+        def e2e_window(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            e0.record(stream)
+            s_h2d.wait_event(e0)
+            st8["k"] = 0
+            for _ in range(n):
+                e2e_step()
+            stream.wait_stream(s_d2h)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / n
+            if world > 1:
+                t = torch.tensor([ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            return ms
+
+        e2e_window(3)
+        e2e_ms = statistics.median(e2e_window(args.steps) for _ in range(5))
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": q_host.numel() * q_host.element_size(),
-               "d2h_bytes_per_step": out_host.numel() * out_host.element_size()}
+               "d2h_bytes_per_step": ohost[0].numel() * ohost[0].element_size(),
+               "pipeline": "per step: pinned H2D of q, decode step, D2H of out; copies on their own streams "
+                           "overlap the neighbouring steps' compute (double-buffered)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:

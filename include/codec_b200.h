@@ -185,9 +185,7 @@ typedef struct {
 #define CODEC_FLAG_DBG_NO_EXP   512  /* TC softmax skips the exponentials: timing only, wrong output (debug) */
 #define CODEC_FLAG_CTALOG       1024 /* record {smid, start ns, end ns, cta} per TC / GEMV CTA (debug) */
 #define CODEC_FLAG_GEMV_SIMT    2048 /* suffix groups on the CUDA-core GEMV kernel instead of the mma.sync one */
-#define CODEC_FLAG_FUSE_SUFFIX  4096 /* experimental: suffix groups on the TC kernel's suffix warps (mma.sync)
-                                        instead of their own kernel after it (slower on cfg2 so far) */
-#define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* fused TC kernel skips its shared-node units: timing only, wrong output (debug) */
+#define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* TC kernel skips its shared-node units: timing only, wrong output (debug) */
 #define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
 
 typedef struct codec_table codec_table;
@@ -206,10 +204,7 @@ typedef struct {
   int32_t off_merge_req, off_merge_ptr, off_merge_slot;
   int32_t h_local;                                     /* head_end - head_begin */
   int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTA pairs, their (group, head) unit CSR */
-  int32_t max_merge;                                   /* most partials of one merged request */
-  int32_t n_sfx_slots;                                 /* fused: suffix warp slots of the TC grid (0: separate kernel) */
-  int32_t off_sfx_ptr, off_sfx_item;                   /* fused: slot -> (GEMV group * h_local + head) CSR */
-  int32_t reserved;
+  int32_t max_merge, reserved;                         /* most partials of one merged request */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

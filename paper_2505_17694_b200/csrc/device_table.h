@@ -33,8 +33,6 @@ constexpr int kTcMinRows = 16;
 constexpr int kTcGroupRows = 256;
 // SMs (CTAs) that run one tensor-core schedule block
 constexpr int kTcCtasPerBlock = 2;
-// suffix (GEMV-group) warps of each fused TC CTA
-constexpr int kTcSfxWarps = 2;
 
 // debug CTA log (CODEC_FLAG_CTALOG): TC records first, GEMV from this index
 constexpr int kCtaLogGemv = 4096;

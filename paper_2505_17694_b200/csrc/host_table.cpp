@@ -247,15 +247,6 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   in.h_local = dims->head_end - dims->head_begin;
   in.max_merge = max_merge;
   in.gemv_rows = gemv_rows;
-  // fused suffix path: the TC kernel's suffix warps run the GEMV groups
-  // (mma.sync) on every SM while the shared nodes run on tcgen05
-  int32_t n_gemv_groups = 0, n_tc_groups0 = 0;
-  for (auto& gr : groups) {
-    n_gemv_groups += gr.kind == kKindGemv;
-    n_tc_groups0 += gr.kind == kKindTc;
-  }
-  const bool fuse = n_tc_groups0 > 0 && n_gemv_groups > 0 && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
-                    (dims->flags & CODEC_FLAG_FUSE_SUFFIX) && !(dims->flags & CODEC_FLAG_GEMV_SIMT);
   std::vector<int32_t>& blob = t->blob;
   auto emit_groups = [&](int kind, int32_t& count, int32_t& offset) {
     offset = (int32_t)blob.size();
@@ -282,7 +273,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     const int32_t h_local = dims->head_end - dims->head_begin;
     const int64_t n_units = (int64_t)tcg.size() * h_local;
     int32_t m_tc = std::max(1, sms / kTcCtasPerBlock);
-    if (!fuse) m_tc = (int32_t)std::min<int64_t>(m_tc, n_units);  // fused: every pair runs suffix work
+    m_tc = (int32_t)std::min<int64_t>(m_tc, n_units);
     std::vector<int64_t> cost(tcg.size());
     for (size_t i = 0; i < tcg.size(); ++i) cost[i] = (tcg[i].max_vis + 63) / 64;
     // units in (cost desc, KV slice, head) order: the row chunks of one
@@ -323,40 +314,6 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     blob.insert(blob.end(), block_ptr.begin(), block_ptr.end());
   }
   emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
-  // ---- fused suffix items: (GEMV group, local head), LPT by visible tokens
-  // onto the suffix warp slots of the TC grid (kTcSfxWarps per CTA)
-  in.n_sfx_slots = 0;
-  if (fuse) {
-    const int32_t h_local = dims->head_end - dims->head_begin;
-    const int32_t n_slots_sfx = in.n_tc_blocks * kTcCtasPerBlock * kTcSfxWarps;
-    std::vector<int64_t> cost;
-    for (auto& gr : groups)
-      if (gr.kind == kKindGemv) cost.push_back(gr.max_vis + 64);  // + per-item overhead
-    const int64_t n_items = (int64_t)cost.size() * h_local;
-    std::vector<int64_t> order(n_items);
-    for (int64_t u = 0; u < n_items; ++u) order[u] = u;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return cost[a / h_local] > cost[b / h_local]; });
-    std::vector<int64_t> load(n_slots_sfx, 0);
-    std::vector<std::vector<int32_t>> per_slot(n_slots_sfx);
-    for (int64_t u : order) {
-      int32_t best = 0;
-      for (int32_t b = 1; b < n_slots_sfx; ++b)
-        if (load[b] < load[best]) best = b;
-      load[best] += cost[u / h_local];
-      per_slot[best].push_back((int32_t)u);  // group * h_local + head
-    }
-    in.n_sfx_slots = n_slots_sfx;
-    in.off_sfx_ptr = (int32_t)blob.size();
-    int32_t acc = 0;
-    blob.push_back(0);
-    for (auto& v : per_slot) {
-      acc += (int32_t)v.size();
-      blob.push_back(acc);
-    }
-    in.off_sfx_item = (int32_t)blob.size();
-    for (auto& v : per_slot) blob.insert(blob.end(), v.begin(), v.end());
-  }
   emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
   in.off_rows = (int32_t)blob.size();
   in.n_rows = (int32_t)(rows.size() / 4);

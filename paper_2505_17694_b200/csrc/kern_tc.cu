@@ -48,7 +48,7 @@ constexpr int kTcProducerWarp = kTcSoftmaxWarps;       // K loads
 constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
 constexpr int kTcVProducerWarp = kTcSoftmaxWarps + 2;  // V loads (own warp: K must not queue behind V)
 constexpr int kTcQWarp = kTcSoftmaxWarps + 3;          // gathers the next unit's Q rows into SMEM
-constexpr int kTcSfxWarp0 = kTcSoftmaxWarps + 4;       // suffix warpgroup (kTcSfxWarps active; fused only)
+constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 4);
 constexpr int kTcBN = 128;                   // tokens per KV tile
 constexpr int kTcD = 128;                    // head dim
 constexpr int kTcPrefetch = 4;               // tiles ahead the producer warms L2
@@ -56,50 +56,33 @@ constexpr int kQBytes = 128 * 128 * 2;       // this CTA's 128-row Q tile (32 KB
 constexpr int kQAtom = kQBytes / 2;          // Q atom column: 128 rows x 64 d (16 KB)
 constexpr int kHalfBytes = 64 * 128 * 2;     // this CTA's half of a K or V tile (16 KB)
 constexpr int kKAtom = kHalfBytes / 2;       // K-half atom column: 64 tokens x 64 d (8 KB)
-// suffix rings (fused only): per suffix warp kSfxStages chunks of kSfxCT token rows, K box + V box
-constexpr int kSfxCT = 32, kSfxStages = 2;  // two m16 token tiles per chunk
-constexpr int kSfxTiles = kSfxCT / 16;
-constexpr int kSfxPrefetchChunks = 4;       // L2 prefetch granule (one 1D bulk prefetch of K and of V)
-constexpr int kSfxBox = kSfxCT * 256;        // one TMA box: kSfxCT whole token rows
-constexpr int kSfxStage = 2 * kSfxBox;       // K box + V box
-
-// Two builds of the kernel. Plain: 12 warps (softmax x 8, K / MMA / V / Q),
-// 384 x 168 registers at launch, setmaxnreg 200 / 96, K and V rings of 4
-// and 5 half-tiles. Fused (CODEC_FLAG_FUSE_SUFFIX): + a suffix warpgroup
-// running the GEMV groups on mma.sync (sfx_run), 512 x 128 at launch,
-// setmaxnreg 176 / 64 / 96 (per SMSP 2 x 176 + 64 + 96 = 512), 3 + 2
-// half-tile rings to make room for the suffix rings. Either way one CTA
-// owns its SM: the setmaxnreg hand-off corrupted the registers of a
-// co-resident CTA of another kernel in testing.
-template <bool F>
-struct TcCfg {
-  static constexpr int Threads = 32 * (kTcSoftmaxWarps + (F ? 8 : 4));
-  static constexpr int RegsSoftmax = F ? 176 : 200, RegsOther = F ? 64 : 96, RegsSfx = 96;
-  static constexpr int KStages = F ? 3 : 4, VStages = F ? 2 : 5;
-  static constexpr int OffQ = 0;             // Q0, Q1 (double-buffered across units)
-  static constexpr int OffK = OffQ + 2 * kQBytes;
-  static constexpr int OffV = OffK + KStages * kHalfBytes;
-  static constexpr int OffSfx = OffV + VStages * kHalfBytes;
-  static constexpr int OffMpub = OffSfx + (F ? kTcSfxWarps * kSfxStages * kSfxStage : 0);  // [2][128] f32 row max
-  static constexpr int OffLx = OffMpub + 2 * 128 * 4;  // [128 rows] float2 (l, m) at a unit's end
-  static constexpr int OffBar = OffLx + 128 * 8;
-  static constexpr int Smem = OffBar + 512;
-  static_assert(Smem <= 232448, "exceeds the 227 KB opt-in shared memory");
-};
+// One CTA owns its SM: 384 threads x 168 registers at launch, then
+// setmaxnreg moves the role warps' surplus to the softmax warps (per SMSP:
+// 2 softmax warps x 200 + 1 role warp x 96 <= 512). No other kernel may
+// share the SM: the hand-off corrupted the registers of a co-resident CTA
+// of another kernel in testing (tools/determinism.py).
+constexpr int kTcRegsSoftmax = 200, kTcRegsOther = 96;
+constexpr int kTcKStages = 4, kTcVStages = 6;
+constexpr int kOffQ = 0;                     // Q0, Q1 (double-buffered across units)
+constexpr int kOffK = kOffQ + 2 * kQBytes;
+constexpr int kOffV = kOffK + kTcKStages * kHalfBytes;
+constexpr int kOffMpub = kOffV + kTcVStages * kHalfBytes;  // [2 groups][128 rows] f32 published row max
+constexpr int kOffLx = kOffMpub + 2 * 128 * 4;             // [128 rows] float2 (l, m) at a unit's end
+constexpr int kOffBar = kOffLx + 128 * 8;
+constexpr int kTcSmem = kOffBar + 512;
+static_assert(kTcSmem <= 232448, "exceeds the 227 KB opt-in shared memory");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr float kRescaleLog2 = 8.f;
 constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 
-template <int KS, int VS>
 struct TcBars {
-  uint64_t k_full[KS], k_empty[KS];
-  uint64_t v_full[VS], v_empty[VS];
+  uint64_t k_full[kTcKStages], k_empty[kTcKStages];
+  uint64_t v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], p_full[2];
   uint64_t epi_done[2];  // unit n's epilogue no longer uses Q buffer n % 2 as staging
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4] (parity waits stay within one phase)
   uint64_t o_free;
-  uint64_t sfx_full[kTcSfxWarps][kSfxStages];
   uint32_t tmem_slot;
 };
 
@@ -200,256 +183,8 @@ struct TileCursor {
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// ------------------------------------------------------------------ suffix warps
-// One suffix warp runs its list of (GEMV group, kv head) items -- a request's
-// unshared suffix slice for one kv head -- with the mma.sync math of
-// kern_mma.cu (S^T = K Q^T, O^T += V^T P^T, m16n8k16, heads padded to 8),
-// while the rest of the CTA runs the tcgen05 shared-node units: the
-// suffix stream keeps HBM busy and costs ~3.5 warp instructions per token,
-// so it hides under the tensor-bound softmax. The warp is its own producer:
-// lane 0 keeps kSfxStages 16-token chunks in flight through TMA (SW128
-// boxes), continuing into the next item before the current one ends.
-// byte offset of 16-byte chunk c (0..15 along d) of token row r in a
-// [rows][2][64] SW128 box: line = 2 r + half, chunk XOR (line % 8)
-__device__ __forceinline__ uint32_t row_sw(int r, int c) {
-  const int line = 2 * r + (c >> 3);
-  return line * 128 + (((c & 7) ^ (line & 7)) << 4);
-}
-__device__ __forceinline__ uint32_t sfx_sw(int r, int c) { return row_sw(r, c); }
-
-struct SfxItem {
-  int req, n_tok, slot, kh, row0;
-};
-
-__device__ __forceinline__ SfxItem sfx_item(const int32_t* table, int off_gemv, int off_rows, int h_local,
-                                            int64_t pool_tokens, int code) {
-  const int gi = code / h_local, kh = code % h_local;
-  const int32_t* grp = table + off_gemv + gi * kGroupInts;
-  const int32_t* row = table + off_rows + grp[kGrpRowBegin] * kRowInts;
-  SfxItem it;
-  it.req = row[0];
-  it.n_tok = row[1];
-  it.slot = row[2];
-  it.kh = kh;
-  it.row0 = kh * (int)pool_tokens + grp[kGrpKvTok];
-  return it;
-}
-
-__device__ __forceinline__ void sfx_run(const CUtensorMap* tmk, const CUtensorMap* tmv, const int32_t* __restrict__ table,
-                                     int off_gemv, int off_rows, const int32_t* __restrict__ items, int n_items,
-                                     int h_local, const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g,
-                                     int hq_local, float* __restrict__ out, float* __restrict__ part_o,
-                                     float* __restrict__ part_ml, uint8_t* ring, uint64_t* full,
-                                     const __nv_bfloat16* __restrict__ kpool, const __nv_bfloat16* __restrict__ vpool) {
-  const int lane = threadIdx.x & 31;
-  const int gid = lane >> 2, tig = lane & 3;
-  // producer cursor (item, chunk) and the global chunk sequence number
-  int p_it = 0, p_c = 0, p_nch = 0, p_row0 = 0, k_issue = 0;
-  // L2 prefetch of whole chunks kSfxPrefetch ahead of the TMA loads: the
-  // SMEM ring holds only kSfxStages chunks, too few to cover HBM latency
-  // under the tensor-core kernel's load by themselves
-  auto prefetch = [&](int row0, int tok0, int ntok) {
-#ifdef CODEC_DBG_NO_SFX_PREFETCH
-    return;
-#endif
-    if (lane == 0 && ntok > 0) {
-      const uint32_t bytes = (uint32_t)ntok * kTcD * 2;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kpool + (int64_t)(row0 + tok0) * kTcD), "r"(bytes)
-                   : "memory");
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vpool + (int64_t)(row0 + tok0) * kTcD), "r"(bytes)
-                   : "memory");
-    }
-  };
-  int p_ntok = 0;
-  auto p_open = [&]() {
-    for (; p_it < n_items; ++p_it) {
-      const SfxItem it = sfx_item(table, off_gemv, off_rows, h_local, pool_tokens, items[p_it]);
-      p_nch = (it.n_tok + kSfxCT - 1) / kSfxCT;
-      p_row0 = it.row0;
-      p_ntok = it.n_tok;
-      if (p_nch > 0) return;
-    }
-  };
-  auto issue = [&]() {
-    if (p_it >= n_items) return;
-    const int st = k_issue % kSfxStages;
-    // this warp's ldmatrix reads of the stage (generic proxy) before the TMA overwrite
-    __syncwarp();
-#ifndef CODEC_DBG_NO_SFX_FENCE
-    tc::fence_proxy_async_smem();
-#endif
-    if (lane == 0) {
-      uint8_t* dst = ring + st * kSfxStage;
-      const int y = p_row0 + p_c * kSfxCT;
-      mbar_arrive_expect_tx(&full[st], kSfxStage);
-      tc::tma_load_3d(dst, tmk, 0, 0, y, &full[st]);
-      tc::tma_load_3d(dst + kSfxBox, tmv, 0, 0, y, &full[st]);
-    }
-    if (p_c % kSfxPrefetchChunks == 0) {
-      // warm L2 one granule ahead of the TMA loads: the rest of this item, or
-      // the first granule of the next one
-      const int tok = p_c * kSfxCT + kSfxPrefetchChunks * kSfxCT;
-      if (tok < p_ntok) {
-        prefetch(p_row0, tok, min(kSfxPrefetchChunks * kSfxCT, p_ntok - tok));
-      } else if (p_it + 1 < n_items) {
-        const SfxItem nx = sfx_item(table, off_gemv, off_rows, h_local, pool_tokens, items[p_it + 1]);
-        prefetch(nx.row0, 0, min(kSfxPrefetchChunks * kSfxCT, nx.n_tok));
-      }
-    }
-    ++k_issue;
-    if (++p_c == p_nch) {
-      p_c = 0;
-      ++p_it;
-      p_open();
-    }
-  };
-  p_open();
-  for (int i = 0; i < kSfxStages; ++i) issue();
-
-  const float cscale = 1.4426950408889634f * rsqrtf((float)kTcD);
-  const int mat = lane >> 3, rr = lane & 7;
-  const int tk_qk = rr + ((mat & 1) << 3), ck_qk = mat >> 1;  // ldmatrix rows of K for S^T
-  const int tk_pv = rr + ((mat >> 1) << 3), ck_pv = mat & 1;  // ldmatrix.trans rows of V for V^T
-  const uint32_t ring_s = smem_u32(ring);
-  int k = 0;
-  for (int ii = 0; ii < n_items; ++ii) {
-    const SfxItem it = sfx_item(table, off_gemv, off_rows, h_local, pool_tokens, items[ii]);
-    const int nch = (it.n_tok + kSfxCT - 1) / kSfxCT;
-    if (nch == 0) continue;
-    uint32_t qf[8][2];
-    {
-      const bool hv = gid < g;
-      const uint32_t* qp =
-          reinterpret_cast<const uint32_t*>(q + ((int64_t)it.req * hq_local + it.kh * g + (hv ? gid : 0)) * kTcD);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        qf[ks][0] = hv ? __ldg(qp + ks * 8 + tig) : 0u;
-        qf[ks][1] = hv ? __ldg(qp + ks * 8 + 4 + tig) : 0u;
-      }
-    }
-    float acc[8][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    float m_run[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
-    float l_run[2] = {0.f, 0.f};
-    for (int c = 0; c < nch; ++c, ++k) {
-      const int st = k % kSfxStages;
-      mbar_wait(&full[st], (k / kSfxStages) & 1);
-      const uint32_t kb = ring_s + st * kSfxStage, vb = kb + kSfxBox;
-      // S^T of the chunk's 16-token tiles; k split over two accumulators per
-      // tile so the dependent HMMA chains are 4 long, not 8
-      float sc[kSfxTiles][2][4];
-#pragma unroll
-      for (int tt = 0; tt < kSfxTiles; ++tt)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) sc[tt][h][0] = sc[tt][h][1] = sc[tt][h][2] = sc[tt][h][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-        for (int tt = 0; tt < kSfxTiles; ++tt) {
-          uint32_t a[4];
-          ldsm_x4(kb + sfx_sw(16 * tt + tk_qk, 2 * ks + ck_qk), a);
-          hmma(sc[tt][ks & 1], a, qf[ks][0], qf[ks][1]);
-        }
-      const float ninf = -__int_as_float(0x7f800000);
-      float sv[kSfxTiles][4];
-#pragma unroll
-      for (int tt = 0; tt < kSfxTiles; ++tt) {
-        const int t0 = c * kSfxCT + 16 * tt + gid;
-        const bool va = t0 < it.n_tok, vb8 = t0 + 8 < it.n_tok;
-        sv[tt][0] = va ? (sc[tt][0][0] + sc[tt][1][0]) * cscale : ninf;
-        sv[tt][1] = va ? (sc[tt][0][1] + sc[tt][1][1]) * cscale : ninf;
-        sv[tt][2] = vb8 ? (sc[tt][0][2] + sc[tt][1][2]) * cscale : ninf;
-        sv[tt][3] = vb8 ? (sc[tt][0][3] + sc[tt][1][3]) * cscale : ninf;
-      }
-      float mx0 = fmaxf(sv[0][0], sv[0][2]), mx1 = fmaxf(sv[0][1], sv[0][3]);
-#pragma unroll
-      for (int tt = 1; tt < kSfxTiles; ++tt) {
-        mx0 = fmaxf(mx0, fmaxf(sv[tt][0], sv[tt][2]));
-        mx1 = fmaxf(mx1, fmaxf(sv[tt][1], sv[tt][3]));
-      }
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-      }
-      const bool n0 = mx0 > m_run[0] + 8.f, n1 = mx1 > m_run[1] + 8.f;
-      if (__any_sync(0xffffffffu, n0 || n1)) {
-        const float a0 = n0 ? fast_exp2(m_run[0] - mx0) : 1.f;
-        const float a1 = n1 ? fast_exp2(m_run[1] - mx1) : 1.f;
-        l_run[0] *= a0;
-        l_run[1] *= a1;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc[i][0] *= a0;
-          acc[i][2] *= a0;
-          acc[i][1] *= a1;
-          acc[i][3] *= a1;
-        }
-        if (n0) m_run[0] = mx0;
-        if (n1) m_run[1] = mx1;
-      }
-      const bool d0 = m_run[0] == ninf, d1 = m_run[1] == ninf;
-      uint32_t bf[kSfxTiles][2];
-#pragma unroll
-      for (int tt = 0; tt < kSfxTiles; ++tt) {
-        const float p0 = d0 ? 0.f : fast_exp2(sv[tt][0] - m_run[0]);
-        const float p1 = d1 ? 0.f : fast_exp2(sv[tt][1] - m_run[1]);
-        const float p2 = d0 ? 0.f : fast_exp2(sv[tt][2] - m_run[0]);
-        const float p3 = d1 ? 0.f : fast_exp2(sv[tt][3] - m_run[1]);
-        l_run[0] += p0 + p2;
-        l_run[1] += p1 + p3;
-        bf[tt][0] = movm_t(pack2_bf16(p0, p1));
-        bf[tt][1] = movm_t(pack2_bf16(p2, p3));
-      }
-#pragma unroll
-      for (int dm = 0; dm < 8; ++dm)
-#pragma unroll
-        for (int tt = 0; tt < kSfxTiles; ++tt) {
-          uint32_t a[4];
-          ldsm_x4_t(vb + sfx_sw(16 * tt + tk_pv, 2 * dm + ck_pv), a);
-          hmma(acc[dm], a, bf[tt][0], bf[tt][1]);
-        }
-      issue();  // refill the stage just consumed
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], o);
-      l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], o);
-    }
-    const float inv0 = 1.f / l_run[0], inv1 = 1.f / l_run[1];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int h = 2 * tig + j;
-      if (h >= g) continue;
-      const int qh = it.kh * g + h;
-      const float inv = j ? inv1 : inv0;
-      float* dst;
-      if (it.slot < 0) {
-        dst = out + ((int64_t)it.req * hq_local + qh) * kTcD;
-      } else {
-        const int64_t ei = (int64_t)it.slot * hq_local + qh;
-        dst = part_o + ei * kTcD;
-        if (gid == 0) {
-          part_ml[2 * ei] = m_run[j] * 0.69314718055994530942f;  // natural-log units
-          part_ml[2 * ei + 1] = l_run[j];
-        }
-      }
-#pragma unroll
-      for (int dm = 0; dm < 8; ++dm) {
-        dst[16 * dm + gid] = acc[dm][j] * inv;
-        dst[16 * dm + gid + 8] = acc[dm][2 + j] * inv;
-      }
-    }
-  }
-}
-
-template <bool F>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     tc_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                  const __grid_constant__ CUtensorMap tmk16, const __grid_constant__ CUtensorMap tmv16,
-                  int off_gemv, int off_sfx_ptr, int off_sfx_item, int n_sfx_slots, const void* kpool_raw,
-                  const void* vpool_raw,
                   const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
@@ -458,13 +193,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
-  using Cfg = TcCfg<F>;
-  constexpr int kTcKStages = Cfg::KStages, kTcVStages = Cfg::VStages;
-  constexpr int kOffQ = Cfg::OffQ, kOffK = Cfg::OffK, kOffV = Cfg::OffV, kOffSfx = Cfg::OffSfx;
-  constexpr int kOffMpub = Cfg::OffMpub, kOffLx = Cfg::OffLx;
-  using Bars = TcBars<kTcKStages, kTcVStages>;
-  static_assert(sizeof(Bars) <= 512, "barrier block");
-  Bars* bars = reinterpret_cast<Bars*>(smem + Cfg::OffBar);
+  static_assert(sizeof(TcBars) <= 512, "barrier block");
+  TcBars* bars = reinterpret_cast<TcBars*>(smem + kOffBar);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = tc::cluster_rank();
@@ -497,9 +227,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
     }
     for (int i = 0; i < 4; ++i) mbar_init(&bars->pv_done[i], 1);
     mbar_init(&bars->o_free, kGroupWarpArrivals);
-    if (F)
-      for (int w = 0; w < kTcSfxWarps; ++w)
-        for (int s = 0; s < kSfxStages; ++s) mbar_init(&bars->sfx_full[w][s], 1);
     fence_barrier_init();
   }
   if (warp == kTcMmaWarp) tc::tmem_alloc_pair(&bars->tmem_slot, kTmemCols);
@@ -511,24 +238,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
   tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
-  if (F && warp >= kTcSfxWarp0) {
-    // ================================================ suffix warpgroup (fused build)
-#ifndef CODEC_NO_SETMAXNREG
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::RegsSfx));
-#endif
-    const int sw = warp - kTcSfxWarp0;
-    if (sw < kTcSfxWarps && n_sfx_slots > 0) {
-      const int slot = blockIdx.x * kTcSfxWarps + sw;
-      const int i0 = table[off_sfx_ptr + slot], i1 = table[off_sfx_ptr + slot + 1];
-      sfx_run(&tmk16, &tmv16, table, off_gemv, off_rows, table + off_sfx_item + i0, i1 - i0, hq_local / g, q,
-              pool_tokens, g, hq_local, out, part_o, part_ml, smem + kOffSfx + sw * kSfxStages * kSfxStage,
-              bars->sfx_full[sw], (const __nv_bfloat16*)kpool_raw, (const __nv_bfloat16*)vpool_raw);
-      if (ctalog && lane == 0) ctalog[4 * (2048 + blockIdx.x) + 1 + sw] = global_ns();
-    }
-  } else if (warp >= kTcSoftmaxWarps) {
+  if (warp >= kTcSoftmaxWarps) {
   // producer / MMA warpgroup: hands registers to the softmax warpgroups
 #ifndef CODEC_NO_SETMAXNREG
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::RegsOther));
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegsOther));
 #endif
   if (warp == kTcProducerWarp || warp == kTcVProducerWarp) {
     // ================================================ TMA producers (both CTAs)
@@ -662,11 +375,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         sc.next();
         ++ts;
       };
-      // Polling scheduler: issue S(ts) or PV(tp), whichever is ready, S
-      // first. A fixed order would deadlock at short units: PV(tl) (ending
-      // unit n) would queue behind S(tl + 3), whose Q (unit n + 2) waits
-      // for unit n's epilogue, which waits for PV(tl). Parity probes are
-      // exact: each barrier's next phase depends on an MMA not yet issued.
+      // Issue order S0 S1 S2 S3 PV0 S4 PV1 S5 PV2 ...: S(ts) once ts <= tp + 3,
+      // else PV(tp), with blocking waits (the issuing thread sleeps in
+      // mbarrier.try_wait and wakes as soon as the phase completes -- a
+      // polling loop reacted 1-3k clk late on an SMSP shared with four
+      // softmax warps). Deadlock-free: every S / PV wait depends only on
+      // MMAs issued earlier, except a new unit's Q, which can wait for the
+      // epilogue of the unit two back (its O staging buffer) -- so before
+      // blocking on Q the pending PVs are issued first.
       TileCursor pc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
       pc.open();
       auto issue_pv = [&](int tp) {
@@ -690,32 +406,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
         if (lane == 0) stamp(1, tp);
         pc.next();
       };
-      auto s_ready = [&]() {
-        if (ts >= 2 && !tc::mbar_ready(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1)) return false;
-        if (sc.j == 0 && !tc::mbar_ready(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1)) return false;
-        return tc::mbar_ready(&bars->k_full[ts % kTcKStages], (ts / kTcKStages) & 1);
-      };
-      auto pv_ready = [&](int tp) {
-        if (!tc::mbar_ready(&bars->p_full[tp & 1], (tp >> 1) & 1)) return false;
-        if (!tc::mbar_ready(&bars->v_full[tp % kTcVStages], (tp / kTcVStages) & 1)) return false;
-        return pc.j != 0 || pc.n == 0 || tc::mbar_ready(&bars->o_free, (pc.n - 1) & 1);
-      };
       int tp = 0;
+      const int lookahead = (dbg_flags & 4096) ? 2 : 3;  // S tiles issued ahead of the next PV
       while (!pc.done()) {
-        if (!sc.done() && s_ready()) {
+        if (!sc.done() && ts <= tp + lookahead) {
+          if (sc.j == 0 && tp < ts && !tc::mbar_ready(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1)) {
+            issue_pv(tp);
+            ++tp;
+            continue;
+          }
+          if (ts >= 2) mbar_wait(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1);  // S(ts-2) pulled out by both CTAs
           if (lane == 0) stamp(8, ts);
           if (lane == 0) stamp(13, ts);
           issue_s();
           if (lane == 0) stamp(6, ts - 3);
           continue;
         }
-        if (tp < ts && pv_ready(tp)) {
-          if (lane == 0) stamp(10, tp);
-          issue_pv(tp);
-          ++tp;
-          continue;
-        }
-        __nanosleep(20);
+        issue_pv(tp);
+        ++tp;
       }
       PROG(0, 9999, 7);
     }
@@ -723,7 +431,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<F>::Threads, 1
   } else {
     // ================================================ softmax warpgroups
 #ifndef CODEC_NO_SETMAXNREG
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::RegsSoftmax));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kTcRegsSoftmax));
 #endif
     const int grp = warp >> 2;   // 0: even tiles, 1: odd tiles
     const int quad = warp & 3;   // TMEM lane quadrant
@@ -1100,23 +808,16 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
     cudaMemsetAsync(g_trace, 0, kTraceLen * sizeof(long long), st);
   }
   if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
-  CUtensorMap mk, mv, mk16, mv16;
+  CUtensorMap mk, mv;
   CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, 64));      // K half: 64 tokens
   CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kTcBN));   // V half: 64 d columns
-  CODEC_TRY(encode_pool_rows_map(&mk16, k, (int64_t)h_local * pool_tokens, kSfxCT));  // suffix chunks
-  CODEC_TRY(encode_pool_rows_map(&mv16, v, (int64_t)h_local * pool_tokens, kSfxCT));
-  const bool fused = in.n_sfx_slots > 0;
-  auto kern = fused ? tc_pac_kernel<true> : tc_pac_kernel<false>;
-  const int smem = fused ? TcCfg<true>::Smem : TcCfg<false>::Smem;
-  const int threads = fused ? TcCfg<true>::Threads : TcCfg<false>::Threads;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   if (e != cudaSuccess) return cuda_status(e, "tc smem attribute");
   dim3 grid(kTcCtasPerBlock * in.n_tc_blocks, 1);  // CTA pairs (__cluster_dims__); heads come from the units
-  kern<<<grid, threads, smem, st>>>(mk, mv, mk16, mv16, in.off_gemv, in.off_sfx_ptr, in.off_sfx_item,
-                                    (flags & CODEC_FLAG_SKIP_GEMV) ? 0 : in.n_sfx_slots, k, v, table, in.off_tc,
-                                    in.off_rows, in.off_tc_block_ptr, (const __nv_bfloat16*)q, pool_tokens, g,
-                                    h_local * g, (float*)out, (float*)part_o, (float*)part_ml,
-                                    trace ? g_trace : nullptr, flags, ctalog);
+  tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
+                                                   (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
+                                                   (float*)out, (float*)part_o, (float*)part_ml,
+                                                   trace ? g_trace : nullptr, flags, ctalog);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

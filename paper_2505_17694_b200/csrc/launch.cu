@@ -123,10 +123,9 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   // TC CTA's setmaxnreg register hand-off corrupts the registers of a
   // co-resident CTA of another kernel (observed on B200: wrong O in the
   // suffix partials, tools/determinism.py). It runs after the TC kernel.
-  const bool fused = do_tc && info->n_sfx_slots > 0;  // the TC kernel's suffix warps run the GEMV groups
-  const bool mma_gemv = do_gemv && !fused && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
+  const bool mma_gemv = do_gemv && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & CODEC_FLAG_GEMV_SIMT);
-  const bool fork = aux_stream != nullptr && do_tc && ((do_gemv && !mma_gemv && !fused) || do_gen);
+  const bool fork = aux_stream != nullptr && do_tc && ((do_gemv && !mma_gemv) || do_gen);
   cudaStream_t side = fork ? (cudaStream_t)aux_stream : st;
   long long* ctalog = nullptr;
   if (dims->flags & CODEC_FLAG_CTALOG) {
@@ -151,7 +150,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, st, ctalog));
-  else if (do_gemv && !fused)
+  else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
                           ctalog));
