@@ -207,7 +207,9 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
         int64_t pp = path_pos(r, n);
         if (pp < 0)
           return fail(CODEC_ERR_INCOMPLETE_PARTIALS, "request %d not on a path through node %lld", r, (long long)n);
-        req_units[r].push_back({pp, (int64_t)s, (int64_t)(rows.size() / 4)});
+        // TC rows are templates: their partials come from the per-head
+        // pieces cut below; the other kinds' rows serve every head
+        if (kind != kKindTc) req_units[r].push_back({pp, (int64_t)s, (int64_t)(rows.size() / 4)});
         rows.push_back(r);
         rows.push_back(live[i].second);
         rows.push_back(-1);
@@ -216,35 +218,170 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       groups.push_back(gr);
     }
   }
-  // ---- slots: direct output for single-partial requests, else merged
-  std::vector<int32_t> merge_req, merge_ptr{0}, merge_slot;
-  int32_t n_slots = 0, max_merge = 0;
-  for (int32_t r = 0; r < bs; ++r) {
-    auto& u = req_units[r];
-    if (u.empty()) return fail(CODEC_ERR_NO_VISIBLE_TOKENS, "request %d has no visible tokens anywhere on its path", r);
-    std::sort(u.begin(), u.end());  // path-then-slice order
-    if (u.size() == 1) {
-      rows[4 * u[0][2] + 2] = -1 - r;
-      continue;
-    }
-    merge_req.push_back(r);
-    max_merge = std::max<int32_t>(max_merge, (int32_t)u.size());
-    for (auto& e : u) {
-      rows[4 * e[2] + 2] = n_slots;
-      merge_slot.push_back(n_slots++);
-    }
-    merge_ptr.push_back((int32_t)merge_slot.size());
-  }
   // ---- group order: TC, GEMV, generic; longest slices first within a kind
   std::stable_sort(groups.begin(), groups.end(), [](const Grp& a, const Grp& b) {
     if (a.kind != b.kind) return a.kind < b.kind;
     return a.order_len > b.order_len;
   });
   (void)sub_block;
+  const int32_t h_local = dims->head_end - dims->head_begin;
+
+  // ---- tensor-core pieces (stream-K over CTA pairs). A unit = (TC group,
+  // local kv head) of ceil(max_vis / 128) KV tiles. Units are laid out in
+  // lanes -- lane c holds the c-th row chunk of every KV slice -- and each
+  // lane's unit sequence (slice, head order) is cut into equal tile ranges,
+  // one per CTA pair of the lane: every pair gets the same work, at most
+  // a couple of pieces (few epilogues, few partials), and pair j of every
+  // lane walks the same K/V tiles at the same time, so a tile is read from
+  // HBM once and from L2 by the other lanes. Pieces never cross plan
+  // slices; the reference plan's division stays the outer structure.
+  struct Piece {
+    int32_t grp, head, t0, t1, pair;
+  };
+  std::vector<Piece> pieces;
+  std::vector<int32_t> tcg;  // indices of TC groups in `groups`
+  for (size_t i = 0; i < groups.size(); ++i)
+    if (groups[i].kind == kKindTc) tcg.push_back((int32_t)i);
+  int32_t n_pairs = 0;
+  if (!tcg.empty()) {
+    int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
+    if (dims->tc_sm_budget > 0) sms = std::min(sms, dims->tc_sm_budget);
+    const int32_t pairs = std::max(1, sms / kTcCtasPerBlock);
+    auto tiles_of = [&](int32_t gi) { return (int64_t)(groups[gi].max_vis + 127) / 128; };
+    // lane = rank of the group among the TC groups of its KV slice
+    std::map<std::pair<int32_t, int32_t>, std::vector<int32_t>> by_slice;  // (kv_tok, len) -> groups
+    for (int32_t gi : tcg) by_slice[{groups[gi].kv_tok, groups[gi].len}].push_back(gi);
+    std::vector<std::vector<int32_t>> lanes;
+    for (auto& kv : by_slice) {
+      auto v = kv.second;
+      std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return groups[a].row_begin < groups[b].row_begin; });
+      for (size_t c = 0; c < v.size(); ++c) {
+        if (lanes.size() <= c) lanes.emplace_back();
+        lanes[c].push_back(v[c]);
+      }
+    }
+    std::vector<int64_t> lane_w(lanes.size(), 0);
+    int64_t w_all = 0;
+    for (size_t c = 0; c < lanes.size(); ++c) {
+      for (int32_t gi : lanes[c]) lane_w[c] += tiles_of(gi) * h_local;
+      w_all += lane_w[c];
+    }
+    // pairs per lane, proportional to its work (at least one per busy lane)
+    std::vector<int32_t> lane_p(lanes.size(), 0);
+    int32_t used = 0;
+    for (size_t c = 0; c < lanes.size(); ++c) {
+      lane_p[c] = (int32_t)std::max<int64_t>(lane_w[c] > 0 ? 1 : 0, (int64_t)pairs * lane_w[c] / std::max<int64_t>(w_all, 1));
+      lane_p[c] = (int32_t)std::min<int64_t>(lane_p[c], std::max<int64_t>(lane_w[c], 1));
+      used += lane_p[c];
+    }
+    while (used > pairs) {  // more busy lanes than pairs: shrink the widest
+      size_t c = std::max_element(lane_p.begin(), lane_p.end()) - lane_p.begin();
+      if (lane_p[c] <= 1) break;
+      --lane_p[c];
+      --used;
+    }
+    int32_t pair0 = 0;
+    for (size_t c = 0; c < lanes.size(); ++c) {
+      if (lane_w[c] == 0) continue;
+      const int32_t pc = std::max(1, lane_p[c]);
+      const int64_t per = (lane_w[c] + pc - 1) / pc;
+      int64_t pos = 0;  // tiles of this lane already cut
+      for (int32_t gi : lanes[c])
+        for (int32_t h = 0; h < h_local; ++h) {
+          const int64_t nt = tiles_of(gi);
+          int64_t t = 0;
+          while (t < nt) {
+            const int64_t pair_in_lane = std::min<int64_t>(pos / per, pc - 1);
+            const int64_t end_of_pair = (pair_in_lane + 1) * per;
+            const int64_t take = pair_in_lane == pc - 1 ? nt - t : std::min(nt - t, end_of_pair - pos);
+            pieces.push_back({gi, h, (int32_t)t, (int32_t)(t + take), pair0 + (int32_t)pair_in_lane});
+            t += take;
+            pos += take;
+          }
+        }
+      pair0 += pc;
+    }
+    n_pairs = pair0;
+  }
+  // piece rows (their own records: visible tokens within the piece) and the
+  // per-(request, head) TC contributions, in piece order
+  struct TcRow {
+    int32_t head, row;
+  };
+  std::vector<std::vector<TcRow>> req_tc(bs);
+  struct PieceRec {
+    int32_t kv_tok, len, row_begin, n_rows, max_vis, node, pair, head;
+  };
+  std::vector<PieceRec> prec;
+  for (auto& pc : pieces) {
+    const Grp& gr = groups[pc.grp];
+    const int64_t tok0 = (int64_t)pc.t0 * 128, tok1 = std::min<int64_t>((int64_t)pc.t1 * 128, gr.len);
+    PieceRec rec{(int32_t)(gr.kv_tok + tok0), (int32_t)(tok1 - tok0), (int32_t)(rows.size() / 4), 0, 0, gr.node,
+                 pc.pair, pc.head};
+    for (int32_t k = 0; k < gr.n_rows; ++k) {
+      const int32_t r = rows[4 * (gr.row_begin + k)], vis = rows[4 * (gr.row_begin + k) + 1];
+      const int64_t v = std::min<int64_t>(vis, tok1) - tok0;
+      if (v <= 0) continue;
+      req_tc[r].push_back({pc.head, (int32_t)(rows.size() / 4)});
+      rows.push_back(r);
+      rows.push_back((int32_t)v);
+      rows.push_back(-1);
+      rows.push_back(0);
+      ++rec.n_rows;
+      rec.max_vis = std::max<int32_t>(rec.max_vis, (int32_t)v);
+    }
+    if (rec.n_rows > 0) prec.push_back(rec);
+  }
+  // ---- slots. Per request and kv head: the shared (GEMV / generic) partials
+  // serve every head, the TC pieces only theirs. A (request, head) with a
+  // single partial writes the output directly; otherwise its partials get
+  // slots base, base + 1, ... (shared first) and one merge entry. Partial
+  // storage is slot * hq_local + q head, so heads never collide.
+  std::vector<int32_t> merge_req, merge_ptr{0}, merge_slot;
+  int32_t n_slots = 0, max_merge = 0;
+  for (int32_t r = 0; r < bs; ++r) {
+    auto& u = req_units[r];
+    std::sort(u.begin(), u.end());  // path-then-slice order
+    std::vector<int32_t> n_tc(h_local, 0);
+    for (auto& e : req_tc[r]) ++n_tc[e.head];
+    const int32_t ns = (int32_t)u.size();
+    int32_t most = 0;
+    bool any_tc = false;
+    for (int32_t h = 0; h < h_local; ++h) {
+      most = std::max(most, ns + n_tc[h]);
+      any_tc |= n_tc[h] > 0;
+    }
+    if (most == 0) return fail(CODEC_ERR_NO_VISIBLE_TOKENS, "request %d has no visible tokens anywhere on its path", r);
+    if (most == 1) {  // one partial on every head: direct
+      if (ns == 1) rows[4 * u[0][2] + 2] = -1 - r;
+      for (auto& e : req_tc[r]) rows[4 * e.row + 2] = -1 - r;
+      continue;
+    }
+    const int32_t base = n_slots;
+    n_slots += most;
+    for (int32_t i = 0; i < ns; ++i) rows[4 * u[i][2] + 2] = base + i;
+    std::vector<int32_t> next(h_local, ns);
+    for (auto& e : req_tc[r]) {
+      if (ns + n_tc[e.head] == 1) {
+        rows[4 * e.row + 2] = -1 - r;  // this head has just this piece
+      } else {
+        rows[4 * e.row + 2] = base + next[e.head]++;
+      }
+    }
+    (void)any_tc;
+    for (int32_t h = 0; h < h_local; ++h) {
+      const int32_t tot = ns + n_tc[h];
+      if (tot < 2) continue;
+      merge_req.push_back(r * h_local + h);
+      max_merge = std::max(max_merge, tot);
+      for (int32_t i = 0; i < tot; ++i) merge_slot.push_back(base + i);
+      merge_ptr.push_back((int32_t)merge_slot.size());
+    }
+  }
 
   auto t = new codec_table();
   codec_table_info& in = t->info;
-  in.h_local = dims->head_end - dims->head_begin;
+  in.h_local = h_local;
   in.max_merge = max_merge;
   in.gemv_rows = gemv_rows;
   std::vector<int32_t>& blob = t->blob;
@@ -258,58 +395,19 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
         ++count;
       }
   };
-  // ---- tensor-core units: one (group, local kv head) pair of the table is
-  // a unit; units are LPT-scheduled onto the persistent CTA pairs of the
-  // whole GPU (cost = 64-token tiles, the unit the kernel iterates), same
-  // rule as greedy_assign (scheduler.py:142-155) -- heads are not pinned
-  // to CTAs, so every SM of the budget gets work whatever h_local is.
-  // Each pair keeps its units in assignment order.
+  // ---- TC pieces, grouped per pair (each pair walks its list in order)
   {
-    std::vector<Grp> tcg;
-    for (auto& gr : groups)
-      if (gr.kind == kKindTc) tcg.push_back(gr);
-    int32_t sms = dims->sm_count > 0 ? dims->sm_count : 148;
-    if (dims->tc_sm_budget > 0) sms = std::min(sms, dims->tc_sm_budget);
-    const int32_t h_local = dims->head_end - dims->head_begin;
-    const int64_t n_units = (int64_t)tcg.size() * h_local;
-    int32_t m_tc = std::max(1, sms / kTcCtasPerBlock);
-    m_tc = (int32_t)std::min<int64_t>(m_tc, n_units);
-    std::vector<int64_t> cost(tcg.size());
-    for (size_t i = 0; i < tcg.size(); ++i) cost[i] = (tcg[i].max_vis + 63) / 64;
-    // units in (cost desc, KV slice, head) order: the row chunks of one
-    // (slice, head) -- they read the same K/V tiles -- land on consecutive
-    // pairs of the same LPT round and run concurrently, so their tiles are
-    // read from HBM once and from L2 by the others
-    std::vector<int64_t> order(n_units);
-    for (int64_t u = 0; u < n_units; ++u) order[u] = u;
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-      const Grp &ga = tcg[a / h_local], &gb = tcg[b / h_local];
-      if (cost[a / h_local] != cost[b / h_local]) return cost[a / h_local] > cost[b / h_local];
-      if (ga.kv_tok != gb.kv_tok) return ga.kv_tok < gb.kv_tok;
-      return a % h_local < b % h_local;
-    });
-    std::vector<int64_t> load(std::max(m_tc, 1), 0);
-    std::vector<std::vector<int64_t>> per_block(std::max(m_tc, 1));
-    for (int64_t u : order) {
-      int32_t best = 0;
-      for (int32_t b = 1; b < m_tc; ++b)
-        if (load[b] < load[best]) best = b;
-      load[best] += cost[u / h_local];
-      per_block[best].push_back(u);
-    }
+    std::stable_sort(prec.begin(), prec.end(), [](const PieceRec& a, const PieceRec& b) { return a.pair < b.pair; });
     in.off_tc = (int32_t)blob.size();
-    in.n_tc_groups = (int32_t)n_units;
-    std::vector<int32_t> block_ptr{0};
-    for (int32_t b = 0; b < m_tc; ++b) {
-      for (int64_t u : per_block[b]) {
-        const Grp& gr = tcg[u / h_local];
-        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, b,
-                                   (int32_t)(u % h_local)};
-        blob.insert(blob.end(), rec, rec + kGroupInts);
-      }
-      block_ptr.push_back(block_ptr.back() + (int32_t)per_block[b].size());
+    in.n_tc_groups = (int32_t)prec.size();
+    std::vector<int32_t> block_ptr(n_pairs + 1, 0);
+    for (auto& pr : prec) {
+      int32_t rec[kGroupInts] = {pr.kv_tok, pr.len, pr.row_begin, pr.n_rows, pr.max_vis, pr.node, pr.pair, pr.head};
+      blob.insert(blob.end(), rec, rec + kGroupInts);
+      ++block_ptr[pr.pair + 1];
     }
-    in.n_tc_blocks = tcg.empty() ? 0 : m_tc;
+    for (int32_t b = 0; b < n_pairs; ++b) block_ptr[b + 1] += block_ptr[b];
+    in.n_tc_blocks = prec.empty() ? 0 : n_pairs;
     in.off_tc_block_ptr = (int32_t)blob.size();
     blob.insert(blob.end(), block_ptr.begin(), block_ptr.end());
   }

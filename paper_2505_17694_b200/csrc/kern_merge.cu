@@ -9,7 +9,9 @@
 // which equals the reference's balanced pairwise por() fold up to
 // rounding (the merge is associative/commutative in exact arithmetic,
 // test_attention.py:160-180) but takes one pass over the partials.
-// One warp per (request, query head); lanes cover the head dim.
+// A merge entry is (request, local kv head): stream-K cuts the shared nodes
+// per head, so the partial lists differ between heads. One warp per
+// (entry, query head of that kv head); lanes cover the head dim.
 #include <cuda_runtime.h>
 
 #include "common.h"
@@ -20,14 +22,15 @@ namespace codec {
 
 template <typename A, int DPL>
 __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
-                                                    int off_slot, int n_merge, int hq_local, int d,
+                                                    int off_slot, int n_merge, int g, int h_local, int d,
                                                     const A* __restrict__ part_o, const A* __restrict__ part_ml,
                                                     A* __restrict__ out) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
-  const int qh = blockIdx.y * 4 + warp;
-  if (i >= n_merge || qh >= hq_local) return;
-  const int req = table[off_req + i];
+  const int k = blockIdx.y * 4 + warp;
+  if (i >= n_merge || k >= g) return;
+  const int hq_local = g * h_local;
+  const int code = table[off_req + i], req = code / h_local, qh = (code % h_local) * g + k;
   const int p0 = table[off_ptr + i], p1 = table[off_ptr + i + 1];
   const int32_t* slots = table + off_slot;
   A M = neg_inf<A>();
@@ -65,15 +68,16 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
 // four loads in flight (float4 per lane), so the merge costs a few memory
 // latencies instead of one per partial.
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
-                                                       int off_slot, int n_merge, int hq_local,
+                                                       int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
                                                        const float* __restrict__ part_ml, float* __restrict__ out) {
   constexpr int kMax = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
-  const int qh = blockIdx.y * 4 + warp;
-  if (i >= n_merge || qh >= hq_local) return;
-  const int req = table[off_req + i];
+  const int k = blockIdx.y * 4 + warp;
+  if (i >= n_merge || k >= g) return;
+  const int hq_local = g * h_local;
+  const int code = table[off_req + i], req = code / h_local, qh = (code % h_local) * g + k;
   const int p0 = table[off_ptr + i], np = min(table[off_ptr + i + 1] - p0, kMax);
   const int32_t* slots = table + off_slot + p0;
   // lane p (< np) fetches partial p's (m, l); the max is a warp reduction
@@ -118,15 +122,16 @@ int32_t cuda_status(cudaError_t e, const char* what);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st) {
   if (in.n_merge == 0) return CODEC_OK;
-  dim3 grid(in.n_merge, (hq_local + 3) / 4);
+  const int h_local = in.h_local, g = hq_local / h_local;
+  dim3 grid(in.n_merge, (g + 3) / 4);
 #define CODEC_MERGE(A, DPL)                                                                                    \
   merge_kernel<A, DPL><<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot,     \
-                                             in.n_merge, hq_local, d, (const A*)part_o, (const A*)part_ml,      \
+                                             in.n_merge, g, h_local, d, (const A*)part_o, (const A*)part_ml,    \
                                              (A*)out)
   if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
   if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 16) {
     merge128_kernel<<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot, in.n_merge,
-                                          hq_local, (const float*)part_o, (const float*)part_ml, (float*)out);
+                                          g, h_local, (const float*)part_o, (const float*)part_ml, (float*)out);
     return cuda_status(cudaGetLastError(), "merge launch");
   }
   if (dtype == CODEC_F64) {

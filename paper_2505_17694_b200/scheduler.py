@@ -160,24 +160,24 @@ def concat_plans(plans) -> DivisionPlan:
 
 
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
-                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT,
-                units_per_pair: int = 4) -> DivisionPlan:
+                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT) -> DivisionPlan:
     """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
-    head rows per chunk) are divided and LPT-scheduled with the reference
-    algorithm onto m = ceil(units_per_pair * pairs / h_local) blocks, where
-    pairs = budget // 2 persistent tensor-core CTA pairs serve every local
-    kv head: the table builder then LPT-packs the (slice, head) units onto
-    the pairs (host_table.cpp), ~units_per_pair units per pair. Unshared
-    nodes stay whole (their GEMV CTAs are hardware-scheduled and stream at
-    HBM speed regardless of order). Returns one plan over both."""
+    head rows per chunk) stay whole here: on the tensor cores every KV tile
+    costs the same (an M=256 MMA pair whatever the rows), so the device
+    balancer in the task table (host_table.cpp) divides them itself --
+    stream-K over the CTA pairs, per kv head, into equal tile ranges with
+    the row chunks of a slice in lockstep. Unshared nodes stay whole too
+    (their suffix CTAs are hardware-scheduled and stream at HBM speed
+    regardless of order). Returns one plan over both, in the reference's
+    DivisionPlan form (any reference plan is accepted by execute() as well;
+    its slices then bound the device pieces)."""
     tasks = device_tasks(forest, group_size)
     tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
     gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
     pairs = max(1, (tc_sm_budget or sm_count) // TC_CTAS_PER_BLOCK)
-    m_tc = max(1, -(-units_per_pair * pairs // max(1, h_local)))
     plans = []
     if tc:
-        plans.append(divide_and_schedule(tc, table, m_tc, search_limit=search_limit))
+        plans.append(plan_uniform_bk(tc, table, pairs, 1))
     if gv:  # one block per GEMV task: its makespan is the longest single task
         plans.append(plan_uniform_bk(gv, table, len(gv), 1))
     return concat_plans(plans)

@@ -273,9 +273,10 @@ class TestBf16Kernels:
 
 
 class TestConcurrency:
-    def test_aux_stream_and_budgets_bitwise_equal(self, cuda_ok, table):
-        """TC on the main stream || GEMV on the aux stream, and different TC
-        SM budgets, change scheduling only -- results are bit-identical."""
+    def test_aux_stream_and_budgets(self, cuda_ok, table):
+        """The aux stream changes scheduling only (bit-identical results);
+        a different TC SM budget re-cuts the stream-K pieces, which changes
+        the partial-merge rounding only."""
         spec = W.two_level(2048, 200, 96, h_q=32, h_kv=8, d=128, seed=4)
         f, q = build(spec, "bfloat16")
         plan = P.divide_and_schedule(P.device_tasks(f, group_size=4), table, 37)
@@ -283,11 +284,14 @@ class TestConcurrency:
         qd = q.queries.cuda()
         serial = DecodeStep(f, plan, 32, "bfloat16", concurrent=False)
         base = np_(serial(qd, kp, vp))
-        for budget in (0, 120, 64):
-            conc = DecodeStep(f, plan, 32, "bfloat16", concurrent=True, tc_sm_budget=budget)
-            assert np.array_equal(np_(conc(qd, kp, vp)), base)
+        conc = DecodeStep(f, plan, 32, "bfloat16", concurrent=True)
+        assert np.array_equal(np_(conc(qd, kp, vp)), base)
+        for budget in (120, 64):
+            other = np_(DecodeStep(f, plan, 32, "bfloat16", concurrent=True, tc_sm_budget=budget)(qd, kp, vp))
+            # other piece boundaries: other bf16 roundings of P (well inside the bf16 bar)
+            assert np.max(np.abs(other - base)) <= 1e-2 * float(np.max(np.abs(base)))
         best, times = P.autotune_step(DecodeStep(f, plan, 32, "bfloat16"), qd, kp, vp, budgets=[148, 96], iters=2)
-        assert np.array_equal(np_(best(qd, kp, vp)), base)
+        assert np.max(np.abs(np_(best(qd, kp, vp)) - base)) <= 1e-2 * float(np.max(np.abs(base)))
         ups = upcast_spec(spec)
         assert_bf16_close(base, OA.naive_attention(ups.queries, oracle_forest(ups)))
 
