@@ -1,11 +1,12 @@
 mkdir -p gpurun_out
-timeout 60 python tools/trace_tc.py 0 > gpurun_out/trace.log 2>&1; echo "trace exit $?"
 timeout 300 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench exit $?"
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; tail -1 gpurun_out/smoke.log
+for fl in 0 4096; do
+timeout 300 python bench.py --no-cpu-baseline --flags $fl > gpurun_out/bench_$fl.log 2>&1; echo "bench exit $?"
 python -c "
 import json
-for l in open('gpurun_out/bench.log'):
+for l in open('gpurun_out/bench_$fl.log'):
   if l.startswith('{'):
-    d=json.loads(l); print('us/step %.1f GB/s %.0f'%(d['us_per_step'],d['value']), {k:round(v['ms']*1e3,1) for k,v in d['kernels'].items()}, d['clocks']['sm_mhz'], 'e2e', round(d['e2e']['value']))
+    d=json.loads(l); print('$fl us/step %.1f GB/s %.0f'%(d['us_per_step'],d['value']), {k:round(v['ms']*1e3,1) for k,v in d['kernels'].items()}, d['clocks']['sm_mhz'], 'e2e', round(d['e2e']['value']))
 "
-tail -3 gpurun_out/bench.log | grep -i error
+done

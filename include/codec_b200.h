@@ -185,6 +185,8 @@ typedef struct {
 #define CODEC_FLAG_DBG_NO_EXP   512  /* TC softmax skips the exponentials: timing only, wrong output (debug) */
 #define CODEC_FLAG_CTALOG       1024 /* record {smid, start ns, end ns, cta} per TC / GEMV CTA (debug) */
 #define CODEC_FLAG_GEMV_SIMT    2048 /* suffix groups on the CUDA-core GEMV kernel instead of the mma.sync one */
+#define CODEC_FLAG_FUSED_MERGE  4096 /* the mma.sync suffix kernel folds each request's TC partials into its output
+                                        instead of the merge kernel (opt-in: slower on cfg2 so far) */
 #define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* TC kernel skips its shared-node units: timing only, wrong output (debug) */
 #define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
 
@@ -204,7 +206,9 @@ typedef struct {
   int32_t off_merge_req, off_merge_ptr, off_merge_slot;
   int32_t h_local;                                     /* head_end - head_begin */
   int32_t n_tc_blocks, off_tc_block_ptr;               /* persistent TC CTA pairs, their (group, head) unit CSR */
-  int32_t max_merge, reserved;                         /* most partials of one merged request */
+  int32_t max_merge;                                   /* most partials of one merged (request, head) */
+  int32_t n_merge_fused;                               /* further merge entries (after the n_merge) that the
+                                                          suffix kernel folds into its own output */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

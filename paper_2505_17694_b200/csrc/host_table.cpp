@@ -166,7 +166,8 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int64_t order_len;
   };
   std::vector<Grp> groups;
-  std::vector<int32_t> rows;  // 4 per row: req, vis_local, slot, pad
+  std::vector<int32_t> rows;  // 4 per row: req, vis_local, slot, fused merge entry (GEMV rows) or -1
+  std::vector<char> row_gemv;  // per template row: belongs to a GEMV group
   // per request: (path position, subtask, row index)
   std::vector<std::vector<std::array<int64_t, 3>>> req_units(bs);
   std::vector<std::vector<int32_t>> node_pathpos(bs);
@@ -210,10 +211,11 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
         // TC rows are templates: their partials come from the per-head
         // pieces cut below; the other kinds' rows serve every head
         if (kind != kKindTc) req_units[r].push_back({pp, (int64_t)s, (int64_t)(rows.size() / 4)});
+        row_gemv.push_back(kind == kKindGemv);
         rows.push_back(r);
         rows.push_back(live[i].second);
         rows.push_back(-1);
-        rows.push_back(0);
+        rows.push_back(-1);
       }
       groups.push_back(gr);
     }
@@ -326,7 +328,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       rows.push_back(r);
       rows.push_back((int32_t)v);
       rows.push_back(-1);
-      rows.push_back(0);
+      rows.push_back(-1);
       ++rec.n_rows;
       rec.max_vis = std::max<int32_t>(rec.max_vis, (int32_t)v);
     }
@@ -338,6 +340,12 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   // slots base, base + 1, ... (shared first) and one merge entry. Partial
   // storage is slot * hq_local + q head, so heads never collide.
   std::vector<int32_t> merge_req, merge_ptr{0}, merge_slot;
+  // entries merged by the mma.sync suffix kernel itself (its partial is the
+  // request's only non-TC one; the TC pieces finished before it started):
+  // kept after the others, the merge kernel runs only the others
+  std::vector<int32_t> fz_req, fz_ptr{0}, fz_slot, fz_row;
+  const bool mma_suffix = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 && !(dims->flags & CODEC_FLAG_GEMV_SIMT) &&
+                          (dims->flags & CODEC_FLAG_FUSED_MERGE);
   int32_t n_slots = 0, max_merge = 0;
   for (int32_t r = 0; r < bs; ++r) {
     auto& u = req_units[r];
@@ -368,16 +376,33 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
         rows[4 * e.row + 2] = base + next[e.head]++;
       }
     }
-    (void)any_tc;
+    bool all_heads = true;
+    for (int32_t h = 0; h < h_local; ++h) all_heads &= n_tc[h] > 0;
+    int32_t tc_most = 0;
+    for (int32_t h = 0; h < h_local; ++h) tc_most = std::max(tc_most, n_tc[h]);
+    const bool fused = mma_suffix && ns == 1 && row_gemv[u[0][2]] && all_heads && tc_most <= 8 && g * 8 <= 64;
+    if (fused) fz_row.push_back((int32_t)u[0][2]);
     for (int32_t h = 0; h < h_local; ++h) {
       const int32_t tot = ns + n_tc[h];
       if (tot < 2) continue;
-      merge_req.push_back(r * h_local + h);
       max_merge = std::max(max_merge, tot);
-      for (int32_t i = 0; i < tot; ++i) merge_slot.push_back(base + i);
-      merge_ptr.push_back((int32_t)merge_slot.size());
+      auto& rq = fused ? fz_req : merge_req;
+      auto& pt = fused ? fz_ptr : merge_ptr;
+      auto& sl = fused ? fz_slot : merge_slot;
+      rq.push_back(r * h_local + h);
+      for (int32_t i = 0; i < tot; ++i) sl.push_back(base + i);
+      pt.push_back((int32_t)sl.size());
     }
+    (void)any_tc;
   }
+
+  // fused entries after the others; a fused GEMV row's 4th field = the
+  // entry of its request's kv head 0 (heads follow contiguously)
+  const int32_t n_merge_plain = (int32_t)merge_req.size();
+  for (size_t i = 0; i < fz_row.size(); ++i) rows[4 * fz_row[i] + 3] = n_merge_plain + (int32_t)(i * h_local);
+  merge_req.insert(merge_req.end(), fz_req.begin(), fz_req.end());
+  for (size_t i = 1; i < fz_ptr.size(); ++i) merge_ptr.push_back((int32_t)merge_slot.size() + fz_ptr[i]);
+  merge_slot.insert(merge_slot.end(), fz_slot.begin(), fz_slot.end());
 
   auto t = new codec_table();
   codec_table_info& in = t->info;
@@ -416,7 +441,8 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   in.off_rows = (int32_t)blob.size();
   in.n_rows = (int32_t)(rows.size() / 4);
   blob.insert(blob.end(), rows.begin(), rows.end());
-  in.n_merge = (int32_t)merge_req.size();
+  in.n_merge = n_merge_plain;
+  in.n_merge_fused = (int32_t)fz_req.size();
   in.off_merge_req = (int32_t)blob.size();
   blob.insert(blob.end(), merge_req.begin(), merge_req.end());
   in.off_merge_ptr = (int32_t)blob.size();

@@ -38,6 +38,7 @@ constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
 constexpr int kMmaStages = 4;
 constexpr int kMmaCT = 16 * kMmaWarps;             // tokens per stage
 constexpr int kMmaD = 128;
+constexpr int kFzMax = 8;                          // partials besides its own a fused merge folds in
 constexpr int kMmaBox = kMmaCT * 256;              // one box: kMmaCT whole token rows (8 KB)
 constexpr int kMmaStageBytes = 2 * kMmaBox;        // K box + V box
 constexpr int kMmaSmem = kMmaStages * kMmaStageBytes + 1024 /* align */ + 2 * kMmaStages * 8;
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
                    const int32_t* __restrict__ table, int off_groups, int off_rows,
                    const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                    float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                   long long* __restrict__ ctalog) {
+                   int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog) {
   const long long t_start = ctalog ? global_ns() : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
   const int kh = blockIdx.y;
   const int32_t* row = table + off_rows + grp[kGrpRowBegin] * kRowInts;
   const int req = row[0], n_tok = row[1], slot = row[2];
+  const int fz = row[3];  // >= 0: merge entry of (req, kv head 0): fold the TC partials in here
   const int nch = (n_tok + kMmaCT - 1) / kMmaCT;
   const int row0 = kh * (int)pool_tokens + grp[kGrpKvTok];
 
@@ -204,6 +206,23 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kMmaWarps) : "memory");
     const float* wb = reinterpret_cast<const float*>(smem);
+    // fused merge: the other partials' slots and (m, l) of (req, kv head)
+    float2* fz_ml = reinterpret_cast<float2*>(smem + 16384);       // [8 q heads][kFzMax]
+    int* fz_slot = reinterpret_cast<int*>(smem + 16384 + 8 * kFzMax * 8);
+    int fz_np = 0;
+    if (fz >= 0) {
+      const int entry = fz + kh;
+      const int p0 = table[off_merge_ptr + entry] + 1;  // the own slot comes first
+      fz_np = min(table[off_merge_ptr + entry + 1] - p0, kFzMax);
+      const int h = tid / kFzMax, p = tid % kFzMax;
+      if (h < g && p < fz_np) {
+        const int sl = table[off_merge_slot + p0 + p];
+        if (h == 0) fz_slot[p] = sl;
+        fz_ml[h * kFzMax + p] = __ldg(reinterpret_cast<const float2*>(part_ml) + (int64_t)sl * hq_local + kh * g + h);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kMmaWarps) : "memory");
+    }
+#pragma unroll 4
     for (int idx = tid; idx < g * kMmaD; idx += 32 * kMmaWarps) {
       const int h = idx / kMmaD, e = idx % kMmaD;
       float M = neg_inf<float>();
@@ -219,7 +238,30 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         O += x[16 + h * kMmaD + e] * f;
       }
       const int qh = kh * g + h;
-      if (slot < 0) {
+      if (fz >= 0) {
+        // fused merge (kern_merge.cu math): this suffix partial + the TC
+        // pieces' partials of (req, kv head) -- they completed before this
+        // kernel started; their (m, l) were staged in SMEM above
+        const int np = fz_np;
+        float Mn = M * 0.69314718055994530942f;  // natural-log units, like the stored partials
+#pragma unroll
+        for (int p = 0; p < kFzMax; ++p)
+          if (p < np && fz_ml[h * kFzMax + p].y > 0.f) Mn = fmaxf(Mn, fz_ml[h * kFzMax + p].x);
+        const float fo = __expf(M * 0.69314718055994530942f - Mn);
+        float Lt = L * fo, Ot = O * fo;
+        float ov[kFzMax];
+#pragma unroll
+        for (int p = 0; p < kFzMax; ++p)
+          ov[p] = p < np ? __ldg(part_o + ((int64_t)fz_slot[p] * hq_local + qh) * kMmaD + e) : 0.f;
+#pragma unroll
+        for (int p = 0; p < kFzMax; ++p) {
+          const float2 ml = fz_ml[h * kFzMax + p];
+          const float w = (p < np && ml.y > 0.f) ? ml.y * __expf(ml.x - Mn) : 0.f;
+          Lt += w;
+          Ot += w * ov[p];
+        }
+        out[((int64_t)req * hq_local + qh) * kMmaD + e] = Ot / Lt;
+      } else if (slot < 0) {
         out[((int64_t)req * hq_local + qh) * kMmaD + e] = O / L;
       } else {
         const int64_t ei = (int64_t)slot * hq_local + qh;
@@ -242,7 +284,8 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
 
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
-                        void* part_o, void* part_ml, cudaStream_t st, long long* ctalog) {
+                        void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
+                        long long* ctalog) {
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
@@ -255,7 +298,8 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   dim3 grid(n_groups, h_local);
   mma_pac_kernel<<<grid, kMmaThreads, kMmaSmem, st>>>(mk, mv, table, off_groups, off_rows,
                                                       (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
-                                                      (float*)out, (float*)part_o, (float*)part_ml, ctalog);
+                                                      (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
+                                                      off_merge_slot, ctalog);
   return cuda_status(cudaGetLastError(), "mma gemv launch");
 }
 

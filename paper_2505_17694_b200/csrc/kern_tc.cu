@@ -407,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         pc.next();
       };
       int tp = 0;
-      const int lookahead = (dbg_flags & 4096) ? 2 : 3;  // S tiles issued ahead of the next PV
+      constexpr int lookahead = 3;  // S tiles issued ahead of the next PV
       while (!pc.done()) {
         if (!sc.done() && ts <= tp + lookahead) {
           if (sc.j == 0 && tp < ts && !tc::mbar_ready(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1)) {

@@ -305,3 +305,33 @@ class TestConcurrency:
             assert np.array_equal(o, outs[0])
         ups = upcast_spec(spec)
         assert_bf16_close(outs[0], OA.naive_attention(ups.queries, oracle_forest(ups)))
+
+
+class TestSuffixPaths:
+    """The suffix (unshared-node) groups run on the mma.sync kernel and the
+    merge kernel combines the partials; CODEC_FLAG_FUSED_MERGE makes the
+    suffix kernel fold each request's TC partials into its output itself,
+    CODEC_FLAG_GEMV_SIMT swaps in the CUDA-core GEMV kernel. All three agree
+    with the oracle, with and without ragged visibility."""
+
+    @pytest.mark.parametrize("with_masks", [False, True])
+    def test_paths_agree(self, cuda_ok, table, with_masks):
+        spec = W.two_level(1500, 300, 40, h_q=32, h_kv=8, d=128, seed=11)
+        if with_masks:
+            spec = d128_forest(12, with_masks=True)
+        f, q = build(spec, "bfloat16")
+        plan = P.plan_device(f, spec.h_q // spec.h_kv, table, spec.h_kv, 148)
+        kp, vp = f.device_pool("bfloat16")
+        qd = q.queries.cuda()
+        outs = {}
+        for name, fl in (("fused", 4096), ("merge_kernel", 0), ("simt", 2048)):
+            st = DecodeStep(f, plan, spec.h_q, "bfloat16", flags=fl, concurrent=False)
+            if name == "fused" and not with_masks:
+                assert st.info.n_merge_fused > 0
+            outs[name] = np_(st(qd, kp, vp))
+        ups = upcast_spec(spec)
+        ref = OA.naive_attention(ups.queries, oracle_forest(ups))
+        for name, o in outs.items():
+            assert_bf16_close(o, ref)
+        scale = float(np.max(np.abs(outs["merge_kernel"])))
+        assert np.max(np.abs(outs["fused"] - outs["merge_kernel"])) <= 1e-4 * scale
