@@ -285,7 +285,7 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog) {
+                        long long* ctalog, bool after_tc) {
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
@@ -295,11 +295,25 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   if (e != cudaSuccess) return cuda_status(e, "mma smem attribute");
   e = cudaFuncSetAttribute(mma_pac_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return cuda_status(e, "mma carveout attribute");
-  dim3 grid(n_groups, h_local);
-  mma_pac_kernel<<<grid, kMmaThreads, kMmaSmem, st>>>(mk, mv, table, off_groups, off_rows,
-                                                      (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
-                                                      (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
-                                                      off_merge_slot, ctalog);
+  // Programmatic dependent launch after the TC kernel: the suffix CTAs do
+  // not read its output, so they may start on any SM the TC grid leaves
+  // idle or has finished with (a running TC CTA holds its SM's whole
+  // register file and shared memory, so nothing ever co-resides with it).
+  // Not with the fused merge, which reads the TC partials.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_groups, h_local);
+  cfg.blockDim = dim3(kMmaThreads);
+  cfg.dynamicSmemBytes = kMmaSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = after_tc ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, mma_pac_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
+                         pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
+                         off_merge_slot, ctalog);
+  if (e != cudaSuccess) return cuda_status(e, "mma gemv launch");
   return cuda_status(cudaGetLastError(), "mma gemv launch");
 }
 

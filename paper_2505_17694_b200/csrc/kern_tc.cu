@@ -235,6 +235,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     tc::prefetch_tmap(&tmv);
   }
   tc::fence_before();
+  // the suffix kernel launched after this one (programmatic dependent
+  // launch) may take any SM this grid leaves idle or releases
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;

@@ -23,7 +23,7 @@ int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_grou
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog);
+                        long long* ctalog, bool after_tc);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -151,7 +151,8 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
-                              info->off_merge_slot, st, ctalog));
+                              info->off_merge_slot, st, ctalog,
+                              do_tc && info->n_merge_fused == 0 && !kev));
   else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
