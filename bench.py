@@ -37,14 +37,27 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "decode-attn µs/step & effective KV GB/s (unique bytes) vs HBM roofline, 1-8 GPU"
-CONFIGS = {
-    "cfg2": dict(shared_len=32768, leaf_len=512, batch=256, h_q=32, h_kv=8, d=128,
+CONFIGS = {  # BASELINE.json "configs"; structures from workloads.make_config
+    "cfg1": dict(h_q=8, h_kv=8, d=128,
+                 label="cfg1: tiny 2-level tree, 16 requests sharing a 1K prefix + 64-token suffixes, 8 heads x d128"),
+    "cfg2": dict(h_q=32, h_kv=8, d=128,
                  label="cfg2: Llama-3-8B shape (32 q / 8 kv heads, d128, bf16 KV), 256 requests sharing a "
                        "32K system prompt + 512-token suffixes"),
-    "cfg5": dict(shared_len=65536, leaf_len=512, batch=1024, h_q=64, h_kv=8, d=128,
+    "cfg3": dict(h_q=32, h_kv=8, d=128,
+                 label="cfg3: tree-of-thought / beam tree, depth 4, branching 4, 8K root, irregular node lengths "
+                       "(64 requests), Llama-3-8B heads"),
+    "cfg4": dict(h_q=32, h_kv=8, d=128, cpu_trees=range(8),
+                 label="cfg4: imbalanced forest, 64 trees with 512..128K shared prefixes and 1..512 requests per "
+                       "tree + 512-token suffixes (4680 requests), Llama-3-8B heads"),
+    "cfg5": dict(h_q=64, h_kv=8, d=128,
                  label="cfg5: Llama-3-70B shape (64 q / 8 kv heads, d128, bf16 KV), 1024 requests sharing a "
                        "64K prefix + 512-token suffixes"),
 }
+
+
+def structure(name, **kw):
+    from paper_2505_17694_b200 import workloads as W
+    return W.make_config(name, **kw)
 
 
 def peaks():
@@ -120,8 +133,8 @@ def cpu_reference_sample(cfg, workers=None, seed=0):
     workers = workers or os.cpu_count()
     key = (cfg["label"], seed)
     if key not in _CPU_CACHE:
-        spec = W.two_level(cfg["shared_len"], cfg["leaf_len"], cfg["batch"], h_q=cfg["h_q"], h_kv=cfg["h_kv"],
-                           d=cfg["d"], seed=seed, dtype=np.float32)
+        over = {"only_trees": cfg["cpu_trees"]} if "cpu_trees" in cfg else {}
+        spec = structure(cfg["name"], dtype=np.float32, **over)
         z = np.zeros((0, cfg["h_kv"], cfg["d"]), np.float32)
         fd = OA.ForestData(spec.parent, [z] + spec.keys[1:], [z] + spec.values[1:], spec.paths)
         # the CPU's own best split: shared nodes sliced once per host thread so
@@ -137,9 +150,10 @@ def cpu_reference_sample(cfg, workers=None, seed=0):
     OA.execute(fd, spec.queries, subs, workers=workers)
     dt = time.perf_counter() - t0
     kv_bytes = sum(spec.length[1:]) * cfg["h_kv"] * cfg["d"] * 2 * 2
-    desc = (f"the whole workload: all {cfg['h_kv']} kv heads ({cfg['h_q']} q heads), all {cfg['batch']} requests, "
-            f"{cfg['shared_len']}-token root + suffixes; fp32 numpy oracle port of prefixdec.execute, "
-            f"{workers} threads, plan of {len(subs)} subtasks")
+    what = (f"trees {list(cfg['cpu_trees'])} of the workload ({spec.bs} requests)" if "cpu_trees" in cfg
+            else f"the whole workload ({spec.bs} requests)")
+    desc = (f"{what}: all {cfg['h_kv']} kv heads ({cfg['h_q']} q heads), {sum(spec.length[1:])} KV tokens; "
+            f"fp32 numpy oracle port of prefixdec.execute, {workers} threads, plan of {len(subs)} subtasks")
     return dt, kv_bytes, desc
 
 
@@ -162,7 +176,7 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"], "sample": "the whole workload per step"},
+        "config": {"workload": cfg["label"], "sample": desc},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": workers, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -196,7 +210,7 @@ def main():
     ap.add_argument("--quick", action="store_true", help="profiling run: no e2e / clocks / cpu baseline")
     ap.add_argument("--serial", action="store_true", help="one stream: TC, GEMV and merge back to back")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config], name=args.config)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -222,8 +236,9 @@ def main():
     g = h_q // h_kv
 
     # structure + device-resident synthetic KV pool (heads [h0, h0 + h_local))
-    spec = W.two_level(cfg["shared_len"], cfg["leaf_len"], cfg["batch"], h_q=h_q, h_kv=h_kv, d=d, tensors=False)
+    spec = structure(args.config, tensors=False)
     forest = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, h_kv, d)
+    bs = spec.bs
     T = forest.total_tokens
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + h0)
@@ -231,7 +246,7 @@ def main():
     kp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
     vp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
     hq_local = h_local * g
-    q_host = (torch.randn((cfg["batch"], hq_local, d), generator=torch.Generator().manual_seed(99 + rank)) * sc
+    q_host = (torch.randn((bs, hq_local, d), generator=torch.Generator().manual_seed(99 + rank)) * sc
               ).to(torch.bfloat16).pin_memory()
     q_dev = q_host.to(dev)
 
@@ -241,7 +256,7 @@ def main():
     # tuned once per plan (cuDNN-benchmark style), untimed
     table = P.load_default_profile()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    out = torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32, device=dev)
+    out = torch.empty((bs, hq_local, d), dtype=torch.float32, device=dev)
 
     def make(budget):
         t0 = time.perf_counter()
@@ -254,10 +269,9 @@ def main():
                         flags=args.flags, tc_sm_budget=budget, concurrent=not args.serial)
         return pl, st, ms_plan
 
-    # the TC SM budget only matters when a suffix kernel can run beside the
-    # TC kernel (the CUDA-core GEMV on the aux stream); the default mma.sync
-    # suffix kernel runs after it on all SMs
-    budgets = [sms] if (args.serial or args.quick or not (args.flags & 2048)) else [sms, 136, 128, 120, 112, 104, 96]
+    # TC SM budget: the SMs the TC grid leaves free run the suffix kernel
+    # from the start (programmatic dependent launch); tuned once per plan
+    budgets = [sms] if (args.serial or args.quick) else [sms, 136, 128, 120, 112, 104, 96, 88]
     tune_ms = {}
     best = None
     for b in budgets:
@@ -287,7 +301,7 @@ def main():
     # would stop the suffix kernel's programmatic early launch in `value`
     step_ev = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
                          flags=args.flags | KERNEL_EVENTS, tc_sm_budget=budget, concurrent=not args.serial)
-    gathered = torch.empty((world, cfg["batch"], hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
+    gathered = torch.empty((world, bs, hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
 
     def one_step(qd):
         step(qd, kp, vp, out=out)
@@ -398,7 +412,7 @@ def main():
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         qbuf = [torch.empty_like(q_dev) for _ in range(2)]
         obuf = [torch.empty_like(out) for _ in range(2)]
-        ohost = [torch.empty((cfg["batch"], hq_local, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+        ohost = [torch.empty((bs, hq_local, d), dtype=torch.float32).pin_memory() for _ in range(2)]
         ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
         gath2 = [torch.empty_like(gathered) for _ in range(2)] if world > 1 else None
         st8 = {"k": 0}
@@ -465,8 +479,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "timed_windows": windows, "us_per_step": ms * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
-            "config": {"workload": cfg["label"], "bs": cfg["batch"], "h_q": h_q, "h_kv": h_kv, "d": d,
-                       "shared_len": cfg["shared_len"], "suffix_len": cfg["leaf_len"],
+            "config": {"workload": cfg["label"], "bs": bs, "h_q": h_q, "h_kv": h_kv, "d": d,
+                       "kv_tokens": int(sum(spec.length[1:])), "nodes": int(spec.n_nodes - 1),
                        "parallelism": f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else ""),
                        "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
                        "planner": {"m_tc": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,

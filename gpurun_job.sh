@@ -1,10 +1,11 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -1 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench exit $?"
+timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -1 gpurun_out/pytest_gpu.log
+for c in cfg2 cfg5 cfg4; do
+timeout 400 python bench.py --config $c --no-cpu-baseline --steps 10 > gpurun_out/bench_$c.log 2>&1; echo "bench $c exit $?"
 python -c "
 import json
-for l in open('gpurun_out/bench.log'):
+for l in open('gpurun_out/bench_$c.log'):
   if l.startswith('{'):
-    d=json.loads(l); print('us/step %.1f GB/s %.0f'%(d['us_per_step'],d['value']), {k:round(v['ms']*1e3,1) for k,v in d['kernels'].items()}, d['kernels_window_ms_per_step'], d['clocks']['sm_mhz'], 'e2e', round(d['e2e']['value']))
+    d=json.loads(l); print('$c us/step %.1f GB/s %.0f'%(d['us_per_step'],d['value']), {k:round(v['ms']*1e3,1) for k,v in d['kernels'].items()}, 'budget', d['config']['tc_sm_budget'], d['config']['autotune_ms'], 'e2e', round(d['e2e']['value']))
 "
-tail -2 gpurun_out/bench.log | grep -i error
+done

@@ -268,41 +268,53 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       for (int32_t gi : lanes[c]) lane_w[c] += tiles_of(gi) * h_local;
       w_all += lane_w[c];
     }
-    // pairs per lane, proportional to its work (at least one per busy lane)
+    // Every pair gets T = ceil(W / pairs) tiles. Lane c runs on floor(W_c /
+    // T) pairs of its own (in lockstep with the other lanes); the tails
+    // that do not fill a whole pair -- the ends of the lanes, which cover
+    // the same KV region in every lane -- are pooled in lane order and cut
+    // for the remaining pairs. (Whole lanes only would idle pairs whenever
+    // the lane count does not divide them: 10 of 74 at 16 lanes.)
+    const int64_t T = std::max<int64_t>(1, (w_all + pairs - 1) / pairs);
     std::vector<int32_t> lane_p(lanes.size(), 0);
     int32_t used = 0;
     for (size_t c = 0; c < lanes.size(); ++c) {
-      lane_p[c] = (int32_t)std::max<int64_t>(lane_w[c] > 0 ? 1 : 0, (int64_t)pairs * lane_w[c] / std::max<int64_t>(w_all, 1));
-      lane_p[c] = (int32_t)std::min<int64_t>(lane_p[c], std::max<int64_t>(lane_w[c], 1));
+      lane_p[c] = (int32_t)(lane_w[c] / T);
       used += lane_p[c];
     }
-    while (used > pairs) {  // more busy lanes than pairs: shrink the widest
-      size_t c = std::max_element(lane_p.begin(), lane_p.end()) - lane_p.begin();
-      if (lane_p[c] <= 1) break;
-      --lane_p[c];
-      --used;
-    }
+    // (lane-major unit sequence; pos = tiles of the lane before the unit)
+    int32_t tail_pair = used;  // pairs after the lane pairs take the pooled tails
+    int64_t tail_pos = 0;      // tiles already cut from the pool
     int32_t pair0 = 0;
     for (size_t c = 0; c < lanes.size(); ++c) {
       if (lane_w[c] == 0) continue;
-      const int32_t pc = std::max(1, lane_p[c]);
-      const int64_t per = (lane_w[c] + pc - 1) / pc;
-      int64_t pos = 0;  // tiles of this lane already cut
+      const int64_t main_end = (int64_t)lane_p[c] * T;  // lane tiles on the lane's own pairs
+      int64_t pos = 0;
       for (int32_t gi : lanes[c])
         for (int32_t h = 0; h < h_local; ++h) {
           const int64_t nt = tiles_of(gi);
           int64_t t = 0;
           while (t < nt) {
-            const int64_t pair_in_lane = std::min<int64_t>(pos / per, pc - 1);
-            const int64_t end_of_pair = (pair_in_lane + 1) * per;
-            const int64_t take = pair_in_lane == pc - 1 ? nt - t : std::min(nt - t, end_of_pair - pos);
-            pieces.push_back({gi, h, (int32_t)t, (int32_t)(t + take), pair0 + (int32_t)pair_in_lane});
+            int64_t take, pair;
+            if (pos < main_end) {
+              const int64_t k = pos / T;
+              take = std::min(nt - t, (k + 1) * T - pos);
+              pair = pair0 + k;
+            } else {
+              const int64_t k = tail_pos / T;
+              take = std::min(nt - t, (k + 1) * T - tail_pos);
+              pair = tail_pair + std::min<int64_t>(k, std::max(0, pairs - 1 - tail_pair));
+              tail_pos += take;
+            }
+            pieces.push_back({gi, h, (int32_t)t, (int32_t)(t + take), (int32_t)pair});
             t += take;
             pos += take;
           }
         }
-      pair0 += pc;
+      pair0 += lane_p[c];
     }
+    const int32_t n_tail = (int32_t)((tail_pos + T - 1) / T);
+    n_pairs = std::min<int32_t>(pairs, used + n_tail);
+    pair0 = n_pairs;
     n_pairs = pair0;
   }
   // piece rows (their own records: visible tokens within the piece) and the

@@ -335,3 +335,65 @@ class TestSuffixPaths:
             assert_bf16_close(o, ref)
         scale = float(np.max(np.abs(outs["merge_kernel"])))
         assert np.max(np.abs(outs["fused"] - outs["merge_kernel"])) <= 1e-4 * scale
+
+
+def _full_config(name, seed=0):
+    """A BASELINE.json config at full size: structure from workloads, bf16
+    K/V/Q drawn on the device (seeded), the device plan and step."""
+    import torch
+    spec = W.make_config(name, tensors=False)
+    h_q, h_kv, d = spec.h_q, spec.h_kv, spec.d
+    f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, h_kv, d)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    sc = 1.0 / math.sqrt(d)
+    T = f.total_tokens
+    kp = (torch.randn((h_kv, T, d), generator=gen, device="cuda") * sc).to(torch.bfloat16)
+    vp = (torch.randn((h_kv, T, d), generator=gen, device="cuda") * sc).to(torch.bfloat16)
+    q = (torch.randn((f.bs, h_q, d), generator=gen, device="cuda") * sc).to(torch.bfloat16)
+    table = P.load_default_profile()
+    plan = P.plan_device(f, h_q // h_kv, table, h_kv, torch.cuda.get_device_properties(0).multi_processor_count)
+    return f, kp, vp, q, DecodeStep(f, plan, h_q, "bfloat16", concurrent=False)
+
+
+def _path_reference(f, kp, vp, q, r):
+    """Single-softmax attention of request r over its root-to-leaf path
+    (naive_attention, attention.py:164-187) in float64 on the device, from
+    the same bf16 values: a plain torch reference for full-size checks."""
+    import torch
+    toks = torch.cat([torch.arange(f.token_offset[n], f.token_offset[n] + f.visible_count(n, r), device="cuda")
+                      for n in f.paths[r]])
+    g = q.shape[1] // f.h_kv
+    k = kp[:, toks].double()                      # [h_kv, L, d]
+    v = vp[:, toks].double()
+    qq = q[r].double().view(f.h_kv, g, -1)        # [h_kv, g, d]
+    s = torch.einsum("hgd,hld->hgl", qq, k) / math.sqrt(f.d)
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hgl,hld->hgd", p, v).reshape(q.shape[1], -1)
+
+
+class TestFullConfigs:
+    """cfg3 (tree-of-thought), cfg4 (imbalanced 64-tree forest, 17.5 GB of
+    KV) and cfg5 (Llama-3-70B shape) at their BASELINE.json sizes through
+    the device path; sampled requests against a float64 reference of the
+    same bf16 inputs, the bf16 bar (max-abs 2e-3 and rel 1e-2)."""
+
+    @pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
+    def test_sampled_requests(self, cuda_ok, name):
+        import torch
+        f, kp, vp, q, step = _full_config(name, seed=7)
+        out = step(q, kp, vp)
+        torch.cuda.synchronize()
+        assert bool(torch.isfinite(out).all())
+        rng = np.random.default_rng(3)
+        # spread over the forest, shortest paths first for cfg4 (prefixes up to 128K tokens)
+        lens = np.array([f.request_len(r) for r in range(f.bs)])
+        pool = np.argsort(lens)[: max(8, f.bs // 4)] if name == "cfg4" else np.arange(f.bs)
+        for r in sorted(set(rng.choice(pool, size=min(6, len(pool)), replace=False).tolist()) | {f.bs - 1}):
+            ref = _path_reference(f, kp, vp, q, r)
+            got = out[r].double()
+            err = float((got - ref).abs().max())
+            rel = err / float(ref.abs().max())
+            assert err <= 2e-3 and rel <= 1e-2, (name, r, err, rel)
+        del kp, vp
+        torch.cuda.empty_cache()
