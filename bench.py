@@ -377,6 +377,9 @@ def main():
                          "algorithmic_flops": fl, "kv_bytes": kv_tc}
         kernels["tc"]["frac"] = kernels["tc"]["achieved"] / tf_sus
         kernels["tc"]["frac_of_burst"] = kernels["tc"]["achieved"] / tf_burst
+        # the TC grid holds tc_sm_budget SMs; the others stream the suffixes
+        kernels["tc"]["sms"] = int(min(budget, sms))
+        kernels["tc"]["frac_per_sm"] = kernels["tc"]["frac"] * sms / max(1, min(budget, sms))
     if "gemv" in phases:
         kb = work["unique_kv_bytes"] - kv_tc
         kernels["gemv"] = {"bound": "hbm", "achieved": kb / (phases["gemv"] * 1e-3) / 1e9, "peak": hbm,
@@ -401,7 +404,8 @@ def main():
     if dominant:
         k = kernels[dominant]
         roof = {"bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"],
-                "frac": k["frac"], "traffic": k.get("traffic"), "kernel": dominant, "peak_kind": peak_kind}
+                "frac": k["frac"], "traffic": k.get("traffic"), "kernel": dominant, "peak_kind": peak_kind,
+                "sms": k.get("sms"), "frac_per_sm": k.get("frac_per_sm")}
 
     e2e = None
     if not args.quick:

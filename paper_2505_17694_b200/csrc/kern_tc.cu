@@ -607,6 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
             p[0] = make_float2(fast_exp2(x[0].x), fast_exp2(x[0].y));
             p[1] = make_float2(fast_exp2(x[1].x), fast_exp2(x[1].y));
+            // (measured: 6/8 on MUFU = 7/8 = 8/8 within noise, 4/8 is 4% slower)
             p[2] = make_float2(fast_exp2(x[2].x), fast_exp2(x[2].y));
             p[3] = poly_exp2x2(x[3]);
 #pragma unroll
