@@ -18,7 +18,8 @@ constexpr int kGrpLen = 1;      // slice length (tokens)
 constexpr int kGrpRowBegin = 2; // first row record
 constexpr int kGrpNRows = 3;    // number of requests in the group
 constexpr int kGrpMaxVis = 4;   // most visible tokens of any row (kernels size their tile loop by it)
-constexpr int kGrpNode = 5;     // forest node (diagnostics)
+constexpr int kGrpNode = 5;     // GEMV / generic: forest node (diagnostics)
+constexpr int kGrpQReq0 = 5;    // TC pieces: first request of a consecutive request run (Q by TMA), else -1
 constexpr int kGrpBlock = 6;    // TC: schedule block (CTA pair) of the unit
 constexpr int kGrpHead = 7;     // TC: local kv head of the unit
 

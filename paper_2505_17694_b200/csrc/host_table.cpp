@@ -344,6 +344,10 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       ++rec.n_rows;
       rec.max_vis = std::max<int32_t>(rec.max_vis, (int32_t)v);
     }
+    // consecutive request ids: the kernel loads the piece's Q rows with TMA
+    rec.node = rec.n_rows > 0 ? rows[4 * rec.row_begin] : -1;
+    for (int32_t k = 1; k < rec.n_rows; ++k)
+      if (rows[4 * (rec.row_begin + k)] != rec.node + k) rec.node = -1;
     if (rec.n_rows > 0) prec.push_back(rec);
   }
   // ---- slots. Per request and kv head: the shared (GEMV / generic) partials

@@ -81,6 +81,7 @@ struct TcBars {
   uint64_t v_full[kTcVStages], v_empty[kTcVStages];
   uint64_t q_full[2], q_empty[2], s_full[2], s_free[2], p_full[2];
   uint64_t epi_done[2];  // unit n's epilogue no longer uses Q buffer n % 2 as staging
+  uint64_t q_tma[2];     // this CTA's TMA Q load of buffer b landed (local)
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4] (parity waits stay within one phase)
   uint64_t o_free;
   uint32_t tmem_slot;
@@ -125,7 +126,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 struct GroupView {
-  int kv_tok, n_req, n_tiles, kh;
+  int kv_tok, n_req, n_tiles, kh, qreq0;
   const int32_t* rows;
 };
 
@@ -135,6 +136,7 @@ __device__ __forceinline__ GroupView group_view(const int32_t* table, int off_gr
   v.kv_tok = grp[kGrpKvTok];
   v.n_req = grp[kGrpNRows];
   v.kh = grp[kGrpHead];
+  v.qreq0 = grp[kGrpQReq0];
   v.rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
   v.n_tiles = (grp[kGrpMaxVis] + kTcBN - 1) / kTcBN;
   return v;
@@ -185,7 +187,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     tc_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                  const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
+                  const __grid_constant__ CUtensorMap tmq, const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                   long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog) {
@@ -221,6 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       mbar_init(&bars->q_full[i], 2);  // the Q warps of both CTAs
       mbar_init(&bars->q_empty[i], 1);
       mbar_init(&bars->epi_done[i], 4);  // the epilogue group's 4 warps (this CTA)
+      mbar_init(&bars->q_tma[i], 1);
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], kGroupWarpArrivals);
       mbar_init(&bars->p_full[i], kGroupWarpArrivals);
@@ -302,6 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // SW128; the buffer is reused once the unit two back issued its last S
     const int nq_local = hq_local;
     int n = 0;
+    int qtma_uses[2] = {0, 0};  // phases of q_tma[b]
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       if (gv.n_tiles == 0) continue;
@@ -315,6 +319,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         mbar_wait(&bars->epi_done[qb], ((n - 2) >> 1) & 1);  // staging of unit n - 2's O
       }
       uint8_t* qs = smem + kOffQ + qb * kQBytes;
+      if (gv.qreq0 >= 0) {
+        // consecutive requests: two 4D TMA boxes (64 d x g heads x 128/g
+        // requests, SW128) -- one round trip instead of a gather
+        const int rq = 128 / g;
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&bars->q_tma[qb], kQBytes);
+          tc::tma_load_4d(qs, &tmq, 0, 0, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[qb]);
+          tc::tma_load_4d(qs + kQAtom, &tmq, 0, 1, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[qb]);
+        }
+        mbar_wait(&bars->q_tma[qb], (qtma_uses[qb]++) & 1);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(&bars->q_full[qb], 0);
+        ++n;
+        continue;
+      }
 #pragma unroll 1
       for (int i0 = 0; i0 < 64; i0 += 8) {
         uint4 v[8];
@@ -803,8 +822,32 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
 constexpr int kTraceLen = 17 * 2 * 64;
 static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
 
+// Q [bs][hq_local][128] bf16 viewed as [bs][hq_local][2 halves][64 d]: a box
+// of 64 d x 1 half x g heads x 128/g requests is one CTA's 128 Q rows of a
+// piece with consecutive requests, in the SW128 K-major layout the MMA reads
+static int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_local, int g) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !p)
+      return fail(CODEC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  cuuint64_t dims[4] = {64, 2, (cuuint64_t)hq_local, (cuuint64_t)bs};
+  cuuint64_t strides[3] = {128, (cuuint64_t)kTcD * 2, (cuuint64_t)hq_local * kTcD * 2};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CODEC_ERR_CUDA, "cuTensorMapEncodeTiled (q) failed (%d)", (int)r);
+  return CODEC_OK;
+}
+
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
-                  int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
+                  int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
                   cudaStream_t st, int flags, long long* ctalog) {
   const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
@@ -812,13 +855,14 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
     cudaMemsetAsync(g_trace, 0, kTraceLen * sizeof(long long), st);
   }
   if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
-  CUtensorMap mk, mv;
+  CUtensorMap mk, mv, mq;
   CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, 64));      // K half: 64 tokens
   CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kTcBN));   // V half: 64 d columns
+  CODEC_TRY(encode_q_map(&mq, q, bs, h_local * g, g));
   cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   if (e != cudaSuccess) return cuda_status(e, "tc smem attribute");
   dim3 grid(kTcCtasPerBlock * in.n_tc_blocks, 1);  // CTA pairs (__cluster_dims__); heads come from the units
-  tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
+  tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, mq, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
                                                    trace ? g_trace : nullptr, flags, ctalog);

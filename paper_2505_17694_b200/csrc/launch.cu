@@ -13,7 +13,7 @@
 
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
-                  int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
+                  int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
                   cudaStream_t st, int flags, long long* ctalog);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
@@ -145,7 +145,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool kev = (dims->flags & CODEC_FLAG_KERNEL_EVENTS) && !fork;
   if (kev) CODEC_TRY(kev_record(0, st));
   if (do_tc)
-    CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
+    CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
                         dims->flags, ctalog));
   if (kev) CODEC_TRY(kev_record(1, st));
   if (mma_gemv)
