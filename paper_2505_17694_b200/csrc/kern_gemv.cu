@@ -1,5 +1,6 @@
-// K3: unshared / lightly shared nodes -- bulk-async streamed, warp-shuffle
-// GEMV split attention on CUDA cores.
+// K3' (fp32 KV, d in {64, 256}, g <= 16, or CODEC_FLAG_GEMV_SIMT): unshared /
+// lightly shared nodes -- bulk-async streamed, warp-shuffle GEMV split
+// attention on CUDA cores. bf16 d=128 suffixes run on kern_mma.cu instead.
 //
 // Same math as the reference's pac_kernel (_kernels.pyx:25-54): scores
 // q.k/sqrt(d) over the visible prefix, online softmax, normalised output
@@ -28,9 +29,9 @@
 
 namespace codec {
 
-constexpr int kGemvWarps = 2;                  // consumer warps (3 warps per CTA: one per SMSP next to a TC CTA)
+constexpr int kGemvWarps = 4;                  // consumer warps
 constexpr int kGemvThreads = 32 * (kGemvWarps + 1);
-constexpr int kGemvStages = 3;                 // 48 KB ring: fits beside a TC CTA on one SM
+constexpr int kGemvStages = 4;
 constexpr int kGemvStageBytes = 8192;          // K (and V) bytes per stage
 
 template <typename T, int D, int R>
