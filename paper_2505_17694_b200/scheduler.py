@@ -138,6 +138,7 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
+SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
 
 
 def concat_plans(plans) -> DivisionPlan:
@@ -178,8 +179,14 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     plans = []
     if tc:
         plans.append(plan_uniform_bk(tc, table, pairs, 1))
-    if gv:  # one block per GEMV task: its makespan is the longest single task
-        plans.append(plan_uniform_bk(gv, table, len(gv), 1))
+    # suffix-kernel tasks: one CTA streams a slice at a few tens of GB/s, so
+    # long ones (a lightly shared 128K-token root in cfg4) are cut into
+    # slices of <= SUFFIX_SLICE tokens that run on separate CTAs
+    by_bk = {}
+    for t in gv:
+        by_bk.setdefault(max(1, -(-t.n // SUFFIX_SLICE)), []).append(t)
+    for bk in sorted(by_bk):
+        plans.append(plan_uniform_bk(by_bk[bk], table, len(by_bk[bk]) * bk, bk))
     return concat_plans(plans)
 
 
