@@ -127,6 +127,27 @@ class DecodeStep:
             C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None))
         return out
 
+    def capture(self, q, k_pool, v_pool, out):
+        """Record one decode step over these buffers into a CUDA graph and
+        return its replay function: the serving loop re-runs the step with
+        new query values written into `q` in place, without the per-step
+        host work (tensor-map encoding, argument checks, launches)."""
+        import torch
+
+        if self.aux is not None and (self.flags & 2048):
+            raise ValueError("capture() needs the single-stream launch (no aux-stream GEMV)")
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):  # warm the kernels' attributes outside the capture
+            self(q, k_pool, v_pool, out=out, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self(q, k_pool, v_pool, out=out, stream=s)
+        self._graph = graph  # keep alive with the step
+        return graph.replay
+
     def with_budget(self, tc_sm_budget: int) -> "DecodeStep":
         return DecodeStep(self.forest, self.plan, self.h_q, self.tdtype, self.head_begin, self.head_end,
                           self.device, self.flags, tc_sm_budget, self.aux is not None)

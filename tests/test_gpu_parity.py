@@ -397,3 +397,26 @@ class TestFullConfigs:
             assert err <= 2e-3 and rel <= 1e-2, (name, r, err, rel)
         del kp, vp
         torch.cuda.empty_cache()
+
+
+class TestGraph:
+    def test_capture_replay_matches(self, cuda_ok, table):
+        """DecodeStep.capture(): a CUDA-graph replay of the step gives the
+        direct call's result bit for bit, also after new query values are
+        written into the captured buffer."""
+        import torch
+        spec = W.two_level(3000, 200, 48, h_q=32, h_kv=8, d=128, seed=21)
+        f, q = build(spec, "bfloat16")
+        plan = P.plan_device(f, 4, table, 8, 148)
+        kp, vp = f.device_pool("bfloat16")
+        qd = q.queries.cuda().contiguous()
+        step = DecodeStep(f, plan, 32, "bfloat16", concurrent=False)
+        out = torch.empty((f.bs, 32, 128), dtype=torch.float32, device="cuda")
+        replay = step.capture(qd, kp, vp, out)
+        for trial in range(2):
+            if trial:
+                qd.copy_((torch.randn_like(qd, dtype=torch.float32) * 0.1).to(torch.bfloat16))
+            replay()
+            torch.cuda.synchronize()
+            direct = step(qd, kp, vp)
+            assert np.array_equal(np_(out), np_(direct))
