@@ -148,6 +148,46 @@ class DecodeStep:
         self._graph = graph  # keep alive with the step
         return graph.replay
 
+    def grow(self, delta: int = 1) -> None:
+        """Decode-step growth between re-plans (the
+        reference re-plans every DEFAULT_REPLAN_EVERY steps, scheduler.py:23).
+        Build the forest with spare leaf capacity (leaf length > visible_len),
+        write each request's new token K/V into the pool at
+        token_offset[leaf] + visible, then call grow(): every request's leaf
+        sees `delta` more tokens. Only the suffix groups' row records change,
+        in place in the device table, so a captured graph replays the grown
+        step unchanged; shared nodes are untouched. The forest object (and
+        its index) keep the visible counts they were built with -- the next
+        re-plan builds a new forest. Raises ValueError when a leaf has no
+        room left (re-plan with new capacity)."""
+        import torch
+
+        i, blob = self.info, self.blob_host
+        extra = getattr(self, "_grown", 0)
+        leaf = {n.id for n in self.forest.nodes[1:] if not self.forest.children[n.id]}
+        touched = []
+        for off, count in ((i.off_gemv, i.n_gemv_groups), (i.off_gen, i.n_gen_groups)):
+            for gidx in range(count):
+                rec = off + 8 * gidx
+                node = int(blob[rec + 5])
+                if node not in leaf:
+                    continue
+                start_tok = int(blob[rec]) - self.forest.token_offset[node]  # slice start within the node
+                for k in range(int(blob[rec + 3])):
+                    r = i.off_rows + 4 * (int(blob[rec + 2]) + k)
+                    vis = int(blob[r + 1])
+                    if start_tok + vis != self.forest.visible_count(node, int(blob[r])) + extra:
+                        continue  # not the request's last slice of this leaf
+                    if vis + delta > int(blob[rec + 1]):
+                        raise ValueError(f"leaf {node} has no room for {delta} more tokens: re-plan")
+                    blob[r + 1] = vis + delta
+                    blob[rec + 4] = max(int(blob[rec + 4]), vis + delta)
+                    touched += [r + 1, rec + 4]
+        self._grown = extra + delta
+        if touched:
+            lo, hi = min(touched), max(touched) + 1
+            self.table[lo:hi].copy_(torch.from_numpy(blob[lo:hi]))
+
     def with_budget(self, tc_sm_budget: int) -> "DecodeStep":
         return DecodeStep(self.forest, self.plan, self.h_q, self.tdtype, self.head_begin, self.head_end,
                           self.device, self.flags, tc_sm_budget, self.aux is not None)

@@ -420,3 +420,39 @@ class TestGraph:
             torch.cuda.synchronize()
             direct = step(qd, kp, vp)
             assert np.array_equal(np_(out), np_(direct))
+
+
+class TestGrow:
+    def test_grow_matches_rebuilt_step(self, cuda_ok, table):
+        """DecodeStep.grow(): leaves built with spare capacity (visible_len
+        below their length) grow one token per decode step in the device
+        table; each grown step equals a step built from scratch on a forest
+        whose visible counts include the new tokens -- also through a
+        captured CUDA graph."""
+        import torch
+        bs, shared, cap, start = 24, 2048, 160, 100
+        spec = W.two_level(shared, cap, bs, h_q=32, h_kv=8, d=128, seed=5, tensors=False)
+
+        def forest(leaf_visible):  # node 1 = the shared root, node 2 + r = request r's leaf
+            return P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128,
+                                      visible=[None] + [{r: leaf_visible} for r in range(bs)])
+
+        f0 = forest(start)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(3)
+        shape = (8, f0.total_tokens, 128)
+        kp = (torch.randn(shape, generator=gen, device="cuda") / math.sqrt(128)).to(torch.bfloat16)
+        vp = (torch.randn(shape, generator=gen, device="cuda") / math.sqrt(128)).to(torch.bfloat16)
+        q = (torch.randn((bs, 32, 128), generator=gen, device="cuda") / math.sqrt(128)).to(torch.bfloat16)
+        step = DecodeStep(f0, P.plan_device(f0, 4, table, 8, 148), 32, "bfloat16", concurrent=False)
+        out = torch.empty((bs, 32, 128), dtype=torch.float32, device="cuda")
+        replay = step.capture(q, kp, vp, out)
+        for k in range(1, 4):
+            step.grow(1)
+            replay()
+            torch.cuda.synchronize()
+            f2 = forest(start + k)
+            ref = DecodeStep(f2, P.plan_device(f2, 4, table, 8, 148), 32, "bfloat16", concurrent=False)(q, kp, vp)
+            assert np.array_equal(np_(out), np_(ref)), k
+        with pytest.raises(ValueError, match="no room"):
+            step.grow(cap)
