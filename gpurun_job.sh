@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -1 gpurun_out/pytest_gpu.log; grep -E "^E  |FAILED" gpurun_out/pytest_gpu.log | head -8
+cp paper_2505_17694_b200/profiles/b200_d128.csv gpurun_out/b200_d128_model.csv
+timeout 1200 python -m paper_2505_17694_b200.profile_b200 measure > gpurun_out/profile_measure.log 2>&1; echo "measure exit $?"
+cp paper_2505_17694_b200/profiles/b200_d128.csv gpurun_out/b200_d128_measured.csv
+tail -3 gpurun_out/profile_measure.log
