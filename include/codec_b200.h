@@ -189,6 +189,9 @@ typedef struct {
                                         instead of the merge kernel (opt-in: slower on cfg2 so far) */
 #define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* TC kernel skips its shared-node units: timing only, wrong output (debug) */
 #define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
+#define CODEC_FLAG_DBG_NO_LOADS 32768 /* TC producers skip the K/V TMA loads: timing only, wrong output (debug) */
+#define CODEC_FLAG_DBG_ISSUER_ONLY 131072 /* TC kernel runs only its MMA issuer, no waits: timing only (debug) */
+#define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,

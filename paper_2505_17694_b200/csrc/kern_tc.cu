@@ -31,7 +31,8 @@
 // P1 [320,384) O [384,512).
 // Warps: 0-3 softmax group A, 4-7 group B (lane quadrant = warp & 3),
 // 8 / 10 TMA producers of K / V (both CTAs load their halves; completion on
-// the leader's barriers), 9 TMEM allocator + MMA issuer (leader only).
+// the leader's barriers), 9 TMEM allocator + S MMA issuer (leader only),
+// 10 also the PV MMA issuer (leader only), 11 Q loads of later units.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -46,7 +47,7 @@ namespace codec {
 constexpr int kTcSoftmaxWarps = 8;           // 2 groups x 4 lane quadrants
 constexpr int kTcProducerWarp = kTcSoftmaxWarps;       // K loads
 constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
-constexpr int kTcVProducerWarp = kTcSoftmaxWarps + 2;  // V loads (own warp: K must not queue behind V)
+constexpr int kTcVProducerWarp = kTcSoftmaxWarps + 2;  // V loads + PV MMAs (K must not queue behind V)
 constexpr int kTcQWarp = kTcSoftmaxWarps + 3;          // gathers the next unit's Q rows into SMEM
 constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 4);
 constexpr int kTcBN = 128;                   // tokens per KV tile
@@ -203,10 +204,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   const bool leader = rank == 0;
   const int blk = blockIdx.x >> 1;
   // optional timeline of pair (0, 0): trace[(event * 2 + rank) * 64 + tile]
+#ifdef CODEC_TC_TRACE
+  // debug builds only (CODEC_NVCC_EXTRA=-DCODEC_TC_TRACE): the stamps cost
+  // the single-warp MMA issuer ~70 instructions per tile even when off
   const bool tracing = trace != nullptr && blk == 0;
   auto stamp = [&](int ev, int tt) {
     if (tracing && tt < 64) trace[(ev * 2 + rank) * 64 + tt] = clock64();
   };
+  // sequential MMA-issuer log after the per-tile stamps: (clock, code << 16 | tile)
+  int seq_n = 0;
+  auto seq = [&](int code, int tt) {
+    if (tracing && seq_n < 2048) {
+      trace[17 * 2 * 64 + 2 * seq_n] = clock64();
+      trace[17 * 2 * 64 + 2 * seq_n + 1] = (code << 16) | (tt & 0xffff);
+      ++seq_n;
+    }
+  };
+#else
+  (void)trace;
+  auto stamp = [](int, int) {};
+  auto seq = [](int, int) {};
+#endif
   const int g_begin = table[off_block_ptr + blk];
   const int g_end = (dbg_flags & CODEC_FLAG_DBG_NO_TC_UNITS) ? g_begin : table[off_block_ptr + blk + 1];
 
@@ -244,23 +262,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
-  if (warp >= kTcSoftmaxWarps) {
+  const bool iso = (dbg_flags & CODEC_FLAG_DBG_ISSUER_ONLY) != 0;  // timing experiment
+  if (iso && warp != kTcMmaWarp && warp != kTcVProducerWarp) {
+    // nothing: only the MMA issuers run
+  } else if (warp >= kTcSoftmaxWarps) {
   // producer / MMA warpgroup: hands registers to the softmax warpgroups
 #ifndef CODEC_NO_SETMAXNREG
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegsOther));
 #endif
-  if (warp == kTcProducerWarp || warp == kTcVProducerWarp) {
-    // ================================================ TMA producers (both CTAs)
+  if (warp == kTcProducerWarp) {
+    // ================================================ K producer (both CTAs)
     // K half: tokens [64 rank, 64 rank + 64) x all 128 d (two SW128 atom
-    // columns); V half: all 128 tokens x d [64 rank, 64 rank + 64). K and V
-    // stream from separate warps: the S MMAs run ahead of the PV MMAs, so a
-    // K load must never wait behind a V slot.
-    const bool is_k = warp == kTcProducerWarp;
+    // columns), completing on the leader's k_full. Also warms L2 with the
+    // K and V tiles kTcPrefetch ahead.
     int t = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       const int row0 = gv.kh * (int)pool_tokens + gv.kv_tok;
-      if (is_k && tc::elect_one()) {
+      if (tc::elect_one()) {
         for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
           tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN + 64 * rank);
           tc::tma_prefetch_2d(&tmk, 64, row0 + j * kTcBN + 64 * rank);
@@ -270,32 +289,87 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
         const int y = row0 + j * kTcBN;
-        if (is_k) {
-          const int ks = t % kTcKStages;
-          PROG(3, t, 1);
-          if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
-          PROG(3, t, 2);
-          if (tc::elect_one()) {
-            if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
-            uint8_t* kd = smem + kOffK + ks * kHalfBytes;
-            tc::tma_load_2d_pair(kd, &tmk, 0, y + 64 * rank, &bars->k_full[ks]);
-            tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, y + 64 * rank, &bars->k_full[ks]);
-            if (j + kTcPrefetch < gv.n_tiles) {
-              const int yp = y + kTcPrefetch * kTcBN;
-              tc::tma_prefetch_2d(&tmk, 0, yp + 64 * rank);
-              tc::tma_prefetch_2d(&tmk, 64, yp + 64 * rank);
-              tc::tma_prefetch_2d(&tmv, 64 * rank, yp);
-            }
-          }
-        } else {
-          const int vs = t % kTcVStages;
-          if (t >= kTcVStages) mbar_wait(&bars->v_empty[vs], ((t / kTcVStages) - 1) & 1);
-          if (tc::elect_one()) {
-            if (leader) mbar_arrive_expect_tx(&bars->v_full[vs], 2 * kHalfBytes);
-            tc::tma_load_2d_pair(smem + kOffV + vs * kHalfBytes, &tmv, 64 * rank, y, &bars->v_full[vs]);
+        const int ks = t % kTcKStages;
+        PROG(3, t, 1);
+        if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
+        PROG(3, t, 2);
+        if (dbg_flags & CODEC_FLAG_DBG_NO_LOADS) {
+          if (leader && tc::elect_one()) mbar_arrive(&bars->k_full[ks]);
+        } else if (tc::elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
+          uint8_t* kd = smem + kOffK + ks * kHalfBytes;
+          tc::tma_load_2d_pair(kd, &tmk, 0, y + 64 * rank, &bars->k_full[ks]);
+          tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, y + 64 * rank, &bars->k_full[ks]);
+          if (j + kTcPrefetch < gv.n_tiles) {
+            const int yp = y + kTcPrefetch * kTcBN;
+            tc::tma_prefetch_2d(&tmk, 0, yp + 64 * rank);
+            tc::tma_prefetch_2d(&tmk, 64, yp + 64 * rank);
+            tc::tma_prefetch_2d(&tmv, 64 * rank, yp);
           }
         }
         __syncwarp();
+      }
+    }
+  } else if (warp == kTcVProducerWarp) {
+    // ================================================ V producer (both CTAs) + PV issuer (leader)
+    // V half: all 128 tokens x d [64 rank, 64 rank + 64), completing on the
+    // leader's v_full. The leader's warp interleaves its loads with the PV
+    // MMAs, kVAhead tiles ahead: V(tp + 4) reuses the stage of V(tp - 2),
+    // free once PV(tp - 2) landed -- which P(tp) waits for anyway, so the
+    // load never delays PV(tp). The S and PV MMAs come from two warps: one
+    // in-order issuer for both spent ~1800 clk per tile on its own
+    // instruction latency (the pipe needs 1024).
+    // PV: A = P (TMEM, 8 columns per 16 tokens), B = V half (MN-major SW128,
+    // one atom column).
+    constexpr int kVAhead = 4;
+    static_assert(kVAhead + 2 <= kTcVStages, "V(tp + kVAhead) must reuse a stage PV(tp - 2) released");
+    TileCursor vc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
+    vc.open();
+    int tv = 0;  // V tiles loaded
+    auto load_v = [&]() {
+      const int vs = tv % kTcVStages;
+      if (tv >= kTcVStages && !iso) mbar_wait(&bars->v_empty[vs], ((tv / kTcVStages) - 1) & 1);
+      if ((dbg_flags & CODEC_FLAG_DBG_NO_LOADS) || iso) {
+        if (leader && tc::elect_one() && !iso) mbar_arrive(&bars->v_full[vs]);
+      } else if (tc::elect_one()) {
+        if (leader) mbar_arrive_expect_tx(&bars->v_full[vs], 2 * kHalfBytes);
+        const int y = vc.gv.kh * (int)pool_tokens + vc.gv.kv_tok + vc.j * kTcBN;
+        tc::tma_load_2d_pair(smem + kOffV + vs * kHalfBytes, &tmv, 64 * rank, y, &bars->v_full[vs]);
+      }
+      __syncwarp();
+      vc.next();
+      ++tv;
+    };
+    if (!leader) {
+      while (!vc.done()) load_v();
+    } else {
+      while (!vc.done() && tv < kVAhead) load_v();
+      constexpr uint32_t idesc_o = tc::idesc_bf16(256, kTcD, false, true);
+      const uint64_t dv = tc::smem_desc(sbase + kOffV, kHalfBytes, 1024);
+      TileCursor pc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
+      pc.open();
+      for (int tp = 0; !pc.done(); ++tp) {
+        if (!vc.done()) load_v();  // V(tp + kVAhead)
+        const int b = tp & 1, vs = tp % kTcVStages;
+        if (lane == 0) seq(5, tp);
+        if (!iso) mbar_wait(&bars->p_full[b], (tp >> 1) & 1);  // P(tp) in both CTAs' TMEM
+        if (lane == 0) seq(6, tp);
+        if (!iso) mbar_wait(&bars->v_full[vs], (tp / kTcVStages) & 1);
+        if (lane == 0) seq(7, tp);
+        if (pc.j == 0 && pc.n > 0 && !iso) mbar_wait(&bars->o_free, (pc.n - 1) & 1);  // epilogue read O
+        tc::fence_after();
+        const uint64_t bv = dv + (uint64_t)((vs * kHalfBytes) >> 4);
+        if (tc::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kTcBN / 16; ++k)
+            tc::mma2_f16_ts(tmem + kColO, tmem + kColP + b * 64 + k * 8, bv + (uint64_t)((k * 16 * 128) >> 4),
+                            idesc_o, (pc.j > 0 || k > 0) ? 1u : 0u);
+          tc::commit_pair(&bars->v_empty[vs]);
+          tc::commit_pair(&bars->pv_done[tp & 3]);
+        }
+        __syncwarp();
+        if (lane == 0) seq(9, tp);
+        pc.next();
       }
     }
   } else if (warp == kTcQWarp) {
@@ -361,24 +435,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       ++n;
     }
   } else if (warp == kTcMmaWarp) {
-    // ================================================ MMA issuer (leader only)
+    // ================================================ S issuer (leader only)
+    // S(ts) into S buffer ts % 2 once the softmax pulled S(ts - 2) out of it
+    // (blocking waits: the issuing thread sleeps in mbarrier.try_wait). A
+    // new unit's Q may wait for the epilogue of the unit two back; the PV
+    // MMAs come from another warp, so that wait blocks nothing else.
+    // A = Q tile (K-major SW128, 16 KB atom columns), B = K half (K-major
+    // SW128, 8 KB atom columns).
     if (leader) {
-      // S: A = Q tile (K-major SW128, 16 KB atom columns), B = K half
-      // (K-major SW128, 8 KB atom columns). PV: A = P (TMEM, 8 columns per
-      // 16 tokens), B = V half (MN-major SW128, one atom column).
       constexpr uint32_t idesc_s = tc::idesc_bf16(256, kTcBN, false, false);
-      constexpr uint32_t idesc_o = tc::idesc_bf16(256, kTcD, false, true);
       const uint64_t dq = tc::smem_desc(sbase + kOffQ, 16, 1024);
       const uint64_t dk = tc::smem_desc(sbase + kOffK, 16, 1024);
-      const uint64_t dv = tc::smem_desc(sbase + kOffV, kHalfBytes, 1024);
       TileCursor sc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
       sc.open();
-      int ts = 0;  // next S tile (global)
-      auto issue_s = [&]() {
-        if (sc.done()) return;
+      for (int ts = 0; !sc.done(); ++ts) {
         const int s = ts % kTcKStages, b = ts & 1;
-        if (sc.j == 0) mbar_wait(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1);
-        mbar_wait(&bars->k_full[s], (ts / kTcKStages) & 1);  // (probed ready in the loop below)
+        if (lane == 0) seq(1, ts);
+        if (ts >= 2 && !iso) mbar_wait(&bars->s_free[b], ((ts - 2) >> 1) & 1);  // S(ts-2) pulled out by both CTAs
+        if (sc.j == 0 && !iso) mbar_wait(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1);
+        if (lane == 0) seq(2, ts);
+        if (!iso) mbar_wait(&bars->k_full[s], (ts / kTcKStages) & 1);
+        if (lane == 0) seq(3, ts);
         tc::fence_after();
         const uint64_t aq = dq + (uint64_t)(((sc.n & 1) * kQBytes) >> 4);
         const uint64_t bk = dk + (uint64_t)((s * kHalfBytes) >> 4);
@@ -394,58 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           if (sc.j + 1 == sc.gv.n_tiles) tc::commit_pair(&bars->q_empty[sc.n & 1]);  // unit's Q no longer read
         }
         __syncwarp();
+        if (lane == 0) seq(4, ts);
         sc.next();
-        ++ts;
-      };
-      // Issue order S0 S1 S2 S3 PV0 S4 PV1 S5 PV2 ...: S(ts) once ts <= tp + 3,
-      // else PV(tp), with blocking waits (the issuing thread sleeps in
-      // mbarrier.try_wait and wakes as soon as the phase completes -- a
-      // polling loop reacted 1-3k clk late on an SMSP shared with four
-      // softmax warps). Deadlock-free: every S / PV wait depends only on
-      // MMAs issued earlier, except a new unit's Q, which can wait for the
-      // epilogue of the unit two back (its O staging buffer) -- so before
-      // blocking on Q the pending PVs are issued first.
-      TileCursor pc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
-      pc.open();
-      auto issue_pv = [&](int tp) {
-        const int b = tp & 1, vs = tp % kTcVStages;
-        mbar_wait(&bars->p_full[b], (tp >> 1) & 1);  // P(tp) in both CTAs' TMEM
-        if (lane == 0) stamp(10, tp);
-        mbar_wait(&bars->v_full[vs], (tp / kTcVStages) & 1);
-        if (pc.j == 0 && pc.n > 0) mbar_wait(&bars->o_free, (pc.n - 1) & 1);  // epilogue read O
-        tc::fence_after();
-        if (lane == 0) stamp(0, tp);
-        const uint64_t bv = dv + (uint64_t)((vs * kHalfBytes) >> 4);
-        if (tc::elect_one()) {
-#pragma unroll
-          for (int k = 0; k < kTcBN / 16; ++k)
-            tc::mma2_f16_ts(tmem + kColO, tmem + kColP + b * 64 + k * 8, bv + (uint64_t)((k * 16 * 128) >> 4),
-                            idesc_o, (pc.j > 0 || k > 0) ? 1u : 0u);
-          tc::commit_pair(&bars->v_empty[vs]);
-          tc::commit_pair(&bars->pv_done[tp & 3]);
-        }
-        __syncwarp();
-        if (lane == 0) stamp(1, tp);
-        pc.next();
-      };
-      int tp = 0;
-      constexpr int lookahead = 3;  // S tiles issued ahead of the next PV
-      while (!pc.done()) {
-        if (!sc.done() && ts <= tp + lookahead) {
-          if (sc.j == 0 && tp < ts && !tc::mbar_ready(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1)) {
-            issue_pv(tp);
-            ++tp;
-            continue;
-          }
-          if (ts >= 2) mbar_wait(&bars->s_free[ts & 1], ((ts - 2) >> 1) & 1);  // S(ts-2) pulled out by both CTAs
-          if (lane == 0) stamp(8, ts);
-          if (lane == 0) stamp(13, ts);
-          issue_s();
-          if (lane == 0) stamp(6, ts - 3);
-          continue;
-        }
-        issue_pv(tp);
-        ++tp;
       }
       PROG(0, 9999, 7);
     }
@@ -588,7 +615,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
         // for at tile t-4; PV(t+2) cannot be)
         if (quad == 0) PROG(1 + grp, t, 5);
-        if (t >= 2) mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+        if (t >= 2 && (dbg_flags & (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM)) !=
+                          (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM))
+          mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
         if (quad == 0) PROG(1 + grp, t, 6);
         if (tid == grp * 128) stamp(12, t);
         // my row sum follows the reference
@@ -819,7 +848,7 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
   return CODEC_OK;
 }
 
-constexpr int kTraceLen = 17 * 2 * 64;
+constexpr int kTraceLen = 17 * 2 * 64 + 2 * 2048;
 static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
 
 // Q [bs][hq_local][128] bf16 viewed as [bs][hq_local][2 halves][64 d]: a box

@@ -72,4 +72,22 @@ units = np.diff(bp)
 recs = blob[info.off_tc: info.off_tc + 8 * info.n_tc_groups].reshape(-1, 8)
 tiles = [int(sum((recs[j, 4] + 127) // 128 for j in range(bp[b], bp[b + 1]))) for b in range(info.n_tc_blocks)]
 print("TC pairs", info.n_tc_blocks, "units/pair", np.bincount(units).tolist(), "tiles/pair min/med/max",
-      min(tiles), int(np.median(tiles)), max(tiles), "sfx slots", info.n_sfx_slots)
+      min(tiles), int(np.median(tiles)), max(tiles))
+
+# per-pair duration against its tiles / units (TC entries are indexed by blockIdx.x)
+tcl = a[:4096]
+dur = {}
+for x in range(2 * info.n_tc_blocks):
+    if tcl[x, 2] > 0:
+        dur.setdefault(x >> 1, []).append((tcl[x, 2] - tcl[x, 1]) / 1e3)
+rows = []
+for b in range(info.n_tc_blocks):
+    if b in dur:
+        rows.append((max(dur[b]), tiles[b], int(units[b]), int(tcl[2 * b, 0])))
+rows.sort()
+print("pair duration us / tiles / units / smid (fastest 8, slowest 8):")
+for r in rows[:8] + rows[-8:]:
+    print("  %.1f %d %d %d" % r)
+for u in sorted(set(r[2] for r in rows)):
+    d = [r[0] / r[1] for r in rows if r[2] == u]
+    print(f"units {u}: n={len(d)} us/tile mean {np.mean(d):.3f} min {np.min(d):.3f} max {np.max(d):.3f}")
