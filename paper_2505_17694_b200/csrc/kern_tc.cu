@@ -59,10 +59,14 @@ constexpr int kHalfBytes = 64 * 128 * 2;     // this CTA's half of a K or V tile
 constexpr int kKAtom = kHalfBytes / 2;       // K-half atom column: 64 tokens x 64 d (8 KB)
 // One CTA owns its SM: 384 threads x 168 registers at launch, then
 // setmaxnreg moves the role warps' surplus to the softmax warps (per SMSP:
-// 2 softmax warps x 200 + 1 role warp x 96 <= 512). No other kernel may
+// 2 softmax warps x 200 + 1 role warp x 96 <= 512; the pool the CTA got at
+// launch, 384 x 168, must cover it: 256 x 200 + 128 x 96 <= 64512). No other kernel may
 // share the SM: the hand-off corrupted the registers of a co-resident CTA
 // of another kernel in testing (tools/determinism.py).
 constexpr int kTcRegsSoftmax = 200, kTcRegsOther = 96;
+static_assert(32 * kTcSoftmaxWarps * kTcRegsSoftmax + (kTcThreads - 32 * kTcSoftmaxWarps) * kTcRegsOther <=
+                  kTcThreads * (65536 / kTcThreads / 8 * 8),
+              "setmaxnreg.inc would wait forever for registers the CTA does not own");
 constexpr int kTcKStages = 4, kTcVStages = 6;
 constexpr int kOffQ = 0;                     // Q0, Q1 (double-buffered across units)
 constexpr int kOffK = kOffQ + 2 * kQBytes;
@@ -193,6 +197,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                   long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog) {
   const long long t_start = ctalog ? global_ns() : 0;
+#ifdef CODEC_TC_DEBUG
+  // timing-only ablations (tools/tc_ablate.py); compiled out of the product
+  // build -- even untaken, their code cost the softmax ~110 register moves
+  // per tile
+  const int dbg = dbg_flags;
+#else
+  constexpr int dbg = 0;
+#endif
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   if (sbase & 1023) __trap();  // SWIZZLE_128B atoms need 1024-byte alignment
@@ -214,9 +226,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   // sequential MMA-issuer log after the per-tile stamps: (clock, code << 16 | tile)
   int seq_n = 0;
   auto seq = [&](int code, int tt) {
-    if (tracing && seq_n < 2048) {
-      trace[17 * 2 * 64 + 2 * seq_n] = clock64();
-      trace[17 * 2 * 64 + 2 * seq_n + 1] = (code << 16) | (tt & 0xffff);
+    // S issuer entries [0, 1024), PV issuer entries [1024, 2048)
+    const int base = warp == kTcVProducerWarp ? 1024 : 0;
+    if (tracing && seq_n < 1024) {
+      trace[17 * 2 * 64 + 2 * (base + seq_n)] = clock64();
+      trace[17 * 2 * 64 + 2 * (base + seq_n) + 1] = (code << 16) | (tt & 0xffff);
       ++seq_n;
     }
   };
@@ -225,8 +239,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   auto stamp = [](int, int) {};
   auto seq = [](int, int) {};
 #endif
-  const int g_begin = table[off_block_ptr + blk];
-  const int g_end = (dbg_flags & CODEC_FLAG_DBG_NO_TC_UNITS) ? g_begin : table[off_block_ptr + blk + 1];
+  // The block's unit range is re-read inside each role branch (asm loads
+  // the compiler cannot hoist): kept live across the setmaxnreg hand-off it
+  // was spilled to local memory and reloaded on the issuers' loop paths.
+  auto ld_range = [&](int& gb, int& ge) {
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(gb) : "l"(table + off_block_ptr + blk));
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(ge) : "l"(table + off_block_ptr + blk + 1));
+    if (dbg_flags & CODEC_FLAG_DBG_NO_TC_UNITS) ge = gb;
+  };
+#define CODEC_TC_RANGE \
+  int g_begin, g_end;  \
+  ld_range(g_begin, g_end)
 
   if (tid == 0) {
     for (int s = 0; s < kTcKStages; ++s) {
@@ -262,7 +285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
-  const bool iso = (dbg_flags & CODEC_FLAG_DBG_ISSUER_ONLY) != 0;  // timing experiment
+  const bool iso = (dbg & CODEC_FLAG_DBG_ISSUER_ONLY) != 0;  // timing experiment
   if (iso && warp != kTcMmaWarp && warp != kTcVProducerWarp) {
     // nothing: only the MMA issuers run
   } else if (warp >= kTcSoftmaxWarps) {
@@ -272,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #endif
   if (warp == kTcProducerWarp) {
     // ================================================ K producer (both CTAs)
+    CODEC_TC_RANGE;
     // K half: tokens [64 rank, 64 rank + 64) x all 128 d (two SW128 atom
     // columns), completing on the leader's k_full. Also warms L2 with the
     // K and V tiles kTcPrefetch ahead.
@@ -293,7 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         PROG(3, t, 1);
         if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
         PROG(3, t, 2);
-        if (dbg_flags & CODEC_FLAG_DBG_NO_LOADS) {
+        if (dbg & CODEC_FLAG_DBG_NO_LOADS) {
           if (leader && tc::elect_one()) mbar_arrive(&bars->k_full[ks]);
         } else if (tc::elect_one()) {
           if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
@@ -321,6 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // instruction latency (the pipe needs 1024).
     // PV: A = P (TMEM, 8 columns per 16 tokens), B = V half (MN-major SW128,
     // one atom column).
+    CODEC_TC_RANGE;
     constexpr int kVAhead = 4;
     static_assert(kVAhead + 2 <= kTcVStages, "V(tp + kVAhead) must reuse a stage PV(tp - 2) released");
     TileCursor vc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
@@ -329,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     auto load_v = [&]() {
       const int vs = tv % kTcVStages;
       if (tv >= kTcVStages && !iso) mbar_wait(&bars->v_empty[vs], ((tv / kTcVStages) - 1) & 1);
-      if ((dbg_flags & CODEC_FLAG_DBG_NO_LOADS) || iso) {
+      if ((dbg & CODEC_FLAG_DBG_NO_LOADS) || iso) {
         if (leader && tc::elect_one() && !iso) mbar_arrive(&bars->v_full[vs]);
       } else if (tc::elect_one()) {
         if (leader) mbar_arrive_expect_tx(&bars->v_full[vs], 2 * kHalfBytes);
@@ -377,6 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // this CTA's 128 query-head rows of each unit (row r = request r / g of
     // the unit, q head kv_head * g + r % g) into Q buffer n % 2, K-major
     // SW128; the buffer is reused once the unit two back issued its last S
+    CODEC_TC_RANGE;
     const int nq_local = hq_local;
     int n = 0;
     int qtma_uses[2] = {0, 0};  // phases of q_tma[b]
@@ -443,6 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // A = Q tile (K-major SW128, 16 KB atom columns), B = K half (K-major
     // SW128, 8 KB atom columns).
     if (leader) {
+      CODEC_TC_RANGE;
       constexpr uint32_t idesc_s = tc::idesc_bf16(256, kTcBN, false, false);
       const uint64_t dq = tc::smem_desc(sbase + kOffQ, 16, 1024);
       const uint64_t dk = tc::smem_desc(sbase + kOffK, 16, 1024);
@@ -482,6 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #ifndef CODEC_NO_SETMAXNREG
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kTcRegsSoftmax));
 #endif
+    CODEC_TC_RANGE;
     const int grp = warp >> 2;   // 0: even tiles, 1: odd tiles
     const int quad = warp & 3;   // TMEM lane quadrant
     const int r = quad * 32 + lane;
@@ -541,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         if (tid == grp * 128) stamp(2, t);
         uint32_t sr[128];
         const uint32_t my_s = tmem + lane_addr + kColS + b * 128;
-        if (dbg_flags & 256) {  // timing experiment: no TMEM S traffic
+        if (dbg & CODEC_FLAG_DBG_NO_TMEM) {  // timing experiment: no TMEM S traffic
 #pragma unroll
           for (int i = 0; i < 128; ++i) sr[i] = __float_as_uint((float)((i * 37 + lane) & 15) * 0.1f);
         } else {
@@ -612,14 +640,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           named_arrive(pub_mine, 64);
         }
         if (tid == grp * 128) stamp(5, t);
-        // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
-        // for at tile t-4; PV(t+2) cannot be)
-        if (quad == 0) PROG(1 + grp, t, 5);
-        if (t >= 2 && (dbg_flags & (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM)) !=
-                          (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM))
-          mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
-        if (quad == 0) PROG(1 + grp, t, 6);
-        if (tid == grp * 128) stamp(12, t);
         // my row sum follows the reference
         if (!have) {
           my_m = mr;
@@ -628,17 +648,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           l *= fast_exp2(my_m - mr);
           my_m = mr;
         }
-        tc::fence_after();
-        // P = 2^(S c - m) as bf16 pairs, 16 TMEM columns per 32 scores
+        // P = 2^(S c - m) as bf16 pairs, 16 TMEM columns per 32 scores, all
+        // computed into registers before waiting for the P buffer: that wait
+        // (PV(t-2) landed) then costs only the TMEM stores on the PV chain
         const float2 nm = make_float2(-mr, -mr);
         // four independent row-sum chains (a single fadd2 chain would be
         // 64 dependent adds long)
         float2 l2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const uint32_t my_p = tmem + lane_addr + kColP + b * 64;
+        uint32_t pall[64];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t pw[16];
-          if (dbg_flags & 512) {  // timing experiment: no exponentials
+          uint32_t* pw = pall + 16 * c;
+          if (dbg & CODEC_FLAG_DBG_NO_EXP) {  // timing experiment: no exponentials
 #pragma unroll
             for (int w = 0; w < 16; ++w) pw[w] = sr[c * 32 + 2 * w] ^ sr[c * 32 + 2 * w + 1];
           } else
@@ -664,8 +686,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
               pw[w + k] = pack_bf16(p[k].x, p[k].y);
             }
           }
-          if (!(dbg_flags & 256)) tc::tmem_st16(my_p + c * 16, pw);
-          else if (pw[0] == 12345u) sr[c] = pw[1];  // keep the math alive
+        }
+        // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
+        // for at tile t-4; PV(t+2) cannot be)
+        if (quad == 0) PROG(1 + grp, t, 5);
+        if (t >= 2 && (dbg & (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM)) !=
+                          (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM))
+          mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+        if (quad == 0) PROG(1 + grp, t, 6);
+        if (tid == grp * 128) stamp(12, t);
+        tc::fence_after();
+        if (!(dbg & CODEC_FLAG_DBG_NO_TMEM)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tc::tmem_st16(my_p + c * 16, pall + 16 * c);
+        } else if (pall[0] == 12345u) {
+          sr[0] = pall[1];  // keep the math alive
         }
         {
           const float2 la = tc::fadd2(l2[0], l2[1]), lb = tc::fadd2(l2[2], l2[3]);
@@ -768,6 +803,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   // phase behind its final one, so the parity waits are exact.
   __syncthreads();
   if (warp == kTcMmaWarp) {
+    CODEC_TC_RANGE;
     int tiles = 0, units = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const int nt = group_view(table, off_groups, off_rows, gi).n_tiles;
@@ -792,6 +828,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   if (warp == kTcMmaWarp) tc::tmem_dealloc_pair(tmem, kTmemCols);
   cta_log(ctalog, blockIdx.x, t_start);
 }
+
+#undef CODEC_TC_RANGE
 
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

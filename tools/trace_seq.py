@@ -1,4 +1,6 @@
-"""Debug: the MMA issuer's event sequence on pair 0 of cfg2 (CODEC_FLAG_TRACE).
+"""Debug: the MMA issuers' event sequence on pair 0 of cfg2 (CODEC_FLAG_TRACE;
+needs a build with CODEC_NVCC_EXTRA=-DCODEC_TC_TRACE, e.g. CODEC_BUILD_TAG=trace,
+selected with CODEC_B200_LIB).
 
     python tools/trace_seq.py [flags] [first_event] [n_events]
 
@@ -32,6 +34,7 @@ buf = (C.c_longlong * n)()
 _lib.check(_lib.lib().codec_debug_trace(buf, n))
 a = np.array(buf, dtype=np.int64)[17 * 2 * 64:].reshape(-1, 2)
 a = a[a[:, 0] > 0]
+a = a[np.argsort(a[:, 0], kind='stable')]  # S and PV issuers log separately
 names = {1: 'S want s_free', 2: 'S q ok', 3: 'S k_full ok', 4: 'S issued', 5: 'PV want p_full',
          6: 'PV p_full ok', 7: 'PV v_full ok', 9: 'PV issued'}
 t0 = a[0, 0]
@@ -57,3 +60,19 @@ for i in gaps:
     print(f'  gap {a[i + 1, 0] - a[i, 0]:6d} before {names.get(int(c), c)} {tt} (at {a[i + 1, 0] - t0})')
 si = a[(a[:, 1] >> 16) == 4, 0]
 print('S issued period: median', int(np.median(np.diff(si))), 'mean', int(np.diff(si).mean()), 'n', len(si))
+
+# per-tile chain on CTA rank 0 (softmax stamps: 14 wait S, 2 saw S, 4 freed S,
+# 5 row max settled, 12 P buffer free, 3 P released), times relative to S issued
+st = np.array(buf, dtype=np.int64)[:17 * 2 * 64].reshape(17, 2, 64)
+ev = {}
+for clk, tag in a:
+    ev[(int(tag >> 16), int(tag & 0xffff))] = clk
+print('tile: S_issued->sawS  ->freedS  ->m_set  ->Pbuf_ok  ->relP  ->PV_sees_P  ->PV_issued | S_issued(t)-S_issued(t-1)')
+for t in range(20, 40):
+    s_iss = ev.get((4, t))
+    if s_iss is None:
+        continue
+    r = lambda e: st[e, 0, t] - s_iss if st[e, 0, t] > 0 else -1
+    pv_p = ev.get((6, t), s_iss) - s_iss
+    pv_i = ev.get((9, t), s_iss) - s_iss
+    print(f'{t:3d}: {r(2):6d} {r(4):8d} {r(5):8d} {r(12):9d} {r(3):7d} {pv_p:10d} {pv_i:11d} | {s_iss - ev.get((4, t - 1), s_iss):6d}')
