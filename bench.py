@@ -272,7 +272,7 @@ def main():
 
     # TC SM budget: the SMs the TC grid leaves free run the suffix kernel
     # from the start (programmatic dependent launch); tuned once per plan
-    budgets = [sms] if (args.serial or args.quick) else [sms, 136, 128, 120, 112, 104, 96, 88]
+    budgets = [sms] if (args.serial or args.quick) else [sms] + list(range(136, 63, -8))
     tune_ms = {}
     best = None
     for b in budgets:

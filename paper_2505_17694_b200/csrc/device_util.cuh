@@ -110,6 +110,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 #endif
 
+// Blocking wait with an explicit suspend-time hint: the thread sleeps in
+// try_wait until the phase completes (or the hint, in ns, elapses) instead
+// of re-issuing the probe.
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t phase, uint32_t hint_ns) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(hint_ns)
+      : "memory");
+}
+
+// Wait for a phase a warp does not need to see promptly (producers running
+// ahead, buffer reuse): between probes the warp sleeps, leaving the issue
+// slots of its SM sub-partition to the warps on the critical path (a plain
+// try_wait loop on a shared SMSP slowed the softmax warps next to it).
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t phase, uint32_t sleep_ns = 256) {
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    __nanosleep(sleep_ns);
+  }
+}
+
 // 1D bulk async copy global -> shared, completion on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -44,6 +44,16 @@
 
 namespace codec {
 
+// critical-path waits of this kernel (issuers, softmax): plain try_wait loop
+// or try_wait with a suspend-time hint (CODEC_TC_WAIT_HINT ns)
+__device__ __forceinline__ void tc_wait(uint64_t* bar, uint32_t phase) {
+#if defined(CODEC_TC_WAIT_HINT) && !defined(CODEC_HANG_CHECK)
+  mbar_wait_hint(bar, phase, CODEC_TC_WAIT_HINT);
+#else
+  mbar_wait(bar, phase);
+#endif
+}
+
 constexpr int kTcSoftmaxWarps = 8;           // 2 groups x 4 lane quadrants
 constexpr int kTcProducerWarp = kTcSoftmaxWarps;       // K loads
 constexpr int kTcMmaWarp = kTcSoftmaxWarps + 1;
@@ -79,6 +89,10 @@ static_assert(kTcSmem <= 232448, "exceeds the 227 KB opt-in shared memory");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColP = 256, kColO = 384;
 constexpr float kRescaleLog2 = 8.f;
+// of every 4 score pairs, how many take the FMA-pipe polynomial instead of MUFU.EX2
+#ifndef CODEC_TC_POLY_PAIRS
+#define CODEC_TC_POLY_PAIRS 0
+#endif
 constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 
 struct TcBars {
@@ -234,6 +248,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       ++seq_n;
     }
   };
+#ifndef CODEC_TC_TRACE_QUAD
+#define CODEC_TC_TRACE_QUAD 0  // lane quadrant (warp & 3) whose softmax warp stamps its tiles
+#endif
 #else
   (void)trace;
   auto stamp = [](int, int) {};
@@ -315,7 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const int y = row0 + j * kTcBN;
         const int ks = t % kTcKStages;
         PROG(3, t, 1);
-        if (t >= kTcKStages) mbar_wait(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
+        if (t >= kTcKStages) mbar_wait_relaxed(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
         PROG(3, t, 2);
         if (dbg & CODEC_FLAG_DBG_NO_LOADS) {
           if (leader && tc::elect_one()) mbar_arrive(&bars->k_full[ks]);
@@ -353,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     int tv = 0;  // V tiles loaded
     auto load_v = [&]() {
       const int vs = tv % kTcVStages;
-      if (tv >= kTcVStages && !iso) mbar_wait(&bars->v_empty[vs], ((tv / kTcVStages) - 1) & 1);
+      if (tv >= kTcVStages && !iso) mbar_wait_relaxed(&bars->v_empty[vs], ((tv / kTcVStages) - 1) & 1);
       if ((dbg & CODEC_FLAG_DBG_NO_LOADS) || iso) {
         if (leader && tc::elect_one() && !iso) mbar_arrive(&bars->v_full[vs]);
       } else if (tc::elect_one()) {
@@ -377,11 +394,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         if (!vc.done()) load_v();  // V(tp + kVAhead)
         const int b = tp & 1, vs = tp % kTcVStages;
         if (lane == 0) seq(5, tp);
-        if (!iso) mbar_wait(&bars->p_full[b], (tp >> 1) & 1);  // P(tp) in both CTAs' TMEM
+        if (!iso) tc_wait(&bars->p_full[b], (tp >> 1) & 1);  // P(tp) in both CTAs' TMEM
         if (lane == 0) seq(6, tp);
-        if (!iso) mbar_wait(&bars->v_full[vs], (tp / kTcVStages) & 1);
+        if (!iso) tc_wait(&bars->v_full[vs], (tp / kTcVStages) & 1);
         if (lane == 0) seq(7, tp);
-        if (pc.j == 0 && pc.n > 0 && !iso) mbar_wait(&bars->o_free, (pc.n - 1) & 1);  // epilogue read O
+        if (pc.j == 0 && pc.n > 0 && !iso) tc_wait(&bars->o_free, (pc.n - 1) & 1);  // epilogue read O
         tc::fence_after();
         const uint64_t bv = dv + (uint64_t)((vs * kHalfBytes) >> 4);
         if (tc::elect_one()) {
@@ -415,8 +432,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       }
       const int qb = n & 1;
       if (n >= 2) {
-        mbar_wait(&bars->q_empty[qb], ((n - 2) >> 1) & 1);
-        mbar_wait(&bars->epi_done[qb], ((n - 2) >> 1) & 1);  // staging of unit n - 2's O
+        mbar_wait_relaxed(&bars->q_empty[qb], ((n - 2) >> 1) & 1);
+        mbar_wait_relaxed(&bars->epi_done[qb], ((n - 2) >> 1) & 1);  // staging of unit n - 2's O
       }
       uint8_t* qs = smem + kOffQ + qb * kQBytes;
       if (gv.qreq0 >= 0) {
@@ -428,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           tc::tma_load_4d(qs, &tmq, 0, 0, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[qb]);
           tc::tma_load_4d(qs + kQAtom, &tmq, 0, 1, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[qb]);
         }
-        mbar_wait(&bars->q_tma[qb], (qtma_uses[qb]++) & 1);
+        tc_wait(&bars->q_tma[qb], (qtma_uses[qb]++) & 1);
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(&bars->q_full[qb], 0);
         ++n;
@@ -478,10 +495,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       for (int ts = 0; !sc.done(); ++ts) {
         const int s = ts % kTcKStages, b = ts & 1;
         if (lane == 0) seq(1, ts);
-        if (ts >= 2 && !iso) mbar_wait(&bars->s_free[b], ((ts - 2) >> 1) & 1);  // S(ts-2) pulled out by both CTAs
-        if (sc.j == 0 && !iso) mbar_wait(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1);
+        if (ts >= 2 && !iso) tc_wait(&bars->s_free[b], ((ts - 2) >> 1) & 1);  // S(ts-2) pulled out by both CTAs
+        if (sc.j == 0 && !iso) tc_wait(&bars->q_full[sc.n & 1], (sc.n >> 1) & 1);
         if (lane == 0) seq(2, ts);
-        if (!iso) mbar_wait(&bars->k_full[s], (ts / kTcKStages) & 1);
+        if (!iso) tc_wait(&bars->k_full[s], (ts / kTcKStages) & 1);
         if (lane == 0) seq(3, ts);
         tc::fence_after();
         const uint64_t aq = dq + (uint64_t)(((sc.n & 1) * kQBytes) >> 4);
@@ -562,11 +579,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         if ((t & 1) != grp) continue;
         const int b = t & 1;
         if (quad == 0) PROG(1 + grp, t, 1);
-        if (tid == grp * 128) stamp(14, t);
-        mbar_wait(&bars->s_full[b], (t >> 1) & 1);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(14, t);
+        tc_wait(&bars->s_full[b], (t >> 1) & 1);
         if (quad == 0) PROG(1 + grp, t, 2);
         tc::fence_after();
-        if (tid == grp * 128) stamp(2, t);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(2, t);
         uint32_t sr[128];
         const uint32_t my_s = tmem + lane_addr + kColS + b * 128;
         if (dbg & CODEC_FLAG_DBG_NO_TMEM) {  // timing experiment: no TMEM S traffic
@@ -582,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(&bars->s_free[b], 0);  // S buffer b may be overwritten
-        if (tid == grp * 128) stamp(4, t);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(4, t);
         const int lim = vis - j * kTcBN;  // visible columns of this tile
         if (!__all_sync(0xffffffffu, !valid || lim >= kTcBN)) {
 #pragma unroll
@@ -618,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             // completes for PV(x), PV(x+4), ...: PV(t-5) is done (this group
             // waited for PV(t-4) at tile t-2) and PV(t+3) cannot be, so the
             // parity wait is exact.
-            mbar_wait(&bars->pv_done[(t - 1) & 3], ((t - 1) >> 2) & 1);
+            tc_wait(&bars->pv_done[(t - 1) & 3], ((t - 1) >> 2) & 1);
             tc::fence_after();
             const float alpha = need ? fast_exp2(m_prev - mt) : 1.f;
             const uint32_t my_o = tmem + lane_addr + kColO;
@@ -639,7 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           mpub[grp * 128 + r] = mr;
           named_arrive(pub_mine, 64);
         }
-        if (tid == grp * 128) stamp(5, t);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(5, t);
         // my row sum follows the reference
         if (!have) {
           my_m = mr;
@@ -651,6 +668,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         // P = 2^(S c - m) as bf16 pairs, 16 TMEM columns per 32 scores, all
         // computed into registers before waiting for the P buffer: that wait
         // (PV(t-2) landed) then costs only the TMEM stores on the PV chain
+#ifdef CODEC_TC_PWAIT_EARLY
+        if (t >= 2) tc_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+#endif
         const float2 nm = make_float2(-mr, -mr);
         // four independent row-sum chains (a single fadd2 chain would be
         // 64 dependent adds long)
@@ -677,9 +697,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
             p[0] = make_float2(fast_exp2(x[0].x), fast_exp2(x[0].y));
             p[1] = make_float2(fast_exp2(x[1].x), fast_exp2(x[1].y));
-            // (measured: 6/8 on MUFU = 7/8 = 8/8 within noise, 4/8 is 4% slower)
+            // (measured after the issuer split: 8/8 on MUFU 114 us, 6/8 117, 4/8 125)
+#if CODEC_TC_POLY_PAIRS >= 2
+            p[2] = poly_exp2x2(x[2]);
+#else
             p[2] = make_float2(fast_exp2(x[2].x), fast_exp2(x[2].y));
+#endif
+#if CODEC_TC_POLY_PAIRS >= 1
             p[3] = poly_exp2x2(x[3]);
+#else
+            p[3] = make_float2(fast_exp2(x[3].x), fast_exp2(x[3].y));
+#endif
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               l2[k] = tc::fadd2(l2[k], p[k]);
@@ -690,11 +718,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
         // for at tile t-4; PV(t+2) cannot be)
         if (quad == 0) PROG(1 + grp, t, 5);
+#ifndef CODEC_TC_PWAIT_EARLY
         if (t >= 2 && (dbg & (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM)) !=
                           (CODEC_FLAG_DBG_NO_PWAIT | CODEC_FLAG_DBG_NO_TMEM))
-          mbar_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+          tc_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+#endif
         if (quad == 0) PROG(1 + grp, t, 6);
-        if (tid == grp * 128) stamp(12, t);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(12, t);
         tc::fence_after();
         if (!(dbg & CODEC_FLAG_DBG_NO_TMEM)) {
 #pragma unroll
@@ -709,8 +739,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         tc::wait_st();
         tc::fence_before();
         __syncwarp();
-        if (tid == grp * 128) stamp(3, t);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(3, t);
         if (lane == 0 && quad == 3) stamp(7, t);
+        if (lane == 0 && quad == 1) stamp(10, t);
+        if (lane == 0 && quad == 2) stamp(11, t);
         if (lane == 0) tc::mbar_arrive_cluster(&bars->p_full[b], 0);
       }
       // ---- epilogue: the group that ran the unit's last tile reads all of
@@ -727,11 +759,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         named_arrive(l_bar, 256);
       } else {
         named_sync(l_bar, 256);
-        if (tid == grp * 128) stamp(16, tl);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(16, tl);
         const float2 o2 = lx[r];
         const float l_run = l + (o2.x > 0.f ? o2.x * fast_exp2(o2.y - my_m) : 0.f);
         // PV(tl) landed => the whole unit landed (PV(tl - 4) is done)
-        mbar_wait(&bars->pv_done[tl & 3], (tl >> 2) & 1);
+        tc_wait(&bars->pv_done[tl & 3], (tl >> 2) & 1);
         tc::fence_after();
         uint32_t o[128];
 #pragma unroll
@@ -740,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(&bars->o_free, 0);
-        if (tid == grp * 128) stamp(15, tl);
+        if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(15, tl);
         // Write O through this unit's Q buffer (its S MMAs are complete) as a
         // staging area, 64 rows per pass: thread-per-row global stores touch
         // 32 lines per instruction; from SMEM each row goes out as one fully
@@ -784,7 +816,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->epi_done[n & 1]);
-          if (tid == grp * 128) stamp(9, tl);
+          if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(9, tl);
         }
       }
       if (quad == 0) PROG(1 + grp, t, 8);

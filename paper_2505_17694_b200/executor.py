@@ -204,7 +204,7 @@ def autotune_step(step: DecodeStep, q, k_pool, v_pool, budgets=None, iters=10):
         return step, {}
     sms = step.dims.sm_count
     h_local = step.head_end - step.head_begin
-    budgets = budgets or sorted({sms, int(sms * 0.9), int(sms * 0.8), int(sms * 0.7), int(sms * 0.6)}, reverse=True)
+    budgets = budgets or sorted({sms} | {int(sms * f) // 2 * 2 for f in (0.9, 0.8, 0.7, 0.6, 0.5, 0.45)}, reverse=True)
     out = torch.empty((step.forest.bs, step.hq_local, step.d), dtype=step.out_dtype, device=step.device)
     times = {}
     best, best_ms = step, None

@@ -67,7 +67,7 @@ st = np.array(buf, dtype=np.int64)[:17 * 2 * 64].reshape(17, 2, 64)
 ev = {}
 for clk, tag in a:
     ev[(int(tag >> 16), int(tag & 0xffff))] = clk
-print('tile: S_issued->sawS  ->freedS  ->m_set  ->Pbuf_ok  ->relP  ->PV_sees_P  ->PV_issued | S_issued(t)-S_issued(t-1)')
+print('tile: S_issued->sawS  ->freedS  ->m_set  ->Pbuf_ok  ->relP  ->PV_sees_P  ->PV_issued | S_issued(t)-S_issued(t-1) | relP w0r1 w3r0 w3r1 w1r0 w1r1 w2r0 w2r1')
 for t in range(20, 40):
     s_iss = ev.get((4, t))
     if s_iss is None:
@@ -75,4 +75,6 @@ for t in range(20, 40):
     r = lambda e: st[e, 0, t] - s_iss if st[e, 0, t] > 0 else -1
     pv_p = ev.get((6, t), s_iss) - s_iss
     pv_i = ev.get((9, t), s_iss) - s_iss
-    print(f'{t:3d}: {r(2):6d} {r(4):8d} {r(5):8d} {r(12):9d} {r(3):7d} {pv_p:10d} {pv_i:11d} | {s_iss - ev.get((4, t - 1), s_iss):6d}')
+    rr = lambda e, k: st[e, k, t] - s_iss if st[e, k, t] > 0 else -1
+    print(f'{t:3d}: {r(2):6d} {r(4):8d} {r(5):8d} {r(12):9d} {r(3):7d} {pv_p:10d} {pv_i:11d} | {s_iss - ev.get((4, t - 1), s_iss):6d} |'
+          f' {rr(3, 1):6d} {rr(7, 0):6d} {rr(7, 1):6d} {rr(10, 0):6d} {rr(10, 1):6d} {rr(11, 0):6d} {rr(11, 1):6d}')
