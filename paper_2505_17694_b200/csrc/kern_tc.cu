@@ -230,6 +230,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   const bool leader = rank == 0;
   const int blk = blockIdx.x >> 1;
   // optional timeline of pair (0, 0): trace[(event * 2 + rank) * 64 + tile]
+#ifndef CODEC_TC_TRACE_QUAD
+#define CODEC_TC_TRACE_QUAD 0  // lane quadrant (warp & 3) whose softmax warp stamps its tiles
+#endif
 #ifdef CODEC_TC_TRACE
   // debug builds only (CODEC_NVCC_EXTRA=-DCODEC_TC_TRACE): the stamps cost
   // the single-warp MMA issuer ~70 instructions per tile even when off
@@ -248,9 +251,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       ++seq_n;
     }
   };
-#ifndef CODEC_TC_TRACE_QUAD
-#define CODEC_TC_TRACE_QUAD 0  // lane quadrant (warp & 3) whose softmax warp stamps its tiles
-#endif
 #else
   (void)trace;
   auto stamp = [](int, int) {};
@@ -652,10 +652,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             if (need) mr = mt;
           }
         }
+#ifndef CODEC_TC_LATE_PUBLISH
         if (t + 1 < t_total) {
           mpub[grp * 128 + r] = mr;
           named_arrive(pub_mine, 64);
         }
+#endif
         if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(5, t);
         // my row sum follows the reference
         if (!have) {
@@ -715,6 +717,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
           }
         }
+#ifdef CODEC_TC_LATE_PUBLISH
+        // (experiment) hand the row's exponent reference to the other group
+        // only after this tile's exponentials, so the two groups' MUFU phases
+        // alternate: the S period becomes uniform (~1570 clk) but the step
+        // is slower (123 vs 115 us on cfg2) -- the groups lose their overlap
+        if (t + 1 < t_total) {
+          mpub[grp * 128 + r] = mr;
+          named_arrive(pub_mine, 64);
+        }
+#endif
         // P buffer b is free once PV(t-2) landed (PV(t-6) is done: waited
         // for at tile t-4; PV(t+2) cannot be)
         if (quad == 0) PROG(1 + grp, t, 5);
