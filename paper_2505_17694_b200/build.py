@@ -58,6 +58,11 @@ def _compile(src: Path, force: bool, verbose: bool):
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
     srcs = _sources()
+    # a failed compile must not leave the previous library in place (tests
+    # and benches would silently run stale kernels)
+    newest_dep = max([s.stat().st_mtime for s in srcs] + [h.stat().st_mtime for h in _headers()])
+    if force or not OUT.exists() or OUT.stat().st_mtime < newest_dep:
+        OUT.unlink(missing_ok=True)
     with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
         results = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
     objs = [o for o, _ in results]
