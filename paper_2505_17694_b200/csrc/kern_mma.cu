@@ -20,8 +20,10 @@
 // Memory path: one producer lane streams the slice with 3D TMA boxes of
 // 32 whole token rows (8 KB, SWIZZLE_128B; one op each for K and V: the
 // TMA unit's per-op cost, not bytes, limits small boxes) of the head-major
-// pool into a 4-stage ring; the swizzle makes the ldmatrix reads
-// conflict-free. Two consumer warps take 16 tokens of each stage.
+// pool into a 2-stage ring (6 CTAs per SM hold ~200 KB in flight: measured
+// better than 4 stages x 3 CTAs, 3 x 4, 6 x 2, or 64-token stages); the
+// swizzle makes the ldmatrix reads conflict-free. Two consumer warps take 16
+// tokens of each stage.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -33,13 +35,21 @@
 
 namespace codec {
 
+#ifndef CODEC_MMA_SUB
+#define CODEC_MMA_SUB 1
+#endif
+#ifndef CODEC_MMA_STAGES
+#define CODEC_MMA_STAGES 2  // 2 x 16 KB per CTA, 6 CTAs per SM: more CTAs beat deeper rings (cfg2 step 187 -> 178 us)
+#endif
 constexpr int kMmaWarps = 2;                       // consumer warps
 constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
-constexpr int kMmaStages = 4;
-constexpr int kMmaCT = 16 * kMmaWarps;             // tokens per stage
+constexpr int kMmaStages = CODEC_MMA_STAGES;
+constexpr int kMmaSub = CODEC_MMA_SUB;             // 16-token steps per consumer warp per stage
+constexpr int kMmaCT = 16 * kMmaWarps * kMmaSub;   // tokens per stage
 constexpr int kMmaD = 128;
 constexpr int kFzMax = 8;                          // partials besides its own a fused merge folds in
-constexpr int kMmaBox = kMmaCT * 256;              // one box: kMmaCT whole token rows (8 KB)
+constexpr int kMmaBox = kMmaCT * 256;              // one box: kMmaCT whole token rows
+static_assert(kMmaCT <= 256, "TMA box rows");
 constexpr int kMmaStageBytes = 2 * kMmaBox;        // K box + V box
 constexpr int kMmaSmem = kMmaStages * kMmaStageBytes + 1024 /* align */ + 2 * kMmaStages * 8;
 
@@ -116,12 +126,15 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
     float m_run[2] = {neg_inf<float>(), neg_inf<float>()};  // heads 2 tig, 2 tig + 1 (log2 units)
     float l_run[2] = {0.f, 0.f};                            // this lane's tokens only
     const int mat = lane >> 3, rr = lane & 7;
-    const int tk_qk = 16 * warp + rr + ((mat & 1) << 3), ck_qk = mat >> 1;  // ldmatrix rows for S^T
-    const int tk_pv = 16 * warp + rr + ((mat >> 1) << 3), ck_pv = mat & 1;  // ldmatrix.trans rows for V^T
     for (int c = 0; c < nch; ++c) {
       const int s = c % kMmaStages;
       mbar_wait(&full[s], (c / kMmaStages) & 1);
       const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + kMmaBox;
+#pragma unroll 1
+      for (int u = 0; u < kMmaSub; ++u) {
+      const int wrow = 16 * (warp * kMmaSub + u);  // this step's first token row in the stage
+      const int tk_qk = wrow + rr + ((mat & 1) << 3), ck_qk = mat >> 1;  // ldmatrix rows for S^T
+      const int tk_pv = wrow + rr + ((mat >> 1) << 3), ck_pv = mat & 1;  // ldmatrix.trans rows for V^T
       // S^T (16 tokens x 8 heads) = K Q^T
       float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         hmma(sc, a, qf[ks][0], qf[ks][1]);
       }
       // sc[0]: (token gid, head 2tig), [1]: (gid, 2tig+1), [2]: (gid+8, 2tig), [3]: (gid+8, 2tig+1)
-      const int t0 = c * kMmaCT + 16 * warp + gid;
+      const int t0 = c * kMmaCT + wrow + gid;
       const bool va = t0 < n_tok, vb8 = t0 + 8 < n_tok;
       sc[0] = va ? sc[0] * cscale : neg_inf<float>();
       sc[1] = va ? sc[1] * cscale : neg_inf<float>();
@@ -176,6 +189,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         uint32_t a[4];
         ldsm_x4_t(vb + mma_sw(tk_pv, 2 * dm + ck_pv), a);
         hmma(acc[dm], a, b0, b1);
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
