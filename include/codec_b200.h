@@ -170,7 +170,26 @@ typedef struct {
   int32_t sm_count;               /* SMs of the device (0 = 148); sizes the persistent TC grid */
   int32_t tc_sm_budget;           /* SMs the TC kernel may occupy (0 = all); the rest stay free
                                      for the GEMV kernel running concurrently on an aux stream */
+  /* Paged KV (ABI v3). page_size 0: k / v are the contiguous node pool
+   * (nodes at their preorder offsets). page_size P > 0 (a power of two
+   * >= 128; bf16, d = 128, tensor-core + mma.sync suffix kernels only):
+   * every node's tokens are split into pages of P tokens, node n owning
+   * logical pages [base[n], base[n+1]) (codec_page_layout); k / v are
+   * [h_local][pool_tokens][d] physical pools and page_table[logical page]
+   * is the physical page (token rows [page * P, page * P + P) of every
+   * head). Plan slices must start at multiples of 128 tokens (shared,
+   * tensor-core nodes) / 32 tokens (suffix nodes) within their node. */
+  int32_t page_size;
+  int32_t reserved0;
+  const int32_t* page_table;      /* device int32[n_logical_pages]; NULL when page_size == 0 */
 } codec_dims;
+
+/* Logical page layout of a paged pool: node n (node-id order) owns pages
+ * [node_page_base[n], node_page_base[n + 1]), ceil(len_n / page_size) of
+ * them; *n_pages = node_page_base[n_nodes]. node_page_base has n_nodes + 1
+ * entries. */
+CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, int64_t* node_page_base,
+                                    int64_t* n_pages);
 
 #define CODEC_FLAG_NO_TC      1   /* never use the tcgen05 shared-node kernel */
 #define CODEC_FLAG_FORCE_TC   2   /* tcgen05 kernel for every eligible group */

@@ -63,7 +63,8 @@ class PlanInfo(C.Structure):
 class Dims(C.Structure):
     _fields_ = [("bs", I32), ("h_q", I32), ("h_kv", I32), ("d", I32), ("head_begin", I32),
                 ("head_end", I32), ("kv_dtype", I32), ("flags", I32), ("pool_tokens", I64),
-                ("sm_count", I32), ("tc_sm_budget", I32)]
+                ("sm_count", I32), ("tc_sm_budget", I32), ("page_size", I32), ("reserved0", I32),
+                ("page_table", C.c_void_p)]
 
 
 class TableInfo(C.Structure):
@@ -97,6 +98,7 @@ _SIGS = {
     "codec_table_free": (None, [P]),
     "codec_table_info_get": (I32, [P, C.POINTER(TableInfo)]),
     "codec_table_copy": (I32, [P, PI32]),
+    "codec_page_layout": (I32, [P, I32, PI64, PI64]),
     "codec_decode_attention": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P]),
     "codec_decode_attention_ex": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P, P]),
     "codec_debug_trace": (I32, [P, I64]),

@@ -74,7 +74,6 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   *out = nullptr;
   const int32_t n_nodes = ix_n_nodes(ix), bs = ix_bs(ix);
   const auto& len = ix_length(ix);
-  const auto& off = ix_node_off(ix);
   const auto& qptr = ix_qset_ptr(ix);
   const auto& qidx = ix_qset_idx(ix);
   const auto& qvis = ix_qset_vis(ix);
@@ -85,9 +84,31 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     return fail(CODEC_ERR_DIMENSION_MISMATCH, "h_q=%d must be a positive multiple of h_kv=%d", dims->h_q, dims->h_kv);
   if (dims->head_begin < 0 || dims->head_end > dims->h_kv || dims->head_begin >= dims->head_end)
     return fail(CODEC_ERR_VALUE, "kv head shard [%d, %d) outside 0..%d", dims->head_begin, dims->head_end, dims->h_kv);
-  if (dims->pool_tokens < ix_total_tokens(ix))
+  // paged pool: node n's token x is logical token base[n] * P + x, which
+  // the kernels map through page_table to a physical pool row
+  const int32_t page = dims->page_size;
+  std::vector<int64_t> off_paged;
+  if (page) {
+    if (page < 128 || !is_pow2(page))
+      return fail(CODEC_ERR_VALUE, "page_size %d must be a power of two >= 128", page);
+    if (!dims->page_table) return fail(CODEC_ERR_VALUE, "page_size %d without a page table", page);
+    if (dims->kv_dtype != CODEC_BF16 || dims->d != 128 || dims->h_q > 8 * dims->h_kv ||
+        (dims->flags & (CODEC_FLAG_NO_TC | CODEC_FLAG_NO_GEMV | CODEC_FLAG_GEMV_SIMT)))
+      return fail(CODEC_ERR_UNSUPPORTED,
+                  "paged KV runs on the tensor-core and mma.sync suffix kernels only: bf16, d = 128, <= 8 "
+                  "query heads per kv head");
+    if (dims->pool_tokens < page) return fail(CODEC_ERR_VALUE, "paged pool of %lld tokens holds no page",
+                                              (long long)dims->pool_tokens);
+    off_paged.resize(n_nodes + 1, 0);
+    for (int32_t n = 0; n < n_nodes; ++n) off_paged[n + 1] = off_paged[n] + (len[n] + page - 1) / page;
+    if (off_paged[n_nodes] * page >= (int64_t(1) << 31))
+      return fail(CODEC_ERR_UNSUPPORTED, "paged pool larger than 2^31 logical tokens");
+    for (auto& x : off_paged) x *= page;
+  } else if (dims->pool_tokens < ix_total_tokens(ix)) {
     return fail(CODEC_ERR_VALUE, "pool holds %lld tokens, forest needs %lld", (long long)dims->pool_tokens,
                 (long long)ix_total_tokens(ix));
+  }
+  const auto& off = page ? off_paged : ix_node_off(ix);
   if (dims->pool_tokens >= (int64_t(1) << 31)) return fail(CODEC_ERR_UNSUPPORTED, "pool larger than 2^31 tokens");
   const int32_t g = dims->h_q / dims->h_kv;
   const int32_t d = dims->d;
@@ -197,6 +218,11 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       kind = kKindGeneric;
       per = 1;
     }
+    // paged pool: every TMA box (128-token K/V tiles, 32-token suffix
+    // chunks) must sit inside one page
+    if (page && start % (kind == kKindTc ? 128 : 32) != 0)
+      return fail(CODEC_ERR_UNSUPPORTED, "paged KV: node %lld slice starts at token %lld, not a multiple of %d",
+                  (long long)n, (long long)start, kind == kKindTc ? 128 : 32);
     for (size_t a = 0; a < live.size(); a += per) {
       size_t b = std::min(live.size(), a + per);
       int32_t max_vis = 0;
@@ -490,5 +516,18 @@ extern "C" int32_t codec_table_info_get(const codec_table* t, codec_table_info* 
 extern "C" int32_t codec_table_copy(const codec_table* t, int32_t* blob) {
   if (!t || !blob) return codec::fail(CODEC_ERR_VALUE, "NULL argument");
   std::copy(t->blob.begin(), t->blob.end(), blob);
+  return CODEC_OK;
+}
+
+extern "C" int32_t codec_page_layout(const codec_index* ix, int32_t page_size, int64_t* node_page_base,
+                                     int64_t* n_pages) {
+  using namespace codec;
+  if (!ix || !node_page_base || !n_pages) return fail(CODEC_ERR_VALUE, "NULL argument");
+  if (page_size < 1) return fail(CODEC_ERR_VALUE, "page_size %d must be positive", page_size);
+  const auto& len = ix_length(ix);
+  const int32_t n_nodes = ix_n_nodes(ix);
+  node_page_base[0] = 0;
+  for (int32_t n = 0; n < n_nodes; ++n) node_page_base[n + 1] = node_page_base[n] + (len[n] + page_size - 1) / page_size;
+  *n_pages = node_page_base[n_nodes];
   return CODEC_OK;
 }

@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
                    const int32_t* __restrict__ table, int off_groups, int off_rows,
                    const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                    float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                   int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog) {
+                   int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog,
+                   const int32_t* __restrict__ page_table, int page_shift) {
   const long long t_start = ctalog ? global_ns() : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
   const int req = row[0], n_tok = row[1], slot = row[2];
   const int fz = row[3];  // >= 0: merge entry of (req, kv head 0): fold the TC partials in here
   const int nch = (n_tok + kMmaCT - 1) / kMmaCT;
-  const int row0 = kh * (int)pool_tokens + grp[kGrpKvTok];
+  const int kv_tok = grp[kGrpKvTok];
 
   if (tid == 0) {
     for (int s = 0; s < kMmaStages; ++s) {
@@ -99,7 +100,9 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         const int s = c % kMmaStages;
         if (c >= kMmaStages) mbar_wait(&empty[s], ((c / kMmaStages) - 1) & 1);
         uint8_t* st = smem + s * kMmaStageBytes;
-        const int y = row0 + c * kMmaCT;
+        int x = kv_tok + c * kMmaCT;  // logical token; paged pool: a 32-token box never crosses a page
+        if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
+        const int y = kh * (int)pool_tokens + x;
         mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
         tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
         tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
@@ -299,7 +302,7 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog, bool after_tc) {
+                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift) {
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
@@ -326,7 +329,7 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   cfg.numAttrs = after_tc ? 1 : 0;
   e = cudaLaunchKernelEx(&cfg, mma_pac_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
                          pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
-                         off_merge_slot, ctalog);
+                         off_merge_slot, ctalog, page_table, page_shift);
   if (e != cudaSuccess) return cuda_status(e, "mma gemv launch");
   return cuda_status(cudaGetLastError(), "mma gemv launch");
 }

@@ -209,7 +209,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                   const __grid_constant__ CUtensorMap tmq, const int32_t* __restrict__ table, int off_groups, int off_rows, int off_block_ptr,
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                  long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog) {
+                  long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog,
+                  const int32_t* __restrict__ page_table, int page_shift) {
   const long long t_start = ctalog ? global_ns() : 0;
 #ifdef CODEC_TC_DEBUG
   // timing-only ablations (tools/tc_ablate.py); compiled out of the product
@@ -227,6 +228,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = tc::cluster_rank();
+  // pool row of logical token x of kv head kh (paged pool: through the
+  // page table; a 64- or 128-token box never crosses a page)
+  auto prow = [&](int kh, int x) -> int {
+    if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
+    return kh * (int)pool_tokens + x;
+  };
   const bool leader = rank == 0;
   const int blk = blockIdx.x >> 1;
   // optional timeline of pair (0, 0): trace[(event * 2 + rank) * 64 + tile]
@@ -319,17 +326,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     int t = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
-      const int row0 = gv.kh * (int)pool_tokens + gv.kv_tok;
       if (tc::elect_one()) {
         for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
-          tc::tma_prefetch_2d(&tmk, 0, row0 + j * kTcBN + 64 * rank);
-          tc::tma_prefetch_2d(&tmk, 64, row0 + j * kTcBN + 64 * rank);
-          tc::tma_prefetch_2d(&tmv, 64 * rank, row0 + j * kTcBN);
+          const int yk = prow(gv.kh, gv.kv_tok + j * kTcBN + 64 * rank), yv = prow(gv.kh, gv.kv_tok + j * kTcBN);
+          tc::tma_prefetch_2d(&tmk, 0, yk);
+          tc::tma_prefetch_2d(&tmk, 64, yk);
+          tc::tma_prefetch_2d(&tmv, 64 * rank, yv);
         }
       }
       __syncwarp();
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
-        const int y = row0 + j * kTcBN;
         const int ks = t % kTcKStages;
         PROG(3, t, 1);
         if (t >= kTcKStages) mbar_wait_relaxed(&bars->k_empty[ks], ((t / kTcKStages) - 1) & 1);
@@ -339,13 +345,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         } else if (tc::elect_one()) {
           if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
           uint8_t* kd = smem + kOffK + ks * kHalfBytes;
-          tc::tma_load_2d_pair(kd, &tmk, 0, y + 64 * rank, &bars->k_full[ks]);
-          tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, y + 64 * rank, &bars->k_full[ks]);
+          const int yk = prow(gv.kh, gv.kv_tok + j * kTcBN + 64 * rank);
+          tc::tma_load_2d_pair(kd, &tmk, 0, yk, &bars->k_full[ks]);
+          tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, yk, &bars->k_full[ks]);
           if (j + kTcPrefetch < gv.n_tiles) {
-            const int yp = y + kTcPrefetch * kTcBN;
-            tc::tma_prefetch_2d(&tmk, 0, yp + 64 * rank);
-            tc::tma_prefetch_2d(&tmk, 64, yp + 64 * rank);
-            tc::tma_prefetch_2d(&tmv, 64 * rank, yp);
+            const int xp = gv.kv_tok + (j + kTcPrefetch) * kTcBN;
+            const int ypk = prow(gv.kh, xp + 64 * rank), ypv = prow(gv.kh, xp);
+            tc::tma_prefetch_2d(&tmk, 0, ypk);
+            tc::tma_prefetch_2d(&tmk, 64, ypk);
+            tc::tma_prefetch_2d(&tmv, 64 * rank, ypv);
           }
         }
         __syncwarp();
@@ -375,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         if (leader && tc::elect_one() && !iso) mbar_arrive(&bars->v_full[vs]);
       } else if (tc::elect_one()) {
         if (leader) mbar_arrive_expect_tx(&bars->v_full[vs], 2 * kHalfBytes);
-        const int y = vc.gv.kh * (int)pool_tokens + vc.gv.kv_tok + vc.j * kTcBN;
+        const int y = prow(vc.gv.kh, vc.gv.kv_tok + vc.j * kTcBN);
         tc::tma_load_2d_pair(smem + kOffV + vs * kHalfBytes, &tmv, 64 * rank, y, &bars->v_full[vs]);
       }
       __syncwarp();
@@ -980,7 +988,7 @@ static int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_loca
 
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags, long long* ctalog) {
+                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift) {
   const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
     if (cudaMalloc(&g_trace, kTraceLen * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
@@ -997,7 +1005,7 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
   tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, mq, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
-                                                   trace ? g_trace : nullptr, flags, ctalog);
+                                                   trace ? g_trace : nullptr, flags, ctalog, page_table, page_shift);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

@@ -14,7 +14,7 @@
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags, long long* ctalog);
+                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
@@ -23,7 +23,7 @@ int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_grou
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog, bool after_tc);
+                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -111,6 +111,12 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
     return fail(CODEC_ERR_VALUE, "q, k and v must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const int g = dims->h_q / dims->h_kv;
+  int page_shift = 0;
+  if (dims->page_size) {
+    if (dims->page_size < 128 || (dims->page_size & (dims->page_size - 1)) || !dims->page_table)
+      return fail(CODEC_ERR_VALUE, "page_size %d must be a power of two >= 128 with a page table", dims->page_size);
+    while ((1 << page_shift) < dims->page_size) ++page_shift;
+  }
   const int h_local = info->h_local, hq_local = h_local * g, d = dims->d;
   const int64_t elem = dims->kv_dtype == CODEC_F64 ? 8 : 4;
   int64_t o_bytes = (int64_t)info->n_slots * hq_local * d * elem;
@@ -146,18 +152,21 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   if (kev) CODEC_TRY(kev_record(0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
-                        dims->flags, ctalog));
+                        dims->flags, ctalog, dims->page_table, page_shift));
   if (kev) CODEC_TRY(kev_record(1, st));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
                               info->off_merge_slot, st, ctalog,
-                              do_tc && info->n_merge_fused == 0 && !kev));
+                              do_tc && info->n_merge_fused == 0 && !kev, dims->page_table, page_shift));
+  else if (do_gemv && page_shift)
+    return fail(CODEC_ERR_UNSUPPORTED, "paged KV: suffix groups need the mma.sync kernel (bf16, d = 128, g <= 8)");
   else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
                           ctalog));
   if (kev) CODEC_TRY(kev_record(2, st));
+  if (do_gen && page_shift) return fail(CODEC_ERR_UNSUPPORTED, "paged KV: no generic-kernel groups");
   if (do_gen)
     CODEC_TRY(launch_generic_groups(dims->kv_dtype, table_dev, info->n_gen_groups, info->off_gen, info->off_rows, q,
                                     k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, side));

@@ -64,10 +64,16 @@ class DecodeStep:
     """A plan expanded into a device task table for one forest, dtype and
     kv-head shard. Call with device queries [bs, h_q_local, d] and the
     head-major pools; returns [bs, h_q_local, d] (float32, or float64 for
-    float64 inputs)."""
+    float64 inputs).
+
+    Paged pools (paging.py): page_size > 0 with page_table (device int32,
+    one physical page per logical page) and pool_tokens = the physical
+    pools' token stride; the pools passed to each call are then the
+    physical ones."""
 
     def __init__(self, forest: Forest, plan, h_q: int, dtype="bfloat16", head_begin=0, head_end=None,
-                 device="cuda", flags=0, tc_sm_budget=0, concurrent=True):
+                 device="cuda", flags=0, tc_sm_budget=0, concurrent=True, page_size=0, page_table=None,
+                 pool_tokens=None):
         import torch
 
         self.forest = forest
@@ -79,9 +85,14 @@ class DecodeStep:
         self.device = torch.device(device)
         sm = torch.cuda.get_device_properties(self.device).multi_processor_count if torch.cuda.is_available() else 148
         self.plan, self.flags, self.tc_sm_budget = plan, int(flags), int(tc_sm_budget)
+        self.page_size, self.page_table = int(page_size), page_table
+        if self.page_size and page_table is None:
+            raise ValueError("page_size without a page_table")
+        self.pool_tokens = int(pool_tokens) if pool_tokens is not None else max(forest.total_tokens, 1)
         self.dims = _lib.Dims(forest.bs, self.h_q, self.h_kv, self.d, self.head_begin, self.head_end,
-                              dtype_code(self.tdtype), int(flags), max(forest.total_tokens, 1), int(sm),
-                              int(tc_sm_budget))
+                              dtype_code(self.tdtype), int(flags), self.pool_tokens, int(sm),
+                              int(tc_sm_budget), self.page_size, 0,
+                              C.c_void_p(page_table.data_ptr()) if self.page_size else None)
         # GEMV/generic kernels run on an aux stream, concurrently with the
         # tensor-core kernel (event fork/join inside the library)
         self.aux = torch.cuda.Stream(self.device) if concurrent and torch.cuda.is_available() else None
@@ -190,7 +201,8 @@ class DecodeStep:
 
     def with_budget(self, tc_sm_budget: int) -> "DecodeStep":
         return DecodeStep(self.forest, self.plan, self.h_q, self.tdtype, self.head_begin, self.head_end,
-                          self.device, self.flags, tc_sm_budget, self.aux is not None)
+                          self.device, self.flags, tc_sm_budget, self.aux is not None, self.page_size,
+                          self.page_table, self.pool_tokens)
 
 
 def autotune_step(step: DecodeStep, q, k_pool, v_pool, budgets=None, iters=10):

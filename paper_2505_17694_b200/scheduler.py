@@ -161,7 +161,7 @@ def concat_plans(plans) -> DivisionPlan:
 
 
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
-                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT) -> DivisionPlan:
+                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT, page_size: int = 0) -> DivisionPlan:
     """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
     head rows per chunk) stay whole here: on the tensor cores every KV tile
     costs the same (an M=256 MMA pair whatever the rows), so the device
@@ -171,7 +171,9 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     (their suffix CTAs are hardware-scheduled and stream at HBM speed
     regardless of order). Returns one plan over both, in the reference's
     DivisionPlan form (any reference plan is accepted by execute() as well;
-    its slices then bound the device pieces)."""
+    its slices then bound the device pieces). With a paged pool
+    (page_size > 0, paging.py) suffix nodes stay whole: a slice must start
+    on a 32-token chunk boundary of its node."""
     tasks = device_tasks(forest, group_size)
     tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
     gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
@@ -184,7 +186,7 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     # slices of <= SUFFIX_SLICE tokens that run on separate CTAs
     by_bk = {}
     for t in gv:
-        by_bk.setdefault(max(1, -(-t.n // SUFFIX_SLICE)), []).append(t)
+        by_bk.setdefault(1 if page_size else max(1, -(-t.n // SUFFIX_SLICE)), []).append(t)
     for bk in sorted(by_bk):
         plans.append(plan_uniform_bk(by_bk[bk], table, len(by_bk[bk]) * bk, bk))
     return concat_plans(plans)

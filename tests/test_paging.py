@@ -1,0 +1,121 @@
+"""Paged KV pools (paging.py, codec_dims.page_size / page_table): the page
+layout and the table builder's checks on CPU; on the GPU, a step over
+randomly permuted physical pages equals the step over the contiguous pool
+bit for bit (same tiles, same order, same arithmetic)."""
+from __future__ import annotations
+
+import ctypes as C
+import io
+
+import numpy as np
+import pytest
+
+from conftest import golden_table_text
+import paper_2505_17694_b200 as P
+from paper_2505_17694_b200 import _lib, workloads as W
+from paper_2505_17694_b200.errors import PrefixDecError
+from paper_2505_17694_b200.executor import _plan_arrays
+from paper_2505_17694_b200.forest import dtype_code
+from paper_2505_17694_b200.paging import page_layout
+
+
+@pytest.fixture(scope="module")
+def table():
+    return P.load_profile(io.StringIO(golden_table_text("a100_d128.csv")))
+
+
+def build_table(forest, plan, h_q, page_size, dtype=13, flags=0):
+    """codec_table_build with a dummy (never dereferenced) page table."""
+    dummy = (C.c_int32 * 4)()
+    dims = _lib.Dims(forest.bs, h_q, forest.h_kv, forest.d, 0, forest.h_kv, dtype, flags, 1 << 20, 148, 0,
+                     page_size, 0, C.cast(dummy, C.c_void_p) if page_size else None)
+    t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
+    Pt = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+    h = C.c_void_p()
+    _lib.check(_lib.lib().codec_table_build(forest._index, C.byref(dims), len(t_node), Pt(t_node, C.c_int64),
+                                            Pt(t_nq, C.c_int64), len(s_task), Pt(s_task, C.c_int32),
+                                            Pt(s_start, C.c_int64), Pt(s_stop, C.c_int64), Pt(s_block, C.c_int32),
+                                            C.byref(h)))
+    _lib.lib().codec_table_free(h)
+
+
+class TestLayout:
+    @pytest.mark.parametrize("page", [128, 256, 1024])
+    def test_node_page_bases(self, page):
+        spec = W.two_level(3000, 333, 5, h_q=8, h_kv=2, d=128, seed=1, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 2, 128)
+        base, n = page_layout(f, page)
+        want = np.concatenate([[0], np.cumsum([-(-node.len // page) for node in f.nodes])])
+        assert np.array_equal(base, want) and n == want[-1]
+
+
+class TestTableChecks:
+    def test_aligned_plan_builds(self, table):
+        spec = W.two_level(3000, 333, 24, h_q=32, h_kv=8, d=128, seed=2, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        plan = P.plan_device(f, 4, table, 8, 148, page_size=128)
+        build_table(f, plan, 32, 128, dtype_code("bfloat16"))
+
+    @pytest.mark.parametrize("page", [64, 100, 129])
+    def test_page_size_must_be_pow2_at_least_128(self, table, page):
+        spec = W.two_level(3000, 333, 24, h_q=32, h_kv=8, d=128, seed=2, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        plan = P.plan_device(f, 4, table, 8, 148)
+        with pytest.raises((PrefixDecError, ValueError), match="power of two"):
+            build_table(f, plan, 32, page, dtype_code("bfloat16"))
+
+    def test_float32_pool_is_unsupported(self, table):
+        spec = W.two_level(3000, 333, 24, h_q=32, h_kv=8, d=128, seed=2, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        plan = P.plan_device(f, 4, table, 8, 148)
+        with pytest.raises((PrefixDecError, ValueError), match="paged KV"):
+            build_table(f, plan, 32, 128, dtype_code("float32"))
+
+    def test_unaligned_suffix_slice_is_rejected(self, table):
+        # a reference plan that cuts a lightly shared 5000-token node into
+        # ceil(n / b)-token slices: 5000 / 3 -> 1667, not a multiple of 32
+        spec = W.two_level(5000, 100, 2, h_q=32, h_kv=8, d=128, seed=2, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        tasks = P.tasks_from_forest(f)
+        plan = P.plan_uniform_bk(tasks, table, 8, 3)
+        with pytest.raises((PrefixDecError, ValueError), match="not a multiple"):
+            build_table(f, plan, 32, 128, dtype_code("bfloat16"))
+
+    def test_contiguous_mode_unchanged(self, table):
+        spec = W.two_level(5000, 100, 2, h_q=32, h_kv=8, d=128, seed=2, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 8, 3)
+        build_table(f, plan, 32, 0, dtype_code("bfloat16"))
+
+
+@pytest.mark.gpu
+class TestPaged:
+    @pytest.mark.parametrize("page,shape", [(128, "two_level"), (256, "two_level"), (128, "forest"),
+                                             (512, "forest")])
+    def test_paged_equals_contiguous(self, table, page, shape):
+        import torch
+        from paper_2505_17694_b200.executor import DecodeStep
+        from paper_2505_17694_b200.paging import paged_pools
+        if shape == "two_level":
+            spec = W.two_level(4200, 300, 40, h_q=32, h_kv=8, d=128, seed=11, tensors=False)
+        else:
+            # three independent trees of different depth, odd node lengths
+            parent = [0, 0, 1, 1, 0, 4, 4, 4, 0, 8]
+            length = [0, 1000, 700, 130, 2600, 77, 300, 511, 900, 260]
+            paths = [(1, 2), (1, 3), (1, 2), (4, 5), (4, 6), (4, 7), (4, 7), (8, 9), (8, 9), (8, 9), (8,)]
+            spec = W.Spec(32, 8, 128, parent, length, None, None, paths, None, None)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        gen = torch.Generator().manual_seed(page)
+        T = f.total_tokens
+        kp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        vp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        q = (torch.randn((f.bs, 32, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        kx, vx, pt = paged_pools(f, kp, vp, page, n_phys_pages=page_layout(f, page)[1] + 7, generator=gen)
+        plan = P.plan_device(f, 4, table, 8, 148, page_size=page)
+        for concurrent in (False, True):
+            ref = DecodeStep(f, plan, 32, "bfloat16", concurrent=concurrent)(q, kp, vp)
+            got = DecodeStep(f, plan, 32, "bfloat16", concurrent=concurrent, page_size=page, page_table=pt,
+                             pool_tokens=kx.shape[1])(q, kx, vx)
+            torch.cuda.synchronize()
+            assert torch.isfinite(ref).all()
+            assert torch.equal(ref, got), (page, shape, concurrent, float((ref - got).abs().max()))
