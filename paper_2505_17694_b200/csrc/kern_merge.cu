@@ -20,11 +20,28 @@
 
 namespace codec {
 
+// The TC grid may still be finishing when the merge starts (the suffix
+// kernel before it was a programmatic dependent launch): wait until every
+// TC CTA bumped the completion counter.
+__device__ __forceinline__ void wait_tc_done(const int32_t* tc_done, int tc_ctas) {
+  if (!tc_done) return;
+  if (threadIdx.x == 0) {
+    int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(tc_done) : "memory");
+      if (v >= tc_ctas) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 template <typename A, int DPL>
 __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                     int off_slot, int n_merge, int g, int h_local, int d,
                                                     const A* __restrict__ part_o, const A* __restrict__ part_ml,
-                                                    A* __restrict__ out) {
+                                                    A* __restrict__ out, const int32_t* tc_done, int tc_ctas) {
+  wait_tc_done(tc_done, tc_ctas);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const int k = blockIdx.y * 4 + warp;
@@ -70,7 +87,9 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
-                                                       const float* __restrict__ part_ml, float* __restrict__ out) {
+                                                       const float* __restrict__ part_ml, float* __restrict__ out,
+                                                       const int32_t* tc_done, int tc_ctas) {
+  wait_tc_done(tc_done, tc_ctas);
   constexpr int kMax = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -120,18 +139,20 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
 int32_t cuda_status(cudaError_t e, const char* what);
 
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
-                     const void* part_o, const void* part_ml, void* out, cudaStream_t st) {
+                     const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
+                     int tc_ctas) {
   if (in.n_merge == 0) return CODEC_OK;
   const int h_local = in.h_local, g = hq_local / h_local;
   dim3 grid(in.n_merge, (g + 3) / 4);
 #define CODEC_MERGE(A, DPL)                                                                                    \
   merge_kernel<A, DPL><<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot,     \
                                              in.n_merge, g, h_local, d, (const A*)part_o, (const A*)part_ml,    \
-                                             (A*)out)
+                                             (A*)out, tc_done, tc_ctas)
   if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
   if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 16) {
     merge128_kernel<<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot, in.n_merge,
-                                          g, h_local, (const float*)part_o, (const float*)part_ml, (float*)out);
+                                          g, h_local, (const float*)part_o, (const float*)part_ml, (float*)out,
+                                          tc_done, tc_ctas);
     return cuda_status(cudaGetLastError(), "merge launch");
   }
   if (dtype == CODEC_F64) {

@@ -20,10 +20,8 @@
 // Memory path: one producer lane streams the slice with 3D TMA boxes of
 // 32 whole token rows (8 KB, SWIZZLE_128B; one op each for K and V: the
 // TMA unit's per-op cost, not bytes, limits small boxes) of the head-major
-// pool into a 2-stage ring (6 CTAs per SM hold ~200 KB in flight: measured
-// better than 4 stages x 3 CTAs, 3 x 4, 6 x 2, or 64-token stages); the
-// swizzle makes the ldmatrix reads conflict-free. Two consumer warps take 16
-// tokens of each stage.
+// pool into a 4-stage ring; the swizzle makes the ldmatrix reads
+// conflict-free. Two consumer warps take 16 tokens of each stage.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -39,7 +37,7 @@ namespace codec {
 #define CODEC_MMA_SUB 1
 #endif
 #ifndef CODEC_MMA_STAGES
-#define CODEC_MMA_STAGES 2  // 2 x 16 KB per CTA, 6 CTAs per SM: more CTAs beat deeper rings (cfg2 step 187 -> 178 us)
+#define CODEC_MMA_STAGES 4  // (2 stages x 6 CTAs per SM measured ~5 % faster on cfg2 but gave nondeterministic outputs, tools/repeat_check.py)
 #endif
 constexpr int kMmaWarps = 2;                       // consumer warps
 constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp

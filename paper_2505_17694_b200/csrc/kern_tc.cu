@@ -210,7 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                   long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog,
-                  const int32_t* __restrict__ page_table, int page_shift) {
+                  const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ tc_done) {
   const long long t_start = ctalog ? global_ns() : 0;
 #ifdef CODEC_TC_DEBUG
   // timing-only ablations (tools/tc_ablate.py); compiled out of the product
@@ -775,6 +775,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const int tl = t - 1, last = tl & 1, l_bar = 9 + (n & 1);
       if (quad == 0) PROG(1 + grp, t, 7);
       if (grp != last) {
+        // lx is single-buffered: the previous unit's epilogue group must
+        // have read its (l, m) first. Without this wait a short unit let
+        // this group overwrite lx while the other group, still finishing
+        // its last tile, had not read it yet (wrong l for a few rows at
+        // some SM budgets: tests/test_gpu_fuzz.py). epi_done[(n-1) % 2]
+        // completes after that epilogue's staging, long after its lx read.
+        if (n > 0) tc_wait(&bars->epi_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
         lx[r] = make_float2(have ? l : 0.f, my_m);
         named_arrive(l_bar, 256);
       } else {
@@ -853,7 +860,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   // exits, or a late arrival hits the shared memory of whatever CTA the SM
   // runs next. After the CTA barrier every such barrier is at most one
   // phase behind its final one, so the parity waits are exact.
+  __threadfence();  // this CTA's output / partial writes before the completion count below
   __syncthreads();
+  if (tid == 0 && tc_done) atomicAdd(tc_done, 1);  // the merge waits for every TC CTA (launch.cu)
   if (warp == kTcMmaWarp) {
     CODEC_TC_RANGE;
     int tiles = 0, units = 0;
@@ -967,7 +976,8 @@ static int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_loca
 
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift) {
+                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift,
+                  int32_t* tc_done) {
   const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
     if (cudaMalloc(&g_trace, kTraceLen * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
@@ -984,7 +994,8 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
   tc_pac_kernel<<<grid, kTcThreads, kTcSmem, st>>>(mk, mv, mq, table, in.off_tc, in.off_rows, in.off_tc_block_ptr,
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
-                                                   trace ? g_trace : nullptr, flags, ctalog, page_table, page_shift);
+                                                   trace ? g_trace : nullptr, flags, ctalog, page_table, page_shift,
+                                                   tc_done);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

@@ -14,7 +14,8 @@
 namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
-                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift);
+                  cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift,
+                  int32_t* tc_done);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
@@ -28,7 +29,8 @@ int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
-                     const void* part_o, const void* part_ml, void* out, cudaStream_t st);
+                     const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
+                     int tc_ctas);
 int32_t cuda_status(cudaError_t e, const char* what);
 }  // namespace codec
 
@@ -126,10 +128,16 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool do_tc = info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC);
   const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
   const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
-  // The mma.sync suffix kernel must not share SMs with the TC kernel: the
-  // TC CTA's setmaxnreg register hand-off corrupts the registers of a
-  // co-resident CTA of another kernel (observed on B200: wrong O in the
-  // suffix partials, tools/determinism.py). It runs after the TC kernel.
+  // The mma.sync suffix kernel is launched right after the TC kernel on the
+  // same stream with programmatic dependent launch: its CTAs start on the
+  // SMs the TC grid leaves once every TC CTA is resident (the TC grid gets
+  // its SMs first; nothing co-resides with a TC CTA, which holds the SM's
+  // whole register file and ~227 KB of SMEM). The merge, launched after the
+  // suffix kernel, may then start before the TC grid finished, so it waits
+  // for the TC CTAs' completion counter in the workspace (zeroed before the
+  // TC launch, bumped by every TC CTA after its last write). The CUDA-core
+  // GEMV / generic kernels fork onto the aux stream and join before the
+  // merge.
   const bool mma_gemv = do_gemv && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & CODEC_FLAG_GEMV_SIMT);
   const bool fork = aux_stream != nullptr && do_tc && ((do_gemv && !mma_gemv) || do_gen);
@@ -149,16 +157,22 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
       return fail(CODEC_ERR_CUDA, "fork failed");
   }
   const bool kev = (dims->flags & CODEC_FLAG_KERNEL_EVENTS) && !fork;
+  // TC completion counter: the first word of the workspace's reserved tail
+  int64_t ml_bytes = (int64_t)info->n_slots * hq_local * 2 * elem;
+  ml_bytes = (ml_bytes + 255) / 256 * 256;
+  int32_t* tc_done = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + o_bytes + ml_bytes);
+  const bool pdl = mma_gemv && do_tc && info->n_merge_fused == 0 && !kev;
+  if (do_tc && cudaMemsetAsync(tc_done, 0, sizeof(int32_t), st) != cudaSuccess)
+    return fail(CODEC_ERR_CUDA, "tc counter reset");
   if (kev) CODEC_TRY(kev_record(0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
-                        dims->flags, ctalog, dims->page_table, page_shift));
+                        dims->flags, ctalog, dims->page_table, page_shift, tc_done));
   if (kev) CODEC_TRY(kev_record(1, st));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
-                              info->off_merge_slot, st, ctalog,
-                              do_tc && info->n_merge_fused == 0 && !kev, dims->page_table, page_shift));
+                              info->off_merge_slot, st, ctalog, pdl, dims->page_table, page_shift));
   else if (do_gemv && page_shift)
     return fail(CODEC_ERR_UNSUPPORTED, "paged KV: suffix groups need the mma.sync kernel (bf16, d = 128, g <= 8)");
   else if (do_gemv)
@@ -175,7 +189,8 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
       return fail(CODEC_ERR_CUDA, "join failed");
   }
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
-    CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st));
+    CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st,
+                           do_tc ? tc_done : nullptr, 2 * info->n_tc_blocks));
   if (kev) {
     CODEC_TRY(kev_record(3, st));
     ++g_kev.n;
