@@ -583,6 +583,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const int qh = gv.kh * g + (grow % g);
       float l = 0.f, my_m = 0.f;  // my tiles' row sum, relative to 2^my_m
       bool have = false;          // processed a tile of this group
+      if (!__any_sync(0xffffffffu, valid)) {
+        // all 32 rows of this warp are padding (a piece with < 256 query-
+        // head rows): its P and O rows are never read back, so it only
+        // keeps the barrier protocol (S release, row-max hand-off with its
+        // equally idle partner warp, P-buffer wait, P release)
+        for (int j = 0; j < gv.n_tiles; ++j, ++t) {
+          if ((t & 1) != grp) continue;
+          const int b = t & 1;
+          tc_wait(&bars->s_full[b], (t >> 1) & 1);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_cluster(&bars->s_free[b], 0);
+          if (t > 0) named_sync(pub_other, 64);
+          if (t + 1 < t_total) {
+            mpub[grp * 128 + r] = 0.f;
+            named_arrive(pub_mine, 64);
+          }
+          if (t >= 2) tc_wait(&bars->pv_done[(t - 2) & 3], ((t - 2) >> 2) & 1);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_cluster(&bars->p_full[b], 0);
+        }
+      } else
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
         if ((t & 1) != grp) continue;
         const int b = t & 1;
