@@ -113,8 +113,9 @@ class DecodeStep:
             L.codec_table_free(h)
         self.blob_host = blob
         self.table = torch.from_numpy(blob).to(self.device)
-        # zeroed once: its last 256 bytes hold the persistent GEMV kernel's
-        # work counters, which every launch leaves at zero again
+        # partials, then a 256-byte tail whose first word is the TC kernel's
+        # per-step completion counter (reset by the library before each TC
+        # launch; the merge waits on it)
         self.workspace = torch.zeros(max(int(self.info.workspace_bytes), 256), dtype=torch.uint8, device=self.device)
         self.out_dtype = torch.float64 if self.tdtype == torch.float64 else torch.float32
         self.hq_local = (self.head_end - self.head_begin) * self.g
