@@ -247,7 +247,10 @@ CODEC_API int32_t codec_table_copy(const codec_table* t, int32_t* blob);
  *   k, v   [h_local][pool_tokens][d]     head-major node pool, nodes at
  *                                        their preorder offsets (kappa)
  *   out    [bs][h_q_local][d]            float32 for BF16/F32, float64 for F64
- *   workspace  >= info.workspace_bytes, 256-byte aligned
+ *   workspace  >= info.workspace_bytes, 256-byte aligned: partial (o, m, l)
+ *              storage, then a tail whose first int32 is the step's TC
+ *              completion counter (reset and used inside each call; a
+ *              workspace must not be shared by calls in flight)
  * All device pointers; asynchronous on `stream`.
  * ==================================================================== */
 /* Same step with the GEMV / generic kernels forked onto `aux_stream`
