@@ -20,8 +20,12 @@
 // Memory path: one producer lane streams the slice with 3D TMA boxes of
 // 32 whole token rows (8 KB, SWIZZLE_128B; one op each for K and V: the
 // TMA unit's per-op cost, not bytes, limits small boxes) of the head-major
-// pool into a 4-stage ring; the swizzle makes the ldmatrix reads
-// conflict-free. Two consumer warps take 16 tokens of each stage.
+// pool into a 2-stage ring (6 CTAs per SM: measured better than 4 stages x
+// 3 CTAs or 64-token stages); the swizzle makes the ldmatrix reads
+// conflict-free. Two consumer warps take 16 tokens of each stage; each
+// fences its generic-proxy reads of a stage before releasing it to the next
+// TMA write (without the fence a stage was sometimes overwritten under a
+// consumer's ldmatrix: wrong O, right l, tools/k3_race2.py).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -37,7 +41,7 @@ namespace codec {
 #define CODEC_MMA_SUB 1
 #endif
 #ifndef CODEC_MMA_STAGES
-#define CODEC_MMA_STAGES 4  // (2 stages x 6 CTAs per SM measured ~5 % faster on cfg2 but gave nondeterministic outputs, tools/repeat_check.py)
+#define CODEC_MMA_STAGES 2  // 2 x 16 KB per CTA, 6 CTAs per SM: more CTAs beat deeper rings (~5 % on cfg2)
 #endif
 constexpr int kMmaWarps = 2;                       // consumer warps
 constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
@@ -192,6 +196,9 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         hmma(acc[dm], a, b0, b1);
       }
       }
+      // this warp's ldmatrix reads of the stage (generic proxy) before the
+      // producer's next TMA write into it (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

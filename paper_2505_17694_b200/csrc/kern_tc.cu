@@ -862,6 +862,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
             named_sync(12, 128);
           }
+          // the staging reads / writes (generic proxy) before the Q warp's
+          // next TMA load into this buffer (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->epi_done[n & 1]);
           if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(9, tl);
