@@ -210,6 +210,7 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
 #define CODEC_FLAG_DBG_NO_LOADS 32768 /* TC producers skip the K/V TMA loads: timing only, wrong output (debug) */
 #define CODEC_FLAG_DBG_ISSUER_ONLY 131072 /* TC kernel runs only its MMA issuer, no waits: timing only (debug) */
+#define CODEC_FLAG_MERGE_NO_PDL 262144 /* launch the merge plainly after the suffix kernel (measurement) */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
 
 typedef struct codec_table codec_table;

@@ -24,6 +24,9 @@ namespace codec {
 // kernel before it was a programmatic dependent launch): wait until every
 // TC CTA bumped the completion counter.
 __device__ __forceinline__ void wait_tc_done(const int32_t* tc_done, int tc_ctas) {
+  // launched as a programmatic dependent of the suffix kernel: wait for its
+  // completion (and memory) first; a no-op for a plain launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!tc_done) return;
   if (threadIdx.x == 0) {
     int v;
@@ -140,7 +143,7 @@ int32_t cuda_status(cudaError_t e, const char* what);
 
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas) {
+                     int tc_ctas, bool pdl) {
   if (in.n_merge == 0) return CODEC_OK;
   const int h_local = in.h_local, g = hq_local / h_local;
   dim3 grid(in.n_merge, (g + 3) / 4);
@@ -150,9 +153,22 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
                                              (A*)out, tc_done, tc_ctas)
   if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
   if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 16) {
-    merge128_kernel<<<grid, 128, 0, st>>>(table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot, in.n_merge,
-                                          g, h_local, (const float*)part_o, (const float*)part_ml, (float*)out,
-                                          tc_done, tc_ctas);
+    // after the suffix kernel on the same stream: programmatic dependent
+    // launch, so the merge CTAs are resident when it retires (they wait in
+    // griddepcontrol.wait, then for the TC counter)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, merge128_kernel, table, in.off_merge_req, in.off_merge_ptr,
+                                       in.off_merge_slot, in.n_merge, g, h_local, (const float*)part_o,
+                                       (const float*)part_ml, (float*)out, tc_done, tc_ctas);
+    if (e != cudaSuccess) return cuda_status(e, "merge launch");
     return cuda_status(cudaGetLastError(), "merge launch");
   }
   if (dtype == CODEC_F64) {

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
                    int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog,
                    const int32_t* __restrict__ page_table, int page_shift) {
   const long long t_start = ctalog ? global_ns() : 0;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge may be scheduled early (it waits)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMmaStages * kMmaStageBytes);

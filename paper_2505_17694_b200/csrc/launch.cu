@@ -30,7 +30,7 @@ int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas);
+                     int tc_ctas, bool pdl);
 int32_t cuda_status(cudaError_t e, const char* what);
 }  // namespace codec
 
@@ -190,7 +190,9 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   }
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st,
-                           do_tc ? tc_done : nullptr, 2 * info->n_tc_blocks));
+                           do_tc ? tc_done : nullptr, 2 * info->n_tc_blocks,
+                           mma_gemv && !fork && !kev && !(dims->flags & CODEC_FLAG_SKIP_GEMV) &&
+                               !(dims->flags & CODEC_FLAG_MERGE_NO_PDL)));
   if (kev) {
     CODEC_TRY(kev_record(3, st));
     ++g_kev.n;
