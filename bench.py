@@ -275,7 +275,17 @@ def main():
     budgets = [sms] if (args.serial or args.quick) else [sms] + list(range(136, 63, -8))
     tune_ms = {}
     best = None
-    for b in budgets:
+
+    def refine():
+        # a finer pass (+-4 SMs) around the coarse optimum
+        if len(budgets) < 2 or best is None:
+            return []
+        b0 = best[1]
+        return [b for b in (b0 - 4, b0 + 4) if 16 <= b < sms and b not in tune_ms]
+
+    queue = list(budgets)
+    while queue:
+        b = queue.pop(0)
         pl, st, ms_plan = make(b)
         for _ in range(3):
             st(q_dev, kp, vp, out=out)
@@ -294,6 +304,9 @@ def main():
         tune_ms[b] = round(t_b, 4)
         if best is None or t_b < best[0]:
             best = (t_b, b, pl, st, ms_plan)
+        if not queue and not getattr(refine, "done", False):
+            refine.done = True
+            queue = refine()
     _, budget, plan, step, plan_ms = best
     m = args.blocks or max(1, budget // h_local)
     # a twin step that records CUDA events around each of its kernels on the
