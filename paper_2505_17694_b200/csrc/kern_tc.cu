@@ -434,7 +434,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       if (gv.n_tiles == 0) continue;
-      if (n == 0) {  // the first unit's Q is gathered by the softmax warps (lower latency)
+      if (n == 0) {  // the first unit's Q is loaded by the softmax warps (lower latency)
+        if (gv.qreq0 >= 0) qtma_uses[0] = 1;  // ... through q_tma[0]'s first phase
         ++n;
         continue;
       }
@@ -552,7 +553,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     };
     int gi = g_begin;
     while (gi < g_end && group_view(table, off_groups, off_rows, gi).n_tiles == 0) ++gi;
-    if (gi < g_end && grp == 0) {
+    if (gi < g_end && grp == 0 && group_view(table, off_groups, off_rows, gi).qreq0 >= 0) {
+      // first unit's Q, consecutive requests: the two 4D TMA boxes the Q
+      // warp uses for later units (q_tma[0]'s first phase)
+      const GroupView gv = group_view(table, off_groups, off_rows, gi);
+      if (tid == 0) {
+        const int rq = 128 / g;
+        mbar_arrive_expect_tx(&bars->q_tma[0], kQBytes);
+        tc::tma_load_4d(smem + kOffQ, &tmq, 0, 0, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[0]);
+        tc::tma_load_4d(smem + kOffQ + kQAtom, &tmq, 0, 1, gv.kh * g, gv.qreq0 + (int)rank * rq, &bars->q_tma[0]);
+        tc_wait(&bars->q_tma[0], 0);
+        tc::mbar_arrive_cluster(&bars->q_full[0], 0);
+      }
+    } else if (gi < g_end && grp == 0) {
       // first unit's Q: one row per thread of group A, all 16 loads in flight
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
       const int ridx = grow / g;
