@@ -77,7 +77,13 @@ constexpr int kTcRegsSoftmax = 200, kTcRegsOther = 96;
 static_assert(32 * kTcSoftmaxWarps * kTcRegsSoftmax + (kTcThreads - 32 * kTcSoftmaxWarps) * kTcRegsOther <=
                   kTcThreads * (65536 / kTcThreads / 8 * 8),
               "setmaxnreg.inc would wait forever for registers the CTA does not own");
-constexpr int kTcKStages = 4, kTcVStages = 6;
+// K / V ring depths (SMEM: 64 KB of Q + 16 KB per stage); 5 / 5 and 3 / 7
+// measured the same as 4 / 6 on cfg2
+#ifndef CODEC_TC_KSTAGES
+#define CODEC_TC_KSTAGES 4
+#define CODEC_TC_VSTAGES 6
+#endif
+constexpr int kTcKStages = CODEC_TC_KSTAGES, kTcVStages = CODEC_TC_VSTAGES;
 constexpr int kOffQ = 0;                     // Q0, Q1 (double-buffered across units)
 constexpr int kOffK = kOffQ + 2 * kQBytes;
 constexpr int kOffV = kOffK + kTcKStages * kHalfBytes;
@@ -371,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // PV: A = P (TMEM, 8 columns per 16 tokens), B = V half (MN-major SW128,
     // one atom column).
     CODEC_TC_RANGE;
-    constexpr int kVAhead = 4;
+    constexpr int kVAhead = kTcVStages - 2;
     static_assert(kVAhead + 2 <= kTcVStages, "V(tp + kVAhead) must reuse a stage PV(tp - 2) released");
     TileCursor vc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
     vc.open();
