@@ -1,23 +1,29 @@
 """Decode-attention benchmark (BASELINE.json metric) for the B200 path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2] [--no-cpu-baseline]
+                    [--config cfg2] [--partition heads|trees] [--no-cpu-baseline]
 
 Workload (config[1] of BASELINE.json): Llama-3-8B shape, 32 q / 8 kv
 heads, d=128, bf16 KV; 256 requests share a 32K-token system prompt, each
 with a private 512-token suffix. Synthetic N(0,1)/sqrt(d) data generated
 on the device (K/V pool 671 MB > 126 MB L2, so every step streams from
-HBM). A "step" = one decode-attention call over all 256 requests.
+HBM). A "step" = one decode-attention call over all requests.
 
-value = effective unique-KV GB/s over the whole job (all ranks); with N
-GPUs the kv heads are split N ways (tensor-parallel head split) and the
-per-rank outputs are all-gathered over NCCL inside the timed step.
-`e2e` times the same step through the public API with queries copied from
-pinned host memory and the output read back every step.
+value = effective unique-KV GB/s over the whole job (all ranks). With N
+GPUs the step is sharded: `--partition heads` splits the
+kv heads N ways (tensor-parallel head split; default) and `--partition
+trees` LPT-assigns whole trees of the forest to ranks (cfg4's default);
+either way the per-rank outputs are all-gathered over NCCL inside the
+timed step (by head block or by request). `e2e` times the same step
+through the public API with queries copied from pinned host memory and the
+output read back every step, in the same >= 2 s windows as `value`.
+After timing, untimed, the bench checks sampled requests of its own output
+against a float64 recomputation on the device (and, with N > 1, that the
+gathered output holds every rank's rows).
 
---impl reference times the reference's CPU algorithm (the oracle port
-under oracle/, numpy, all host threads) on the same whole workload per
-step (rank 0 only).
+--impl reference times the reference's CPU implementation (prefixdec,
+installed unmodified into baseline/_ref; the oracle port under oracle/
+when it is absent) on a bounded sample of the same workload (rank 0 only).
 """
 from __future__ import annotations
 
@@ -30,6 +36,7 @@ import subprocess
 import sys
 import time
 from pathlib import Path
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -40,19 +47,20 @@ METRIC = "decode-attn µs/step & effective KV GB/s (unique bytes) vs HBM rooflin
 CONFIGS = {  # BASELINE.json "configs"; structures from workloads.make_config
     "cfg1": dict(h_q=8, h_kv=8, d=128,
                  label="cfg1: tiny 2-level tree, 16 requests sharing a 1K prefix + 64-token suffixes, 8 heads x d128"),
-    "cfg2": dict(h_q=32, h_kv=8, d=128,
+    "cfg2": dict(h_q=32, h_kv=8, d=128, ref_heads=2,
                  label="cfg2: Llama-3-8B shape (32 q / 8 kv heads, d128, bf16 KV), 256 requests sharing a "
                        "32K system prompt + 512-token suffixes"),
-    "cfg3": dict(h_q=32, h_kv=8, d=128,
+    "cfg3": dict(h_q=32, h_kv=8, d=128, ref_heads=2,
                  label="cfg3: tree-of-thought / beam tree, depth 4, branching 4, 8K root, irregular node lengths "
                        "(64 requests), Llama-3-8B heads"),
-    "cfg4": dict(h_q=32, h_kv=8, d=128, cpu_trees=range(8),
+    "cfg4": dict(h_q=32, h_kv=8, d=128, cpu_trees=range(8), ref_heads=2,
                  label="cfg4: imbalanced forest, 64 trees with 512..128K shared prefixes and 1..512 requests per "
                        "tree + 512-token suffixes (4680 requests), Llama-3-8B heads"),
-    "cfg5": dict(h_q=64, h_kv=8, d=128,
+    "cfg5": dict(h_q=64, h_kv=8, d=128, ref_heads=1,
                  label="cfg5: Llama-3-70B shape (64 q / 8 kv heads, d128, bf16 KV), 1024 requests sharing a "
                        "64K prefix + 512-token suffixes"),
 }
+MIN_WINDOW_S = 2.0  # every timed quantity: >= 2 s of back-to-back windows, median window
 
 
 def structure(name, **kw):
@@ -113,177 +121,181 @@ class ClockSampler:
                 return None
         sm = [v for v in (num(r[0]) for r in rows) if v is not None]
         mx = [v for v in (num(r[1]) for r in rows) if v is not None]
+        pw = [v for v in (num(r[2]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "power_w_median": statistics.median(pw) if pw else None, "reasons": reasons, "samples": len(rows)}
 
 
 # ---------------------------------------------------------------- CPU side
-def cpu_reference_sample(cfg, workers=None, seed=0):
-    """The whole workload (every kv head, all requests) through the oracle
-    port of the reference executor (numpy, host threads): returns (seconds,
-    unique KV bytes at bf16 width, description). Inputs are generated
-    once per process (fp32, the reference's CPU dtype) and not timed."""
-    from oracle import attention as OA
-    from oracle import plan as OP
-    from oracle import index as OI
-    from paper_2505_17694_b200 import workloads as W
-
-    workers = workers or os.cpu_count()
-    key = (cfg["label"], seed)
-    if key not in _CPU_CACHE:
-        over = {"only_trees": cfg["cpu_trees"]} if "cpu_trees" in cfg else {}
-        spec = structure(cfg["name"], dtype=np.float32, **over)
-        z = np.zeros((0, cfg["h_kv"], cfg["d"]), np.float32)
-        fd = OA.ForestData(spec.parent, [z] + spec.keys[1:], [z] + spec.values[1:], spec.paths)
-        # the CPU's own best split: shared nodes sliced once per host thread so
-        # every thread has work (the reference's thread pool, executor.py:194)
-        qs = OI.query_sets(spec.paths, spec.n_nodes)
-        subs = []
-        for node, nq, n in OP.node_tasks(qs, spec.length):
-            for a, b in OP.slices(n, workers if nq > 1 else 1):
-                subs.append((node, a, b))
-        _CPU_CACHE[key] = (spec, fd, subs)
-    spec, fd, subs = _CPU_CACHE[key]
-    t0 = time.perf_counter()
-    OA.execute(fd, spec.queries, subs, workers=workers)
-    dt = time.perf_counter() - t0
-    kv_bytes = sum(spec.length[1:]) * cfg["h_kv"] * cfg["d"] * 2 * 2
-    what = (f"trees {list(cfg['cpu_trees'])} of the workload ({spec.bs} requests)" if "cpu_trees" in cfg
-            else f"the whole workload ({spec.bs} requests)")
-    desc = (f"{what}: all {cfg['h_kv']} kv heads ({cfg['h_q']} q heads), {sum(spec.length[1:])} KV tokens; "
-            f"fp32 numpy oracle port of prefixdec.execute, {workers} threads, plan of {len(subs)} subtasks")
-    return dt, kv_bytes, desc
+def _ref_sample_spec(cfg):
+    """The bounded CPU sample of a config: kv heads [0, ref_heads) of the
+    whole workload (heads are independent, attention.py:91-92), and for
+    cfg4 trees 0..7 only (its fp32 tensors exceed host RAM)."""
+    over = {"only_trees": cfg["cpu_trees"]} if "cpu_trees" in cfg else {}
+    hk = cfg.get("ref_heads", cfg["h_kv"])
+    g = cfg["h_q"] // cfg["h_kv"]
+    if hk != cfg["h_kv"]:
+        over.update(h_q=hk * g, h_kv=hk)
+    spec = structure(cfg["name"], dtype=np.float32, **over)
+    what = (f"trees {list(cfg['cpu_trees'])} ({spec.bs} requests)" if "cpu_trees" in cfg
+            else f"all {spec.bs} requests")
+    desc = f"{what}, kv heads 0..{hk - 1} of {cfg['h_kv']} ({hk * g} q heads), {sum(spec.length[1:])} KV tokens"
+    return spec, hk, desc
 
 
-_CPU_CACHE = {}
+def _ref_bytes(spec, hk, d):
+    """unique KV bytes of the sample at bf16 width (the GPU's unit)"""
+    qs = set(n for p in spec.paths for n in p)
+    return sum(spec.length[n] for n in qs) * hk * d * 2 * 2
+
+
+class ReferenceRunner:
+    """prefixdec.execute() -- the reference's own CPU path, unmodified,
+    from baseline/_ref -- on a bounded sample, with the plan parameters of
+    the GPU run: the same cost CSV (the bundled B200
+    profile) and m = the GPU plan's tensor-core blocks; the numpy kernel
+    backend (faster than Cython at every shared shape, SURVEY.md §6);
+    BlockPool(worker_count = host threads). Falls back to the oracle port
+    when baseline/_ref is absent."""
+
+    def __init__(self, cfg, m=48, workers=None):
+        self.cfg = cfg
+        self.workers = workers or os.cpu_count()
+        spec, hk, desc = _ref_sample_spec(cfg)
+        self.bytes = _ref_bytes(spec, hk, cfg["d"])
+        ref = ROOT / "baseline" / "_ref"
+        self.kind = "port"
+        try:
+            if ref.exists():
+                sys.path.insert(0, str(ref))
+                os.environ["PREFIXDEC_KERNEL"] = "python"
+                import prefixdec  # noqa: F401
+                self.kind = "reference"
+        except ImportError:
+            self.kind = "port"
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            import prefixdec as R
+            q = R.QueryBatch(spec.queries, hk)
+            self.forest = R.build_forest(spec.node_specs(), spec.paths, q)
+            self.queries = q
+            table = R.load_profile(ROOT / "paper_2505_17694_b200" / "profiles" / "b200_d128.csv")
+            self.plan = R.divide_and_schedule(R.tasks_from_forest(self.forest), table, m)
+            self.pool = R.BlockPool(worker_count=self.workers)
+            self.run = lambda: R.execute(self.forest, self.queries, self.plan, self.pool)
+            n_sub = len(self.plan.subtasks)
+            plan_desc = f"divide_and_schedule(m={m}, B200 profile CSV): {n_sub} subtasks"
+        else:
+            from oracle import attention as OA
+            from oracle import index as OI
+            from oracle import plan as OP
+            z = np.zeros((0, hk, cfg["d"]), np.float32)
+            fd = OA.ForestData(spec.parent, [z] + spec.keys[1:], [z] + spec.values[1:], spec.paths)
+            qs = OI.query_sets(spec.paths, spec.n_nodes)
+            subs = [(node, a, b) for node, nq, n in OP.node_tasks(qs, spec.length)
+                    for a, b in OP.slices(n, self.workers if nq > 1 else 1)]
+            self.run = lambda: OA.execute(fd, spec.queries, subs, workers=self.workers)
+            plan_desc = f"oracle port, per-thread split plan of {len(subs)} subtasks"
+        self.plan_s = time.perf_counter() - t0
+        self.desc = (f"{desc}; fp32 inputs (the reference has no bf16); "
+                     f"{'prefixdec.execute from baseline/_ref, numpy backend' if self.kind == 'reference' else 'oracle port'}"
+                     f", {self.workers} threads, {plan_desc}")
+
+    def step(self):
+        t0 = time.perf_counter()
+        self.run()
+        return time.perf_counter() - t0
 
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    workers = os.cpu_count()
+    r = ReferenceRunner(cfg, m=args.ref_m)
     for _ in range(args.warmup):
-        cpu_reference_sample(cfg, workers=workers)
-    times = []
-    for _ in range(args.steps):
-        dt, kv_bytes, desc = cpu_reference_sample(cfg, workers=workers)
-        times.append(dt)
+        r.step()
+    times = [r.step() for _ in range(args.steps)]
     t = statistics.mean(times)
-    value = kv_bytes / t / 1e9
+    value = r.bytes / t / 1e9
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"], "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": workers, "kind": "port", "sample": desc},
+        "config": {"workload": cfg["label"], "sample": r.desc},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": r.workers, "kind": r.kind, "sample": r.desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # ---------------------------------------------------------------- GPU side
-KERNEL_EVENTS = 16384  # CODEC_FLAG_KERNEL_EVENTS (include/codec_b200.h)
+def prepare(config="cfg2", dev=None, rank=0, world=1, partition=None, flags=0, serial=False, blocks=0,
+            budgets=None, seed=1234, quick=False):
+    """Inputs, plan and the autotuned DecodeStep of one rank of the bench
+    (the exact step `value` times; tests/test_gpu_fullsize.py runs it too).
 
-
-def kernel_times():
-    """[calls, 3] ms of (TC, suffix, merge) kernels of the calls recorded
-    under CODEC_FLAG_KERNEL_EVENTS since the last read."""
-    import ctypes as C
-    from paper_2505_17694_b200 import _lib
-    buf = (C.c_float * (3 * 512))()
-    n = C.c_int32()
-    _lib.check(_lib.lib().codec_kernel_times(buf, 512, C.byref(n)))
-    return np.array(buf[:3 * n.value], dtype=np.float64).reshape(-1, 3)
-
-
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flags", type=int, default=0)
-    ap.add_argument("--blocks", type=int, default=0, help="planner m (0: SMs // local kv heads)")
-    ap.add_argument("--quick", action="store_true", help="profiling run: no e2e / clocks / cpu baseline")
-    ap.add_argument("--serial", action="store_true", help="one stream: TC, GEMV and merge back to back")
-    ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph replay")
-    args = ap.parse_args()
-    cfg = dict(CONFIGS[args.config], name=args.config)
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, cfg, rank, world)
-
+    Synthetic bf16 K/V pools and queries drawn on the device (seeded per
+    rank); plan = plan_device (shared nodes whole, divided by the device
+    balancer; suffixes on the mma.sync kernel); the tensor-core SM budget
+    is tuned once per plan (cuDNN-benchmark style, untimed), max over ranks."""
     import torch
     import torch.distributed as dist
 
     import paper_2505_17694_b200 as P
-    from paper_2505_17694_b200 import workloads as W
+    from paper_2505_17694_b200 import parallel as PL
     from paper_2505_17694_b200.executor import DecodeStep
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    cfg = dict(CONFIGS[config], name=config)
+    dev = dev or torch.device("cuda", 0)
     h_kv, h_q, d = cfg["h_kv"], cfg["h_q"], cfg["d"]
-    assert h_kv % world == 0, "kv heads must split evenly across ranks"
-    h_local = h_kv // world
-    h0 = rank * h_local
     g = h_q // h_kv
-
-    # structure + device-resident synthetic KV pool (heads [h0, h0 + h_local))
-    spec = structure(args.config, tensors=False)
-    forest = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, h_kv, d)
-    bs = spec.bs
+    partition = partition or ("trees" if config == "cfg4" and world > 1 else "heads")
+    spec = structure(config, tensors=False)
+    full = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, h_kv, d)
+    table = P.load_default_profile()
+    shard = shards = None
+    if partition == "trees" and world > 1:
+        part = PL.tree_partition(full, table, world, head_multiplicity=g)
+        shards = [PL.shard_trees(full, part, r) for r in range(world)]
+        shard = shards[rank]
+        forest = shard.forest(h_kv, d)
+        h0, h_local = 0, h_kv
+    elif partition in ("heads", "trees"):
+        h0, h1 = PL.head_shard(h_kv, world, rank)
+        forest, h_local = full, h1 - h0
+    else:
+        raise ValueError(f"partition must be heads or trees, got {partition!r}")
+    hq_local = h_local * g
+    bs = forest.bs
     T = forest.total_tokens
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + h0)
+    gen.manual_seed(seed + rank)
     sc = 1.0 / math.sqrt(d)
     kp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
     vp = (torch.randn((h_local, T, d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16)
-    hq_local = h_local * g
     q_host = (torch.randn((bs, hq_local, d), generator=torch.Generator().manual_seed(99 + rank)) * sc
               ).to(torch.bfloat16).pin_memory()
     q_dev = q_host.to(dev)
-
-    # plan: shared-node row chunks divided + LPT-scheduled onto the persistent
-    # tensor-core CTAs (reference planner algorithm, B200 profile), unshared
-    # suffixes on the concurrent GEMV kernel; the SM split between the two is
-    # tuned once per plan (cuDNN-benchmark style), untimed
-    table = P.load_default_profile()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     out = torch.empty((bs, hq_local, d), dtype=torch.float32, device=dev)
 
     def make(budget):
         t0 = time.perf_counter()
-        if args.blocks:
-            pl = P.divide_and_schedule(P.device_tasks(forest, g), table, args.blocks)
+        if blocks:
+            pl = P.divide_and_schedule(P.device_tasks(forest, g), table, blocks)
         else:
             pl = P.plan_device(forest, g, table, h_local, sms, budget)
         ms_plan = (time.perf_counter() - t0) * 1e3
         st = DecodeStep(forest, pl, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
-                        flags=args.flags, tc_sm_budget=budget, concurrent=not args.serial)
+                        flags=flags, tc_sm_budget=budget, concurrent=not serial)
         return pl, st, ms_plan
 
     # TC SM budget: the SMs the TC grid leaves free run the suffix kernel
     # from the start (programmatic dependent launch); tuned once per plan
-    budgets = [sms] if (args.serial or args.quick) else [sms] + list(range(136, 63, -8))
-    tune_ms = {}
-    best = None
-
-    def refine():
-        # a finer pass (+-4 SMs) around the coarse optimum
-        if len(budgets) < 2 or best is None:
-            return []
-        b0 = best[1]
-        return [b for b in (b0 - 4, b0 + 4) if 16 <= b < sms and b not in tune_ms]
-
-    queue = list(budgets)
+    if budgets is None:
+        budgets = [sms] if (serial or quick) else [sms] + list(range(136, 63, -8))
+    tune_ms, best = {}, None
+    queue, refined = list(budgets), len(budgets) < 2
     while queue:
         b = queue.pop(0)
         pl, st, ms_plan = make(b)
@@ -304,40 +316,129 @@ def main():
         tune_ms[b] = round(t_b, 4)
         if best is None or t_b < best[0]:
             best = (t_b, b, pl, st, ms_plan)
-        if not queue and not getattr(refine, "done", False):
-            refine.done = True
-            queue = refine()
+        if not queue and not refined:  # a finer pass (+-4 SMs) around the coarse optimum
+            refined = True
+            queue = [x for x in (best[1] - 4, best[1] + 4) if 16 <= x < sms and x not in tune_ms]
     _, budget, plan, step, plan_ms = best
-    m = args.blocks or max(1, budget // h_local)
-    # a twin step that records CUDA events around each of its kernels on the
-    # launching stream (CODEC_FLAG_KERNEL_EVENTS), timed in its own window
-    # right after the main one: the events sit between the kernels and
-    # would stop the suffix kernel's programmatic early launch in `value`
-    step_ev = DecodeStep(forest, plan, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
-                         flags=args.flags | KERNEL_EVENTS, tc_sm_budget=budget, concurrent=not args.serial)
-    gathered = torch.empty((world, bs, hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
+    return SimpleNamespace(cfg=cfg, config=config, dev=dev, rank=rank, world=world, partition=partition,
+                           spec=spec, full=full, forest=forest, shard=shard, shards=shards, h0=h0,
+                           h_local=h_local, hq_local=hq_local, g=g, kp=kp, vp=vp, q_host=q_host, q_dev=q_dev,
+                           out=out, sms=sms, plan=plan, budget=budget, step=step, plan_ms=plan_ms,
+                           tune_ms=tune_ms, table=table, blocks=blocks)
+
+
+def path_reference(forest, kp, vp, q, r):
+    """Single-softmax attention of (local) request r over its root-to-leaf
+    path (naive_attention, attention.py:164-187) in float64 on the device
+    from the same bf16 values -- the bench's untimed self-check."""
+    import torch
+    toks = torch.cat([torch.arange(forest.token_offset[n], forest.token_offset[n] + forest.visible_count(n, r),
+                                   device=kp.device) for n in forest.paths[r]])
+    h_local = kp.shape[0]
+    g = q.shape[1] // h_local
+    k = kp[:, toks].double()
+    v = vp[:, toks].double()
+    qq = q[r].double().view(h_local, g, -1)
+    s = torch.einsum("hgd,hld->hgl", qq, k) / math.sqrt(forest.d)
+    p = torch.softmax(s, dim=-1)
+    return torch.einsum("hgl,hld->hgd", p, v).reshape(q.shape[1], -1)
+
+
+def verify(ns, out, n=8, seed=0):
+    """Sampled requests of `out` against path_reference: the bf16 bar of
+    the north star (max-abs 2e-3 and max-norm rel 1e-2)."""
+    bs = ns.forest.bs
+    rng = np.random.default_rng(seed)
+    reqs = sorted({0, bs - 1} | set(rng.choice(bs, size=min(n, bs), replace=False).tolist()))
+    worst_abs = worst_rel = 0.0
+    for r in reqs:
+        ref = path_reference(ns.forest, ns.kp, ns.vp, ns.q_dev, r)
+        err = float((out[r].double() - ref).abs().max())
+        worst_abs = max(worst_abs, err)
+        worst_rel = max(worst_rel, err / float(ref.abs().max()))
+    ok = worst_abs <= 2e-3 and worst_rel <= 1e-2 and bool(out.isfinite().all())
+    return {"requests": len(reqs), "max_abs": worst_abs, "max_rel": worst_rel, "ok": ok,
+            "reference": "float64 softmax over each sampled request's path, on the device, same bf16 inputs"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--partition", default=None, choices=["heads", "trees"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--blocks", type=int, default=0, help="planner m (0: the device plan)")
+    ap.add_argument("--ref-m", type=int, default=48, help="reference arm: planner m (the GPU plan's TC blocks)")
+    ap.add_argument("--quick", action="store_true", help="profiling run: no e2e / clocks / cpu baseline / tuning")
+    ap.add_argument("--serial", action="store_true", help="one stream: TC, GEMV and merge back to back")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph replay")
+    ap.add_argument("--budget", type=int, default=0, help="fixed tensor-core SM budget (no tuning)")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config], name=args.config)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_17694_b200 as P
+    from paper_2505_17694_b200 import parallel as PL
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ns = prepare(args.config, dev, rank, world, args.partition, args.flags, args.serial, args.blocks,
+                 budgets=[args.budget] if args.budget else None, quick=args.quick)
+    step, plan, budget = ns.step, ns.plan, ns.budget
+    kp, vp, q_dev, q_host, out = ns.kp, ns.vp, ns.q_dev, ns.q_host, ns.out
+    bs, hq_local, d = ns.forest.bs, ns.hq_local, ns.cfg["d"]
+    full_bs, h_q = ns.full.bs, ns.cfg["h_q"]
+    m = args.blocks or max(1, budget // 2)
+    trees = ns.partition == "trees" and world > 1
+    # receive buffers of the output gather (by head block or by request)
+    n_max = max(s.bs for s in ns.shards) if trees else bs
+    gathered = torch.empty((world, n_max, hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
+    send = torch.zeros((n_max, hq_local, d), dtype=torch.float32, device=dev) if trees else None
+
+    def gather(o, buf):
+        if world == 1:
+            return o
+        if trees:  # pad to the largest shard, one all-gather, scatter back by request
+            send[:bs].copy_(o)
+            dist.all_gather_into_tensor(buf.view(world * n_max, hq_local, d), send)
+            return buf
+        dist.all_gather_into_tensor(buf.view(world * bs, hq_local, d), o)
+        return buf
 
     # the timed step replays a CUDA graph of the decode step (its three
     # launches recorded once; no per-step host work)
     replay = step.capture(q_dev, kp, vp, out) if not args.no_graph else None
 
-    def one_step(qd):
-        if replay is not None and qd is q_dev:
+    def one_step():
+        if replay is not None:
             replay()
         else:
-            step(qd, kp, vp, out=out)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
-        return out
+            step(q_dev, kp, vp, out=out)
+        return gather(out, gathered)
 
-    work = P.device_work(forest, h_q, element_size=2, head_fraction=h_local / h_kv)
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
     stream = torch.cuda.current_stream(dev)
 
     def timed(n, fn, min_seconds=0.0):
         """ms per call over n calls between barrier+sync on both sides, CUDA
-        events on the launching stream, max over ranks. With min_seconds,
-        the n-call window is repeated until that much wall time passed (so
-        the clock sampler sees the load) and the median window is used."""
+        events on the launching stream, max over ranks. The n-call window
+        is repeated until min_seconds of wall time passed (so the clock
+        sampler sees the load and the power cap settles) and the median
+        window is used."""
         windows = []
         t_start = time.perf_counter()
         while True:
@@ -356,60 +457,74 @@ def main():
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             windows.append(ms)
-            if time.perf_counter() - t_start >= min_seconds or len(windows) >= 500:
+            if time.perf_counter() - t_start >= min_seconds or len(windows) >= 5000:
                 break
         return statistics.median(windows), len(windows)
 
+    win_s = 0.0 if args.quick else MIN_WINDOW_S
     for _ in range(max(args.warmup, 3)):
-        one_step(q_dev)
+        one_step()
     torch.cuda.synchronize(dev)
     clocks = None if args.quick else ClockSampler(local_rank)
-    ms, windows = timed(args.steps, lambda: one_step(q_dev), min_seconds=0 if args.quick else 2.0)
+    ms, windows = timed(args.steps, one_step, min_seconds=win_s)
     clock_rec = clocks.stop() if clocks else None
 
-    # per-kernel device time: events around each kernel on its stream, over
-    # a timed window of the twin step (up to 512 calls)
+    # per-kernel device time: a twin step that records CUDA events around
+    # each of its kernels (codec_kernel_timer) on the launching stream, in
+    # the same >= 2 s windows. The events sit between the kernels, so the
+    # twin runs them back to back (no early suffix launch): these times
+    # attribute work to kernels; `value` is the overlapped step.
+    step_ev = step.with_budget(budget, timer=True)
     for _ in range(3):
         step_ev(q_dev, kp, vp, out=out)
     torch.cuda.synchronize(dev)
-    kernel_times()  # drop the warm-up calls' events
-    ms_ev = timed(args.steps, lambda: step_ev(q_dev, kp, vp, out=out))[0]
+    step_ev.kernel_times()  # drop the warm-up calls' events
+    ms_ev = 0.0
+    kt_all = []
+    t_ev0 = time.perf_counter()
+    while True:  # read the ring between windows (4096 calls)
+        ms_w, _ = timed(args.steps, lambda: step_ev(q_dev, kp, vp, out=out))
+        ms_ev = ms_w
+        kt_all.append(step_ev.kernel_times())
+        if time.perf_counter() - t_ev0 >= win_s:
+            break
+    kt = np.concatenate(kt_all) if kt_all else np.zeros((0, 3))
     info = step.info
-    kt = kernel_times()
     phases = {}
     if len(kt):
         for j, (name, present) in enumerate((("tc", info.n_tc_groups), ("gemv", info.n_gemv_groups),
                                              ("merge", info.n_merge))):
             if present:
-                phases[name] = float(np.mean(kt[:, j]))
+                phases[name] = float(np.median(kt[:, j]))
 
-    hbm, tf_burst, tf_sus, peak_kind = peaks()
-    total_bytes = work["unique_kv_bytes"] * world
+    work_local = P.device_work(ns.forest, h_q, element_size=2, head_fraction=ns.h_local / ns.cfg["h_kv"])
+    work_full = P.device_work(ns.full, h_q, element_size=2)
+    total_bytes = work_full["unique_kv_bytes"]
     value = total_bytes / (ms * 1e-3) / 1e9
-    # bytes / flops attributed to each kernel
-    tc_rows = sum(n.len for n in forest.nodes[1:] if len(n.query_set) * g >= 16)
-    kv_tc = tc_rows * h_local * d * 2 * 2
+    g = ns.g
+    tc_rows = sum(n.len for n in ns.forest.nodes[1:] if len(n.query_set) * g >= 16)
+    kv_tc = tc_rows * ns.h_local * d * 2 * 2
     kernels = {}
     if "tc" in phases:
-        fl = sum(n.len * len(n.query_set) for n in forest.nodes[1:] if len(n.query_set) * g >= 16) * hq_local * 4 * d
-        # timed inside the long-running step: the sustained cuBLAS figure
-        kernels["tc"] = {"bound": "tensor", "achieved": fl / (phases["tc"] * 1e-3) / 1e12, "peak": tf_sus,
-                         "peak_figure": "bf16_tflops_sustained", "unit": "TFLOP/s", "ms": phases["tc"],
-                         "algorithmic_flops": fl, "kv_bytes": kv_tc}
-        kernels["tc"]["frac"] = kernels["tc"]["achieved"] / tf_sus
-        kernels["tc"]["frac_of_burst"] = kernels["tc"]["achieved"] / tf_burst
-        # the TC grid holds tc_sm_budget SMs; the others stream the suffixes
-        kernels["tc"]["sms"] = int(min(budget, sms))
-        kernels["tc"]["frac_per_sm"] = kernels["tc"]["frac"] * sms / max(1, min(budget, sms))
+        fl = sum(n.len * len(n.query_set) for n in ns.forest.nodes[1:] if len(n.query_set) * g >= 16) * hq_local * 4 * d
+        ach = fl / (phases["tc"] * 1e-3) / 1e12
+        sms_tc = int(min(budget, ns.sms))
+        # timed inside >= 2 s windows of back-to-back steps: the sustained
+        # cuBLAS figure; the burst figure and the SM share are reported beside it
+        kernels["tc"] = {"bound": "tensor", "achieved": ach, "peak": tf_sus, "peak_figure": "bf16_tflops_sustained",
+                         "unit": "TFLOP/s", "ms": phases["tc"], "algorithmic_flops": fl, "kv_bytes": kv_tc,
+                         "frac": ach / tf_sus, "frac_of_burst": ach / tf_burst, "sms": sms_tc,
+                         "sm_share": sms_tc / ns.sms,
+                         "note": "the TC grid holds `sms` SMs; the rest stream the suffixes concurrently"}
     if "gemv" in phases:
-        kb = work["unique_kv_bytes"] - kv_tc
+        kb = work_local["unique_kv_bytes"] - kv_tc
         kernels["gemv"] = {"bound": "hbm", "achieved": kb / (phases["gemv"] * 1e-3) / 1e9, "peak": hbm,
                            "unit": "GB/s", "ms": phases["gemv"], "algorithmic_bytes": kb}
         kernels["gemv"]["frac"] = kernels["gemv"]["achieved"] / hbm
     if "merge" in phases:
         kernels["merge"] = {"ms": phases["merge"]}
     # DRAM traffic per launch from the committed ncu --set full capture of
-    # this workload (profiles/ncu_summary.json, tools/ncu_summary.py)
+    # this workload at the benchmarked SM budget (profiles/ncu_summary.json)
     ncu = {}
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     if ncu_path.exists():
@@ -420,26 +535,33 @@ def main():
     for name in kernels:
         if name in ncu and "dram_bytes" in ncu[name]:
             kernels[name]["traffic"] = ncu[name]["dram_bytes"]
+            kernels[name]["traffic_budget"] = ncu.get("tc_sm_budget")
     dominant = max((k for k in kernels if "bound" in kernels[k]), key=lambda k: kernels[k]["ms"], default=None)
     roof = None
     if dominant:
         k = kernels[dominant]
         roof = {"bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"],
                 "frac": k["frac"], "traffic": k.get("traffic"), "kernel": dominant, "peak_kind": peak_kind,
-                "sms": k.get("sms"), "frac_per_sm": k.get("frac_per_sm")}
+                "peak_figure": k.get("peak_figure", "hbm_gbs"), "frac_of_burst": k.get("frac_of_burst"),
+                "sms": k.get("sms")}
 
     e2e = None
     if not args.quick:
-        # Serving-style pipeline through the public API: every step uploads
-        # its queries from pinned host memory and reads its output back;
-        # step k's copies run on their own streams, overlapping the compute
-        # of steps k - 1 / k + 1 (double-buffered device q / out).
+        # Serving-style pipeline through the public API (DecodeStep's
+        # captured graphs): every step uploads its queries from pinned host
+        # memory and reads its output back; step k's copies run on their
+        # own streams, overlapping the compute of steps k - 1 / k + 1
+        # (double-buffered device q / out, one captured graph per buffer
+        # set). Same >= 2 s median windows as `value`.
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         qbuf = [torch.empty_like(q_dev) for _ in range(2)]
         obuf = [torch.empty_like(out) for _ in range(2)]
-        ohost = [torch.empty((bs, hq_local, d), dtype=torch.float32).pin_memory() for _ in range(2)]
+        gbuf = [torch.empty_like(gathered) for _ in range(2)] if world > 1 else [None, None]
+        rows_out = full_bs if world > 1 else bs
+        ohost = [torch.empty((rows_out, (h_q if (world > 1 and not trees) else hq_local), d),
+                             dtype=torch.float32).pin_memory() for _ in range(2)]
+        replays = [step.capture(qbuf[i], kp, vp, obuf[i]) for i in range(2)] if not args.no_graph else None
         ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
-        gath2 = [torch.empty_like(gathered) for _ in range(2)] if world > 1 else None
         st8 = {"k": 0}
 
         def e2e_step():
@@ -454,10 +576,14 @@ def main():
             stream.wait_event(ev["h2d"][sl])
             if k >= 2:
                 stream.wait_event(ev["d2h"][sl])
-            step(qbuf[sl], kp, vp, out=obuf[sl], stream=stream)
+            if replays is not None:
+                replays[sl]()
+            else:
+                step(qbuf[sl], kp, vp, out=obuf[sl], stream=stream)
             res = obuf[sl]
             if world > 1:
-                dist.all_gather_into_tensor(gath2[sl], obuf[sl])
+                buf = gather(obuf[sl], gbuf[sl])
+                res = PL.scatter_requests(buf, ns.shards, full_bs) if trees else PL.assemble_heads(buf)
             ev["comp"][sl].record(stream)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev["comp"][sl])
@@ -477,57 +603,90 @@ def main():
             stream.wait_stream(s_d2h)
             e1.record(stream)
             torch.cuda.synchronize(dev)
-            ms = e0.elapsed_time(e1) / n
+            ms_w = e0.elapsed_time(e1) / n
             if world > 1:
-                t = torch.tensor([ms], device=dev)
+                t = torch.tensor([ms_w], device=dev)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = float(t.item())
-            return ms
+                ms_w = float(t.item())
+            return ms_w
 
         e2e_window(3)
-        e2e_ms = statistics.median(e2e_window(args.steps) for _ in range(5))
+        wins, t0 = [], time.perf_counter()
+        while time.perf_counter() - t0 < win_s or not wins:
+            wins.append(e2e_window(args.steps))
+        e2e_ms = statistics.median(wins)
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "windows": len(wins),
                "h2d_bytes_per_step": q_host.numel() * q_host.element_size(),
                "d2h_bytes_per_step": ohost[0].numel() * ohost[0].element_size(),
-               "pipeline": "per step: pinned H2D of q, decode step, D2H of out; copies on their own streams "
-                           "overlap the neighbouring steps' compute (double-buffered)"}
+               "pipeline": "per step: pinned H2D of q, decode step (graph replay), D2H of out; copies on their "
+                           "own streams overlap the neighbouring steps' compute (double-buffered); >= 2 s "
+                           "median windows like `value`"}
+
+    # untimed self-check of the benchmarked step's output
+    torch.cuda.synchronize(dev)
+    if replay is not None:
+        replay()
+    else:
+        step(q_dev, kp, vp, out=out)
+    res = gather(out, gathered)
+    torch.cuda.synchronize(dev)
+    check = verify(ns, out)
+    if world > 1:  # the gathered output holds this rank's rows unchanged
+        full_out = PL.scatter_requests(res, ns.shards, full_bs) if trees else PL.assemble_heads(res)
+        mine = full_out[list(ns.shard.requests)] if trees else full_out[:, ns.h0 * g:(ns.h0 + ns.h_local) * g]
+        check["gather_ok"] = bool(torch.equal(mine, out))
+        flag = torch.tensor([0 if (check["ok"] and check["gather_ok"]) else 1], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        check["all_ranks_ok"] = int(flag.item()) == 0
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.quick:
-        dt, kvb, desc = cpu_reference_sample(cfg)
-        cpu = {"value": kvb / dt / 1e9, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": desc, "seconds": dt}
+        r = ReferenceRunner(ns.cfg, m=m)
+        r.step()  # warm
+        dt = min(r.step() for _ in range(2))
+        cpu = {"value": r.bytes / dt / 1e9, "unit": "GB/s", "cores": r.workers, "kind": r.kind,
+               "sample": r.desc, "seconds": dt, "plan_seconds": r.plan_s}
 
     if rank == 0:
+        traffic = P.traffic_report(ns.full, element_size=2)
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "timed_windows": windows, "us_per_step": ms * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms, "timed_windows": windows, "us_per_step": ms * 1e3,
+            "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
-            "config": {"workload": cfg["label"], "bs": bs, "h_q": h_q, "h_kv": h_kv, "d": d,
-                       "kv_tokens": int(sum(spec.length[1:])), "nodes": int(spec.n_nodes - 1),
-                       "parallelism": f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+            "config": {"workload": ns.cfg["label"], "bs": full_bs, "h_q": h_q, "h_kv": ns.cfg["h_kv"], "d": d,
+                       "kv_tokens": int(sum(ns.spec.length[1:])), "nodes": int(ns.spec.n_nodes - 1),
+                       "parallelism": (f"tree partition x{world} + NCCL all-gather by request" if trees else
+                                       f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else "")),
                        "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
                        "planner": {"m_tc": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,
-                                   "truncated": plan.search_truncated, "ms": plan_ms},
+                                   "truncated": plan.search_truncated, "ms": ns.plan_ms},
                        "launch": "CUDA graph replay of the step" if replay is not None else "direct launches",
                        "suffix_kernel": "mma.sync, early launch on the SMs the TC grid leaves (PDL)",
-                       "tc_sm_budget": step.tc_sm_budget, "tc_ctas": step.info.n_tc_blocks * h_local,
-                       "autotune_ms": tune_ms},
+                       "tc_sm_budget": step.tc_sm_budget, "tc_ctas": step.info.n_tc_blocks * 2,
+                       "autotune_ms": ns.tune_ms},
             "roofline": roof,
             "hbm_roofline_step": {"achieved": value / world, "peak": hbm, "unit": "GB/s",
                                   "frac": value / world / hbm, "frac_of_8tbs": value / world / 8000.0},
             "kernels": kernels,
             "kernels_window_ms_per_step": ms_ev,
-            "work": work,
+            "work": work_full,
+            "flashdecoding_bytes": {"bytes_baseline": traffic.bytes_baseline, "bytes_unique": total_bytes,
+                                    "reduction": traffic.bytes_baseline / total_bytes,
+                                    "dram_bytes_ncu": ncu.get("step_dram_bytes")},
+            "verified": check,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": step.launches * args.steps,
+            "gpu_launches": step.launches * args.steps * windows,
             "clocks": clock_rec,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if not check["ok"] or not check.get("all_ranks_ok", True):
+        raise SystemExit(f"bench output failed its self-check: {check}")
 
 
 if __name__ == "__main__":

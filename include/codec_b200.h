@@ -3,11 +3,14 @@
  * path (CoDec, arXiv 2505.17694).
  *
  * Plain C types only: pointers, sizes, PODs. No torch / C++ types cross
- * this boundary. Every function is reentrant (no global mutable state;
- * the last-error string is thread-local) and every device entry point is
- * asynchronous on the caller's stream (passed as `void*`, a cudaStream_t).
- * Ownership: the caller owns every buffer; host-side handles
- * (codec_index, codec_plan, codec_table) are created and freed here.
+ * this boundary. Every product entry point is reentrant: handles
+ * (codec_index, codec_plan, codec_table, codec_kernel_timer) carry all
+ * state, the last-error string is thread-local, and every device entry
+ * point is asynchronous on the caller's stream (passed as `void*`, a
+ * cudaStream_t). The only process-global buffers belong to the debug
+ * flags CODEC_FLAG_TRACE / CODEC_FLAG_CTALOG (timelines for tools/).
+ * Ownership: the caller owns every buffer; host-side handles are created
+ * and freed here.
  *
  * Each entry point names the reference interface it replaces
  * (/root/reference/pkg/src/prefixdec/<file>:<line>).  Status codes map
@@ -207,7 +210,6 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_FUSED_MERGE  4096 /* the mma.sync suffix kernel folds each request's TC partials into its output
                                         instead of the merge kernel (opt-in: slower on cfg2 so far) */
 #define CODEC_FLAG_DBG_NO_TC_UNITS 8192 /* TC kernel skips its shared-node units: timing only, wrong output (debug) */
-#define CODEC_FLAG_KERNEL_EVENTS 16384 /* record CUDA events around each kernel (codec_kernel_times; profiling) */
 #define CODEC_FLAG_DBG_NO_LOADS 32768 /* TC producers skip the K/V TMA loads: timing only, wrong output (debug) */
 #define CODEC_FLAG_DBG_ISSUER_ONLY 131072 /* TC kernel runs only its MMA issuer, no waits: timing only (debug) */
 #define CODEC_FLAG_MERGE_NO_PDL 262144 /* launch the merge plainly after the suffix kernel (measurement) */
@@ -248,22 +250,36 @@ CODEC_API int32_t codec_table_copy(const codec_table* t, int32_t* blob);
  *   k, v   [h_local][pool_tokens][d]     head-major node pool, nodes at
  *                                        their preorder offsets (kappa)
  *   out    [bs][h_q_local][d]            float32 for BF16/F32, float64 for F64
- *   workspace  >= info.workspace_bytes, 256-byte aligned: partial (o, m, l)
- *              storage, then a tail whose first int32 is the step's TC
- *              completion counter (reset and used inside each call; a
- *              workspace must not be shared by calls in flight)
- * All device pointers; asynchronous on `stream`.
+ *   workspace, workspace_bytes
+ *          >= info.workspace_bytes (checked), 256-byte aligned: partial
+ *          (o, m, l) storage, then a tail whose first int32 is the step's
+ *          TC completion counter (reset and used inside each call; a
+ *          workspace must not be shared by calls in flight)
+ * All device pointers; asynchronous on `stream`. Every check runs before
+ * the first enqueue: a non-OK status leaves stream, output and workspace
+ * untouched.
  * ==================================================================== */
-/* Same step with the GEMV / generic kernels forked onto `aux_stream`
+/* Per-kernel device times of the calls made with this timer (profiling):
+ * CUDA events around each kernel on the launching stream. One ring of up
+ * to 4096 calls per handle; a handle must not be shared across threads. */
+typedef struct codec_kernel_timer codec_kernel_timer;
+CODEC_API int32_t codec_timer_create(codec_kernel_timer** out);
+CODEC_API void codec_timer_free(codec_kernel_timer* timer);
+/* ms[3 i + k] = call i's TC kernel, suffix + generic kernels, merge kernel.
+ * Synchronizes on the recorded events, then clears the ring. */
+CODEC_API int32_t codec_timer_read(codec_kernel_timer* timer, float* ms, int32_t max_calls, int32_t* n_calls);
+
+/* The step with the GEMV / generic kernels forked onto `aux_stream`
  * (event fork/join on `stream`) so they run concurrently with the
- * tensor-core kernel; aux_stream NULL == codec_decode_attention. */
+ * tensor-core kernel; aux_stream NULL: one stream. timer NULL: no events
+ * (a timer also serialises the kernels: the events sit between them). */
 CODEC_API int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
                                             const int32_t* table_dev, const void* q, const void* k,
-                                            const void* v, void* out, void* workspace, void* stream,
-                                            void* aux_stream);
+                                            const void* v, void* out, void* workspace, int64_t workspace_bytes,
+                                            void* stream, void* aux_stream, codec_kernel_timer* timer);
 CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
-                               const int32_t* table_dev, const void* q, const void* k,
-                               const void* v, void* out, void* workspace, void* stream);
+                                         const int32_t* table_dev, const void* q, const void* k, const void* v,
+                                         void* out, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Debug builds only (compiled with -DCODEC_HANG_CHECK): a device pointer to
  * host-mapped int32[8 + 8 * 1000]; a TC-kernel mbarrier wait that spins for
@@ -280,12 +296,6 @@ CODEC_API int32_t codec_debug_trace(long long* host, int64_t n);
    TC CTAs at records [0, 4096), GEMV CTAs (blockIdx.y * gridDim.x +
    blockIdx.x) from record 4096 (debug). */
 CODEC_API int32_t codec_debug_ctalog(long long* host, int64_t n);
-/* Per-kernel device times of the calls made with CODEC_FLAG_KERNEL_EVENTS
-   since the last read (profiling; process-global, not reentrant): ms[3 i
-   + k] = call i's TC kernel, suffix + generic kernels, merge kernel.
-   Synchronizes on the recorded events, then clears the ring. */
-CODEC_API int32_t codec_kernel_times(float* ms, int32_t max_calls, int32_t* n_calls);
-
 /* ======================================================================
  * Device primitives with the reference's argument meaning.
  * ==================================================================== */

@@ -99,11 +99,13 @@ _SIGS = {
     "codec_table_info_get": (I32, [P, C.POINTER(TableInfo)]),
     "codec_table_copy": (I32, [P, PI32]),
     "codec_page_layout": (I32, [P, I32, PI64, PI64]),
-    "codec_decode_attention": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P]),
-    "codec_decode_attention_ex": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, P, P]),
+    "codec_decode_attention": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, I64, P]),
+    "codec_decode_attention_ex": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, P, I64, P, P, P]),
+    "codec_timer_create": (I32, [C.POINTER(P)]),
+    "codec_timer_free": (None, [P]),
+    "codec_timer_read": (I32, [P, P, I32, P]),
     "codec_debug_trace": (I32, [P, I64]),
     "codec_debug_ctalog": (I32, [P, I64]),
-    "codec_kernel_times": (I32, [P, I32, P]),
     "codec_debug_hang_buffer": (I32, [P]),
     "codec_pac": (I32, [I32, P, P, P, P, I64, I64, I64, I64, I64, F64, P, P, P, P]),
     "codec_por": (I32, [I32, I64, I64, P, P, P, P, P, P, P, P, P, P]),

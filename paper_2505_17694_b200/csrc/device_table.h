@@ -21,6 +21,7 @@ constexpr int kGrpMaxVis = 4;   // most visible tokens of any row (kernels size 
 constexpr int kGrpNode = 5;     // GEMV / generic: forest node (diagnostics)
 constexpr int kGrpQReq0 = 5;    // TC pieces: first request of a consecutive request run (Q by TMA), else -1
 constexpr int kGrpBlock = 6;    // TC: schedule block (CTA pair) of the unit
+constexpr int kGrpStart = 6;    // GEMV / generic: slice start within the node (host-side growth)
 constexpr int kGrpHead = 7;     // TC: local kv head of the unit
 
 // a row record: 4 int32 -- request, visible tokens within the slice,

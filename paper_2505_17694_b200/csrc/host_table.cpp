@@ -176,15 +176,18 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   // ---- kernel eligibility
   const bool tc_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && is_pow2(g) && g <= 128 &&
                      !(dims->flags & CODEC_FLAG_NO_TC);
+  // (the GEMV kernels are instantiated for 4 and 8 query-head rows; more
+  // query heads per kv head take the generic kernel)
   const bool gemv_ok = (dims->kv_dtype == CODEC_BF16 || dims->kv_dtype == CODEC_F32) &&
-                       (d == 64 || d == 128 || d == 256) && g <= 16 && !(dims->flags & CODEC_FLAG_NO_GEMV);
+                       (d == 64 || d == 128 || d == 256) && g <= 8 && !(dims->flags & CODEC_FLAG_NO_GEMV);
   const int32_t tc_reqs = tc_ok ? std::max(1, kTcGroupRows / g) : 0;
-  const int32_t gemv_rows = g <= 4 ? 4 : (g <= 8 ? 8 : 16);
+  const int32_t gemv_rows = g <= 4 ? 4 : 8;
 
   // ---- rows and slots
   struct Grp {
     int32_t kind, kv_tok, len, row_begin, n_rows, max_vis, node;
     int64_t order_len;
+    int32_t start;  // slice start within the node (DecodeStep.grow)
   };
   std::vector<Grp> groups;
   std::vector<int32_t> rows;  // 4 per row: req, vis_local, slot, fused merge entry (GEMV rows) or -1
@@ -228,7 +231,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       int32_t max_vis = 0;
       for (size_t i = a; i < b; ++i) max_vis = std::max(max_vis, live[i].second);
       Grp gr{kind, (int32_t)(off[n] + start), (int32_t)(stop - start), (int32_t)(rows.size() / 4),
-             (int32_t)(b - a), max_vis, (int32_t)n, stop - start};
+             (int32_t)(b - a), max_vis, (int32_t)n, stop - start, (int32_t)start};
       for (size_t i = a; i < b; ++i) {
         int32_t r = live[i].first;
         int64_t pp = path_pos(r, n);
@@ -457,7 +460,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     count = 0;
     for (auto& gr : groups)
       if (gr.kind == kind) {
-        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, 0, 0};
+        int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, gr.start, 0};
         blob.insert(blob.end(), rec, rec + kGroupInts);
         ++count;
       }

@@ -29,10 +29,14 @@ __device__ __forceinline__ void wait_tc_done(const int32_t* tc_done, int tc_ctas
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!tc_done) return;
   if (threadIdx.x == 0) {
+    // bounded: the TC grid is resident and finishing (it was launched
+    // before this kernel); a count that never arrives is a bug, and a trap
+    // beats a hung GPU (~4 s of polling)
     int v;
-    while (true) {
+    for (int it = 0;; ++it) {
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(tc_done) : "memory");
       if (v >= tc_ctas) break;
+      if (it > (1 << 24)) __trap();
       __nanosleep(256);
     }
   }

@@ -63,36 +63,53 @@ namespace {
 long long* g_ctalog = nullptr;  // debug CTA log (CODEC_FLAG_CTALOG), one per process
 }
 
-// Profiling (CODEC_FLAG_KERNEL_EVENTS): CUDA events around each kernel of a
-// call on the caller's stream, so a benchmark can time every kernel inside
-// its own timed region. Process-global ring; not for concurrent callers.
-constexpr int kEvCalls = 512;
-struct KernelEvents {
+// Per-kernel timing (codec_kernel_timer, ABI v4): CUDA events around each
+// kernel of a call on the caller's stream, so a benchmark can time every
+// kernel inside its own timed region. One ring per handle -- nothing
+// process-global on this path; a handle must not be shared by threads.
+constexpr int kEvCalls = 4096;
+struct codec_kernel_timer {
   cudaEvent_t ev[kEvCalls][4] = {};
   int n = 0;
 };
-KernelEvents g_kev;
-int32_t kev_record(int slot, cudaStream_t st) {
-  if (g_kev.n >= kEvCalls) return CODEC_OK;  // ring full: drop
-  cudaEvent_t& e = g_kev.ev[g_kev.n][slot];
+
+namespace {
+int32_t kev_record(codec_kernel_timer* tm, int slot, cudaStream_t st) {
+  if (tm->n >= kEvCalls) return CODEC_OK;  // ring full: drop
+  cudaEvent_t& e = tm->ev[tm->n][slot];
   if (!e && cudaEventCreate(&e) != cudaSuccess) return fail(CODEC_ERR_CUDA, "event create");
   if (cudaEventRecord(e, st) != cudaSuccess) return fail(CODEC_ERR_CUDA, "event record");
   return CODEC_OK;
 }
+}  // namespace
 
-extern "C" int32_t codec_kernel_times(float* ms, int32_t max_calls, int32_t* n_calls) {
-  if (!ms || !n_calls) return fail(CODEC_ERR_VALUE, "NULL argument");
-  const int n = g_kev.n < max_calls ? g_kev.n : max_calls;
+extern "C" int32_t codec_timer_create(codec_kernel_timer** out) {
+  if (!out) return fail(CODEC_ERR_VALUE, "NULL argument");
+  *out = new codec_kernel_timer();
+  return CODEC_OK;
+}
+
+extern "C" void codec_timer_free(codec_kernel_timer* tm) {
+  if (!tm) return;
+  for (auto& call : tm->ev)
+    for (auto& e : call)
+      if (e) cudaEventDestroy(e);
+  delete tm;
+}
+
+extern "C" int32_t codec_timer_read(codec_kernel_timer* tm, float* ms, int32_t max_calls, int32_t* n_calls) {
+  if (!tm || !ms || !n_calls) return fail(CODEC_ERR_VALUE, "NULL argument");
+  const int n = tm->n < max_calls ? tm->n : max_calls;
   for (int i = 0; i < n; ++i)
     for (int k = 0; k < 3; ++k) {
       float t = 0.f;
-      if (cudaEventSynchronize(g_kev.ev[i][k + 1]) != cudaSuccess ||
-          cudaEventElapsedTime(&t, g_kev.ev[i][k], g_kev.ev[i][k + 1]) != cudaSuccess)
+      if (cudaEventSynchronize(tm->ev[i][k + 1]) != cudaSuccess ||
+          cudaEventElapsedTime(&t, tm->ev[i][k], tm->ev[i][k + 1]) != cudaSuccess)
         return fail(CODEC_ERR_CUDA, "event read");
       ms[3 * i + k] = t;
     }
   *n_calls = n;
-  g_kev.n = 0;
+  tm->n = 0;
   return CODEC_OK;
 }
 
@@ -104,13 +121,23 @@ extern "C" int32_t codec_debug_ctalog(long long* host, int64_t n) {
 
 extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
                                              const int32_t* table_dev, const void* q, const void* k, const void* v,
-                                             void* out, void* workspace, void* stream, void* aux_stream) {
+                                             void* out, void* workspace, int64_t workspace_bytes, void* stream,
+                                             void* aux_stream, codec_kernel_timer* timer) {
+  // ---- every argument / eligibility check before the first enqueue: an
+  // error leaves the stream, the output and the workspace untouched
   if (!dims || !info || !table_dev) return fail(CODEC_ERR_VALUE, "NULL argument");
+  if (!q || !k || !v || !out || !workspace) return fail(CODEC_ERR_VALUE, "NULL device buffer");
+  if (workspace_bytes < info->workspace_bytes)
+    return fail(CODEC_ERR_VALUE, "workspace of %lld bytes, the table needs %lld", (long long)workspace_bytes,
+                (long long)info->workspace_bytes);
   if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
     return fail(CODEC_ERR_VALUE, "workspace must be 256-byte aligned");
   if ((reinterpret_cast<uintptr_t>(k) & 15) || (reinterpret_cast<uintptr_t>(v) & 15) ||
       (reinterpret_cast<uintptr_t>(q) & 15))
     return fail(CODEC_ERR_VALUE, "q, k and v must be 16-byte aligned");
+  if (dims->h_kv < 1 || dims->h_q % dims->h_kv != 0 || info->h_local != dims->head_end - dims->head_begin)
+    return fail(CODEC_ERR_DIMENSION_MISMATCH, "dims do not match the table (h_q %d, h_kv %d, shard [%d, %d), "
+                "table heads %d)", dims->h_q, dims->h_kv, dims->head_begin, dims->head_end, info->h_local);
   cudaStream_t st = (cudaStream_t)stream;
   const int g = dims->h_q / dims->h_kv;
   int page_shift = 0;
@@ -128,6 +155,8 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool do_tc = info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC);
   const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
   const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
+  if (do_tc && (dims->kv_dtype != CODEC_BF16 || d != 128))
+    return fail(CODEC_ERR_UNSUPPORTED, "tensor-core groups need bf16, d = 128");
   // The mma.sync suffix kernel is launched right after the TC kernel on the
   // same stream with programmatic dependent launch: its CTAs start on the
   // SMs the TC grid leaves once every TC CTA is resident (the TC grid gets
@@ -140,23 +169,31 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   // merge.
   const bool mma_gemv = do_gemv && dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & CODEC_FLAG_GEMV_SIMT);
+  if (do_gemv && !mma_gemv && page_shift)
+    return fail(CODEC_ERR_UNSUPPORTED, "paged KV: suffix groups need the mma.sync kernel (bf16, d = 128, g <= 8)");
+  if (do_gemv && !mma_gemv && info->gemv_rows != 4 && info->gemv_rows != 8)
+    return fail(CODEC_ERR_UNSUPPORTED, "GEMV kernel: %d query-head rows per group", info->gemv_rows);
+  if (do_gen && page_shift) return fail(CODEC_ERR_UNSUPPORTED, "paged KV: no generic-kernel groups");
+  if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
   const bool fork = aux_stream != nullptr && do_tc && ((do_gemv && !mma_gemv) || do_gen);
   cudaStream_t side = fork ? (cudaStream_t)aux_stream : st;
   long long* ctalog = nullptr;
-  if (dims->flags & CODEC_FLAG_CTALOG) {
+  if (dims->flags & CODEC_FLAG_CTALOG) {  // debug builds of a timeline: one process-global buffer
     if (!g_ctalog && cudaMalloc(&g_ctalog, 4 * sizeof(long long) * kCtaLogLen) != cudaSuccess)
       return fail(CODEC_ERR_CUDA, "ctalog alloc");
-    if (cudaMemsetAsync(g_ctalog, 0, 4 * sizeof(long long) * kCtaLogLen, st) != cudaSuccess)
-      return fail(CODEC_ERR_CUDA, "ctalog clear");
     ctalog = g_ctalog;
   }
   ForkJoin* fj = nullptr;
+  if (fork) CODEC_TRY(fork_join_events(fj));
+  const bool kev = timer != nullptr && !fork;
+
+  // ---- enqueue
+  if (ctalog && cudaMemsetAsync(g_ctalog, 0, 4 * sizeof(long long) * kCtaLogLen, st) != cudaSuccess)
+    return fail(CODEC_ERR_CUDA, "ctalog clear");
   if (fork) {
-    CODEC_TRY(fork_join_events(fj));
     if (cudaEventRecord(fj->fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fj->fork, 0) != cudaSuccess)
       return fail(CODEC_ERR_CUDA, "fork failed");
   }
-  const bool kev = (dims->flags & CODEC_FLAG_KERNEL_EVENTS) && !fork;
   // TC completion counter: the first word of the workspace's reserved tail
   int64_t ml_bytes = (int64_t)info->n_slots * hq_local * 2 * elem;
   ml_bytes = (ml_bytes + 255) / 256 * 256;
@@ -164,23 +201,20 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool pdl = mma_gemv && do_tc && info->n_merge_fused == 0 && !kev;
   if (do_tc && cudaMemsetAsync(tc_done, 0, sizeof(int32_t), st) != cudaSuccess)
     return fail(CODEC_ERR_CUDA, "tc counter reset");
-  if (kev) CODEC_TRY(kev_record(0, st));
+  if (kev) CODEC_TRY(kev_record(timer, 0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
                         dims->flags, ctalog, dims->page_table, page_shift, tc_done));
-  if (kev) CODEC_TRY(kev_record(1, st));
+  if (kev) CODEC_TRY(kev_record(timer, 1, st));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
                               info->off_merge_slot, st, ctalog, pdl, dims->page_table, page_shift));
-  else if (do_gemv && page_shift)
-    return fail(CODEC_ERR_UNSUPPORTED, "paged KV: suffix groups need the mma.sync kernel (bf16, d = 128, g <= 8)");
   else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
                           ctalog));
-  if (kev) CODEC_TRY(kev_record(2, st));
-  if (do_gen && page_shift) return fail(CODEC_ERR_UNSUPPORTED, "paged KV: no generic-kernel groups");
+  if (kev) CODEC_TRY(kev_record(timer, 2, st));
   if (do_gen)
     CODEC_TRY(launch_generic_groups(dims->kv_dtype, table_dev, info->n_gen_groups, info->off_gen, info->off_rows, q,
                                     k, v, dims->pool_tokens, d, g, hq_local, out, part_o, part_ml, side));
@@ -194,16 +228,17 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
                            mma_gemv && !fork && !kev && !(dims->flags & CODEC_FLAG_SKIP_GEMV) &&
                                !(dims->flags & CODEC_FLAG_MERGE_NO_PDL)));
   if (kev) {
-    CODEC_TRY(kev_record(3, st));
-    ++g_kev.n;
+    CODEC_TRY(kev_record(timer, 3, st));
+    ++timer->n;
   }
   return CODEC_OK;
 }
 
 extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
                                           const int32_t* table_dev, const void* q, const void* k, const void* v,
-                                          void* out, void* workspace, void* stream) {
-  return codec_decode_attention_ex(dims, info, table_dev, q, k, v, out, workspace, stream, nullptr);
+                                          void* out, void* workspace, int64_t workspace_bytes, void* stream) {
+  return codec_decode_attention_ex(dims, info, table_dev, q, k, v, out, workspace, workspace_bytes, stream, nullptr,
+                                   nullptr);
 }
 
 extern "C" int32_t codec_debug_trace(long long* host, int64_t n) { return read_trace(host, n); }

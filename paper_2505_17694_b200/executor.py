@@ -73,7 +73,7 @@ class DecodeStep:
 
     def __init__(self, forest: Forest, plan, h_q: int, dtype="bfloat16", head_begin=0, head_end=None,
                  device="cuda", flags=0, tc_sm_budget=0, concurrent=True, page_size=0, page_table=None,
-                 pool_tokens=None):
+                 pool_tokens=None, timer=False):
         import torch
 
         self.forest = forest
@@ -118,7 +118,47 @@ class DecodeStep:
         # launch; the merge waits on it)
         self.workspace = torch.zeros(max(int(self.info.workspace_bytes), 256), dtype=torch.uint8, device=self.device)
         self.out_dtype = torch.float64 if self.tdtype == torch.float64 else torch.float32
-        self.hq_local = (self.head_end - self.head_begin) * self.g
+        self.h_local = self.head_end - self.head_begin
+        self.hq_local = self.h_local * self.g
+        self._graphs = []
+        self._grown = 0
+        # per-kernel CUDA-event timer (profiling); it serialises the kernels
+        self._timer = None
+        if timer:
+            h = C.c_void_p()
+            _lib.check(_lib.lib().codec_timer_create(C.byref(h)))
+            self._timer = h
+
+    def __del__(self):
+        if getattr(self, "_timer", None):
+            try:
+                _lib.lib().codec_timer_free(self._timer)
+            except Exception:
+                pass
+            self._timer = None
+
+    def kernel_times(self):
+        """[calls, 3] ms of the (TC, suffix, merge) kernels of every call
+        since the last read (needs timer=True)."""
+        if not self._timer:
+            raise ValueError("DecodeStep built without timer=True")
+        buf = (C.c_float * (3 * 4096))()
+        n = C.c_int32()
+        _lib.check(_lib.lib().codec_timer_read(self._timer, buf, 4096, C.byref(n)))
+        return np.array(buf[:3 * n.value], dtype=np.float64).reshape(-1, 3)
+
+    def _check(self, name, t, shape, dtype):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch tensor on {self.device}")
+        if t.device != self.device and not (self.device.index is None and t.device.type == self.device.type):
+            raise ValueError(f"{name} is on {t.device}, the step on {self.device}")
+        if t.dtype != dtype:
+            raise DimensionMismatch(f"{name} is {t.dtype}, the step computes in {dtype}")
+        if tuple(t.shape) != tuple(shape):
+            raise DimensionMismatch(f"{name} has shape {tuple(t.shape)}, the step needs {tuple(shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
 
     @property
     def launches(self) -> int:
@@ -127,16 +167,26 @@ class DecodeStep:
         return int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) + int(bool(i.n_merge))
 
     def __call__(self, q, k_pool, v_pool, out=None, stream=None):
+        """q [bs, h_q_local, d] and the pools [h_local, pool_tokens, d] in
+        the step's dtype on its device (checked: the kernels get raw
+        pointers); returns / fills out [bs, h_q_local, d]."""
         import torch
 
+        bs = self.forest.bs
+        self._check("q", q, (bs, self.hq_local, self.d), self.tdtype)
+        pool_shape = (self.h_local, self.pool_tokens, self.d)
+        self._check("k_pool", k_pool, pool_shape, self.tdtype)
+        self._check("v_pool", v_pool, pool_shape, self.tdtype)
         if out is None:
-            out = torch.empty((self.forest.bs, self.hq_local, self.d), dtype=self.out_dtype, device=self.device)
+            out = torch.empty((bs, self.hq_local, self.d), dtype=self.out_dtype, device=self.device)
+        else:
+            self._check("out", out, (bs, self.hq_local, self.d), self.out_dtype)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         _lib.check(_lib.lib().codec_decode_attention_ex(
             C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
             C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(out.data_ptr()),
-            C.c_void_p(self.workspace.data_ptr()), C.c_void_p(st.cuda_stream),
-            C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None))
+            C.c_void_p(self.workspace.data_ptr()), self.workspace.numel(), C.c_void_p(st.cuda_stream),
+            C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None, self._timer))
         return out
 
     def capture(self, q, k_pool, v_pool, out):
@@ -157,53 +207,56 @@ class DecodeStep:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=s):
             self(q, k_pool, v_pool, out=out, stream=s)
-        self._graph = graph  # keep alive with the step
+        self._graphs.append(graph)  # keep alive with the step (one per captured buffer set)
         return graph.replay
 
     def grow(self, delta: int = 1) -> None:
         """Decode-step growth between re-plans (the
-        reference re-plans every DEFAULT_REPLAN_EVERY steps, scheduler.py:23).
-        Build the forest with spare leaf capacity (leaf length > visible_len),
-        write each request's new token K/V into the pool at
-        token_offset[leaf] + visible, then call grow(): every request's leaf
-        sees `delta` more tokens. Only the suffix groups' row records change,
-        in place in the device table, so a captured graph replays the grown
-        step unchanged; shared nodes are untouched. The forest object (and
-        its index) keep the visible counts they were built with -- the next
-        re-plan builds a new forest. Raises ValueError when a leaf has no
-        room left (re-plan with new capacity)."""
+        reference re-plans every DEFAULT_REPLAN_EVERY steps, scheduler.py:23;
+        PlanCache below drives that cadence). Build the forest with spare
+        leaf capacity (leaf length > visible_len), write each request's new
+        token K/V into the pool at the leaf's next token, then call grow():
+        every request's leaf sees `delta` more tokens. Only the suffix
+        groups' row records change, in place in the device table, so a
+        captured graph replays the grown step unchanged; shared nodes are
+        untouched. The forest's visible counts (and its index) are updated
+        to match. Works for contiguous and paged pools (the group records
+        carry their slice start within the node). Raises ValueError when a
+        leaf has no room left (re-plan with new capacity)."""
         import torch
 
         i, blob = self.info, self.blob_host
-        extra = getattr(self, "_grown", 0)
         leaf = {n.id for n in self.forest.nodes[1:] if not self.forest.children[n.id]}
-        touched = []
+        touched, grown = [], {}
         for off, count in ((i.off_gemv, i.n_gemv_groups), (i.off_gen, i.n_gen_groups)):
             for gidx in range(count):
                 rec = off + 8 * gidx
                 node = int(blob[rec + 5])
                 if node not in leaf:
                     continue
-                start_tok = int(blob[rec]) - self.forest.token_offset[node]  # slice start within the node
+                start_tok = int(blob[rec + 6])  # slice start within the node
                 for k in range(int(blob[rec + 3])):
                     r = i.off_rows + 4 * (int(blob[rec + 2]) + k)
-                    vis = int(blob[r + 1])
-                    if start_tok + vis != self.forest.visible_count(node, int(blob[r])) + extra:
+                    req, vis = int(blob[r]), int(blob[r + 1])
+                    if start_tok + vis != self.forest.visible_count(node, req):
                         continue  # not the request's last slice of this leaf
                     if vis + delta > int(blob[rec + 1]):
                         raise ValueError(f"leaf {node} has no room for {delta} more tokens: re-plan")
                     blob[r + 1] = vis + delta
                     blob[rec + 4] = max(int(blob[rec + 4]), vis + delta)
                     touched += [r + 1, rec + 4]
-        self._grown = extra + delta
+                    grown[(node, req)] = start_tok + vis + delta
+        self._grown += delta
+        if grown:
+            self.forest.set_visible(grown)
         if touched:
             lo, hi = min(touched), max(touched) + 1
             self.table[lo:hi].copy_(torch.from_numpy(blob[lo:hi]))
 
-    def with_budget(self, tc_sm_budget: int) -> "DecodeStep":
-        return DecodeStep(self.forest, self.plan, self.h_q, self.tdtype, self.head_begin, self.head_end,
-                          self.device, self.flags, tc_sm_budget, self.aux is not None, self.page_size,
-                          self.page_table, self.pool_tokens)
+    def with_budget(self, tc_sm_budget: int, plan=None, flags=None, timer=False) -> "DecodeStep":
+        return DecodeStep(self.forest, self.plan if plan is None else plan, self.h_q, self.tdtype, self.head_begin,
+                          self.head_end, self.device, self.flags if flags is None else flags, tc_sm_budget,
+                          self.aux is not None, self.page_size, self.page_table, self.pool_tokens, timer)
 
 
 def autotune_step(step: DecodeStep, q, k_pool, v_pool, budgets=None, iters=10):
@@ -257,14 +310,74 @@ def execute(forest: Forest, queries: QueryBatch, plan, pool: BlockPool | None = 
     q = queries.queries
     qdt = str(q.dtype).replace("torch.", "")
     tdt = torch_dtype(qdt if qdt in ("float32", "float64", "bfloat16") else "float64")
-    key = ("step", id(plan), str(tdt), flags)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = ("step", id(plan), str(tdt), int(flags), queries.h_q, str(dev))
     cache = forest._pools.setdefault("_steps", {})
     step = cache.get(key)
     if step is None or step[0] is not plan:
-        step = (plan, DecodeStep(forest, plan, queries.h_q, tdt, flags=flags))
+        step = (plan, DecodeStep(forest, plan, queries.h_q, tdt, flags=flags, device=dev))
         cache[key] = step
+        while len(cache) > 4:  # bounded: each step holds its table and workspace
+            cache.pop(next(iter(cache)))
     step = step[1]
     kp, vp = forest.device_pool(tdt)
     qd = (q if isinstance(q, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(q)))
     qd = qd.to(device=step.device, dtype=tdt).contiguous()
     return step(qd, kp, vp)
+
+
+class PlanCache:
+    """Plan reuse across decode steps: the plan
+    and its device table are rebuilt every `replan_every` decode steps
+    (DEFAULT_REPLAN_EVERY = 4, scheduler.py:23) or when the
+    forest changes; in between, `advance()` grows every request's leaf by
+    one token in place (DecodeStep.grow), so a captured graph keeps
+    replaying. `planner(forest)` returns the DivisionPlan (default: the
+    device plan over the profile `table`)."""
+
+    def __init__(self, h_q: int, table=None, replan_every: int | None = None, planner=None, **step_kw):
+        from .scheduler import DEFAULT_REPLAN_EVERY
+        self.h_q = int(h_q)
+        self.replan_every = int(replan_every or DEFAULT_REPLAN_EVERY)
+        if self.replan_every < 1:
+            raise ValueError(f"replan_every must be >= 1, got {self.replan_every}")
+        self.table = table
+        self.planner = planner
+        self.step_kw = step_kw
+        self.step = None
+        self.age = 0        # decode steps served by the current plan
+        self.replans = 0
+
+    def _plan(self, forest):
+        if self.planner is not None:
+            return self.planner(forest)
+        from .cost_model import load_default_profile
+        from .scheduler import plan_device
+        table = self.table if self.table is not None else load_default_profile()
+        h_kv = forest.h_kv
+        lo = self.step_kw.get("head_begin", 0)
+        hi = self.step_kw.get("head_end", h_kv) or h_kv
+        return plan_device(forest, self.h_q // h_kv, table, hi - lo, tc_sm_budget=self.step_kw.get("tc_sm_budget", 0))
+
+    def get(self, forest) -> DecodeStep:
+        """The step for this decode step: the cached one while the plan is
+        young and the forest unchanged, else a re-plan."""
+        if self.step is None or self.step.forest is not forest or self.age >= self.replan_every:
+            self.step = DecodeStep(forest, self._plan(forest), self.h_q, **self.step_kw)
+            self.age = 0
+            self.replans += 1
+        return self.step
+
+    def advance(self, delta: int = 1) -> None:
+        """After a decode step: every request gained `delta` tokens in its
+        leaf (already written to the pool)."""
+        if self.step is None:
+            raise ValueError("no step yet: call get(forest) first")
+        self.age += 1
+        if self.age < self.replan_every:
+            self.step.grow(delta)
+        else:
+            # re-plan at the next get(): the forest carries the grown counts
+            self.step.forest.set_visible(
+                {(n, r): self.step.forest.visible_count(n, r) + delta
+                 for r, p in enumerate(self.step.forest.paths) for n in p[-1:]})

@@ -202,6 +202,25 @@ class Forest:
         self._pools[key] = (kp, vp)
         return kp, vp
 
+    def set_visible(self, updates: dict) -> None:
+        """Set visible_len[request] of nodes ({(node, request): count}, each
+        count in 1..len) -- decode-step growth of partially filled leaves --
+        and rebuild the integer index to match."""
+        for (nid, rid), cnt in updates.items():
+            node = self.node(nid)
+            if rid not in node.query_set:
+                raise UnknownRequest(f"request {rid} does not run through node {nid}")
+            if not 1 <= cnt <= node.len:
+                raise ValueError(f"node {nid} visible_len[{rid}]={cnt} outside 1..{node.len}")
+            if node.visible_len is None:
+                node.visible_len = {}
+            node.visible_len[rid] = int(cnt)
+        old = self._index
+        self._index = _index_build([n.parent for n in self.nodes], [n.len for n in self.nodes], self.paths,
+                                   [n.visible_len if n.id else None for n in self.nodes], self.bs)[0]
+        if old:
+            _lib.lib().codec_index_free(old)
+
     def adopt_pool(self, k_pool, v_pool, head_begin=0, head_end=None):
         head_end = self.h_kv if head_end is None else head_end
         key = (str(k_pool.dtype), str(k_pool.device), head_begin, head_end)

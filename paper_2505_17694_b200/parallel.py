@@ -1,25 +1,31 @@
 """Multi-GPU partitioning of the decode-attention step.
 
 Attention is independent per kv head (a query head h reads kv head h // g,
-attention.py:91-92) and per tree under the virtual root (forest.py:26),
-so the step shards with no cross-GPU reduction:
+attention.py:91-92) and per tree under the virtual root (forest.py:26;
+PAPER.md:506), so the step shards with no cross-GPU reduction:
 
-  * kv-head split (tensor-parallel): rank r owns kv heads
+  * kv-head split (tensor-parallel, PAPER.md:1133): rank r owns kv heads
     [r*h_kv/G, (r+1)*h_kv/G) of every node -- a contiguous slab of the
     head-major pool -- and the matching contiguous block of query heads;
     every rank runs the same plan on 1/G of the bytes and FLOPs. The only
-    collective is one all-gather of the [bs, h_q/G, d] outputs.
+    collective is one all-gather of the [bs, h_q/G, d] outputs
+    (`all_gather_heads`).
   * tree partition: whole trees (children of the virtual root) are
-    LPT-assigned to ranks by their summed cost estimate
-    (greedy_assign, scheduler.py:142-155); each rank plans its own
-    sub-forest; outputs are gathered by request.
+    LPT-assigned to ranks by their summed cost estimate (greedy_assign,
+    scheduler.py:142-155). `shard_trees` cuts a rank's sub-forest (its
+    trees' nodes renumbered in global id order, its requests renumbered
+    in ascending global order); the rank plans and runs it alone over a
+    pool holding only its trees' KV, and `gather_requests` all-gathers
+    the per-rank outputs and scatters them back into global request order.
 
-The collective goes through torch.distributed, NCCL over NVLink on the
-B200 box and gloo in the CPU tests of the reassembly logic.
+The collective goes through torch.distributed: NCCL over NVLink on the
+B200 box, gloo in the CPU tests of the partition / reassembly logic.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
+
+import numpy as np
 
 
 def head_shard(h_kv: int, world: int, rank: int) -> tuple:
@@ -38,27 +44,45 @@ def assemble_heads(gathered):
     return gathered.permute(1, 0, 2, 3).reshape(bs, G * hl, d)
 
 
-def all_gather_heads(local_out, group=None):
-    """All-gather this rank's [bs, h_q/G, d] output into [bs, h_q, d]."""
+def all_gather_heads(local_out, group=None, out=None):
+    """All-gather this rank's [bs, h_q/G, d] output into [bs, h_q, d]
+    (`out`, when given, is the [G, bs, h_q/G, d] receive buffer)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    buf = torch.empty((world,) + tuple(local_out.shape), dtype=local_out.dtype, device=local_out.device)
-    dist.all_gather_into_tensor(buf, local_out.contiguous(), group=group)
+    buf = out if out is not None else torch.empty((world,) + tuple(local_out.shape), dtype=local_out.dtype,
+                                                  device=local_out.device)
+    # rank-major concatenation along dim 0 (the form every backend accepts)
+    flat = buf.view((world * local_out.shape[0],) + tuple(local_out.shape[1:]))
+    dist.all_gather_into_tensor(flat, local_out.contiguous(), group=group)
     return assemble_heads(buf)
 
 
+# ------------------------------------------------------------ tree partition
 @dataclass(frozen=True)
 class TreePartition:
     trees: tuple         # root node id of each tree
     rank_of_tree: tuple  # rank owning each tree
     loads: tuple         # summed estimate per rank (ms)
+    tree_cost: tuple = ()  # summed estimate per tree (ms)
+
+    @property
+    def world(self) -> int:
+        return len(self.loads)
 
     def requests_of(self, forest, rank):
         """Requests whose path starts in a tree owned by `rank`, ascending."""
         own = {t for t, r in zip(self.trees, self.rank_of_tree) if r == rank}
         return [i for i, p in enumerate(forest.paths) if p[0] in own]
+
+
+def tree_roots(forest) -> dict:
+    """node id -> root of its tree (the child of the virtual root above it)."""
+    root_of = {}
+    for n in forest.nodes[1:]:  # parents precede children (forest.py:160-216)
+        root_of[n.id] = n.id if n.parent == 0 else root_of[n.parent]
+    return root_of
 
 
 def tree_partition(forest, table, world: int, head_multiplicity: int = 1) -> TreePartition:
@@ -67,13 +91,126 @@ def tree_partition(forest, table, world: int, head_multiplicity: int = 1) -> Tre
     from .cost_model import estimate
     from .scheduler import greedy_assign
 
+    if world < 1:
+        raise ValueError(f"need world >= 1, got {world}")
     roots = [n.id for n in forest.nodes[1:] if n.parent == 0]
-    root_of = {}
-    for n in forest.nodes[1:]:
-        root_of[n.id] = n.id if n.parent == 0 else root_of[n.parent]
+    root_of = tree_roots(forest)
     cost = {r: 0.0 for r in roots}
     for n in forest.nodes[1:]:
         if n.query_set:
             cost[root_of[n.id]] += estimate(table, len(n.query_set) * head_multiplicity, n.len)
     a = greedy_assign([cost[r] for r in roots], world)
-    return TreePartition(tuple(roots), tuple(a.block_of), tuple(a.loads))
+    return TreePartition(tuple(roots), tuple(a.block_of), tuple(a.loads), tuple(cost[r] for r in roots))
+
+
+@dataclass(frozen=True)
+class TreeShard:
+    """One rank's part of a tree partition.
+
+    requests[i] is the global id of local request i (ascending); nodes[j]
+    the global id of local node j + 1 (ascending, so parents still precede
+    children); parent / lengths / paths / visible describe the sub-forest
+    in local ids, the forest_from_pool argument form."""
+
+    rank: int
+    requests: tuple
+    nodes: tuple
+    parent: tuple
+    lengths: tuple
+    paths: tuple
+    visible: tuple | None
+
+    @property
+    def bs(self) -> int:
+        return len(self.requests)
+
+    def forest(self, h_kv: int, d: int, kv_dtype: str = "bfloat16"):
+        """The sub-forest (no tensors; adopt or pack a pool for it)."""
+        from .forest import forest_from_pool
+        return forest_from_pool(self.parent, self.lengths, self.paths, h_kv, d, visible=self.visible,
+                                kv_dtype=kv_dtype)
+
+    def token_map(self, full_forest, sub_forest) -> np.ndarray:
+        """int64 [T_sub]: global pool token of every sub-forest pool token
+        (the sub-forest's own preorder layout)."""
+        idx = np.zeros(max(sub_forest.total_tokens, 1), dtype=np.int64)
+        for j, gn in enumerate(self.nodes):
+            ln = self.lengths[j]
+            lo = sub_forest.token_offset[j + 1]
+            g0 = full_forest.token_offset[gn]
+            idx[lo:lo + ln] = np.arange(g0, g0 + ln, dtype=np.int64)
+        return idx
+
+    def slice_pool(self, full_forest, sub_forest, k_pool, v_pool):
+        """This shard's head-major pools [h][T_sub][d] cut from the full
+        forest's pools (tests, single-GPU emulation of a sharded run)."""
+        import torch
+        idx = torch.from_numpy(self.token_map(full_forest, sub_forest)).to(k_pool.device)
+        return k_pool.index_select(1, idx).contiguous(), v_pool.index_select(1, idx).contiguous()
+
+
+def shard_trees(forest, part: TreePartition, rank: int) -> TreeShard:
+    """Rank `rank`'s sub-forest under a tree partition."""
+    if not 0 <= rank < part.world:
+        raise ValueError(f"bad rank {rank} of {part.world}")
+    own = {t for t, r in zip(part.trees, part.rank_of_tree) if r == rank}
+    root_of = tree_roots(forest)
+    nodes = [n.id for n in forest.nodes[1:] if root_of[n.id] in own]
+    local = {gn: j + 1 for j, gn in enumerate(nodes)}
+    reqs = [r for r, p in enumerate(forest.paths) if p[0] in own]
+    rloc = {r: i for i, r in enumerate(reqs)}
+    parent = tuple(0 if forest.nodes[gn].parent == 0 else local[forest.nodes[gn].parent] for gn in nodes)
+    lengths = tuple(forest.nodes[gn].len for gn in nodes)
+    paths = tuple(tuple(local[gn] for gn in forest.paths[r]) for r in reqs)
+    vis = []
+    any_vis = False
+    for gn in nodes:
+        v = forest.nodes[gn].visible_len
+        if v:
+            any_vis = True
+            vis.append({rloc[r]: c for r, c in v.items() if r in rloc})
+        else:
+            vis.append(None)
+    return TreeShard(rank, tuple(reqs), tuple(nodes), parent, lengths, paths, tuple(vis) if any_vis else None)
+
+
+def request_index(shards) -> np.ndarray:
+    """Global request id of every row of the rank-major concatenation of
+    the shards' outputs."""
+    return np.concatenate([np.asarray(s.requests, dtype=np.int64) for s in shards]) if shards else \
+        np.zeros(0, np.int64)
+
+
+def scatter_requests(per_rank, shards, bs: int):
+    """Reassemble rank-ordered outputs ([n_r, h_q, d] each, or a padded
+    [G, max n_r, h_q, d] gather buffer) into global request order."""
+    import torch
+    rows = torch.cat([per_rank[r][:s.bs] for r, s in enumerate(shards)])
+    idx = torch.from_numpy(request_index(shards)).to(rows.device)
+    if idx.numel() != bs or not torch.equal(torch.sort(idx).values, torch.arange(bs, device=rows.device)):
+        raise ValueError("the shards do not cover every request exactly once")
+    out = torch.empty((bs,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+    out.index_copy_(0, idx, rows)
+    return out
+
+
+def gather_requests(local_out, shards, bs: int, group=None, buf=None):
+    """All-gather every rank's [n_r, h_q, d] output (padded to the largest
+    shard, one all_gather_into_tensor) and return [bs, h_q, d] in global
+    request order. `shards` = every rank's TreeShard (all ranks derive the
+    same partition)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if len(shards) != world:
+        raise ValueError(f"{len(shards)} shards for {world} ranks")
+    n_max = max(s.bs for s in shards)
+    send = local_out
+    if local_out.shape[0] != n_max:
+        send = torch.zeros((n_max,) + tuple(local_out.shape[1:]), dtype=local_out.dtype, device=local_out.device)
+        send[:local_out.shape[0]] = local_out
+    if buf is None:
+        buf = torch.empty((world,) + tuple(send.shape), dtype=send.dtype, device=send.device)
+    dist.all_gather_into_tensor(buf.view((world * n_max,) + tuple(send.shape[1:])), send.contiguous(), group=group)
+    return scatter_requests(buf, shards, bs)

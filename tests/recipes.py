@@ -102,3 +102,49 @@ def pac_inputs(shape, dtype=np.float64, seed=7, masked=False):
     v = rng.standard_normal((n, h_kv, d)).astype(dtype)
     vis = rng.integers(1, n + 1, size=n_q) if masked else None
     return q, k, v, vis
+
+
+def multi_tree_spec(seed, n_trees=5, h_q=8, h_kv=4, d=16, with_masks=True):
+    """Several independent trees under the virtual root (forest.py:26):
+    random depth / fan-out / lengths per tree, optional per-request
+    visible_len masks. The tree partition tests' input."""
+    rng = np.random.default_rng(seed)
+    scale = 1.0 / math.sqrt(d)
+    spec = Spec(h_q, h_kv, d)
+
+    def grow(parent):
+        n = int(rng.integers(1, 96))
+        spec.parent.append(parent)
+        spec.length.append(n)
+        spec.keys.append(rng.standard_normal((n, h_kv, d)) * scale)
+        spec.values.append(rng.standard_normal((n, h_kv, d)) * scale)
+        return spec.n_nodes - 1
+
+    for _ in range(n_trees):
+        root = grow(0)
+        frontier, tree = [root], [root]
+        for _ in range(int(rng.integers(0, 3))):
+            nxt = [grow(p) for p in frontier for _ in range(int(rng.integers(1, 4)))]
+            tree += nxt
+            frontier = nxt
+        inner = {spec.parent[n] for n in tree}
+        leaves = [n for n in tree if n not in inner]
+        for leaf in leaves:
+            for _ in range(int(rng.integers(1, 3))):  # some leaves serve two requests
+                chain, cur = [], leaf
+                while cur:
+                    chain.append(cur)
+                    cur = spec.parent[cur]
+                spec.paths.append(tuple(reversed(chain)))
+    # interleave the trees' requests (a shard's requests are then scattered)
+    spec.paths = [spec.paths[i] for i in rng.permutation(len(spec.paths))]
+    spec.visible = [None] * spec.n_nodes
+    if with_masks:
+        for rid, path in enumerate(spec.paths):
+            for nid in path:
+                ln = spec.length[nid]
+                if ln > 1 and rng.random() < 0.25:
+                    spec.visible[nid] = spec.visible[nid] or {}
+                    spec.visible[nid][rid] = int(rng.integers(1, ln + 1))
+    spec.queries = rng.standard_normal((spec.bs, h_q, d)) * scale
+    return spec

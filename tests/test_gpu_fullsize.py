@@ -1,0 +1,339 @@
+"""Full-size parity of the benchmarked path, sharded steps and the numerics
+edge cases of the bf16 kernels. Needs a B200.
+
+* cfg2 at its BASELINE.json size through the bench's exact step
+  (bench.prepare: plan_device, the autotuned tensor-core SM budget, the
+  concurrent PDL suffix launch, CUDA-graph replay): sampled requests
+  against the CPU oracle (oracle/attention.py naive_attention on the same
+  bf16 values upcast to float64) and many more against a float64 device
+  recomputation that is itself pinned to the oracle on those requests.
+* cfg4 including the 128K-prefix tree and the tree with most requests.
+* kv-head-sharded steps for G = 2, 4, 8 and tree-partitioned steps
+  (per-rank sub-forest, plan, pool; request-order reassembly), emulated
+  rank by rank on one GPU, against the oracle.
+* peaked and +-500 scores (reference test_attention.py:255-271,
+  test_acceptance.py:101-126) in bf16 through the tensor-core kernel's lazy
+  rescale and the suffix kernel's.
+* 16 query heads per kv head (suffixes on the generic kernel) and paged
+  growth.
+The bar is the north star's bf16 tolerance: max-abs 2e-3 and max-norm rel
+1e-2 against the oracle on the bf16 values."""
+from __future__ import annotations
+
+import io
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_table_text
+from oracle import attention as OA
+import paper_2505_17694_b200 as P
+from paper_2505_17694_b200 import parallel as PL
+from paper_2505_17694_b200 import workloads as W
+from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_TC, DecodeStep
+
+pytestmark = pytest.mark.gpu
+
+BF16_ABS, BF16_REL = 2e-3, 1e-2
+
+
+def close(got, ref, what=""):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    assert np.isfinite(got).all(), what
+    err = float(np.max(np.abs(got - ref)))
+    rel = err / max(float(np.max(np.abs(ref))), 1e-300)
+    assert err <= BF16_ABS and rel <= BF16_REL, (what, err, rel)
+    return err, rel
+
+
+@pytest.fixture(scope="module")
+def table():
+    return P.load_profile(io.StringIO(golden_table_text("a100_d128.csv")))
+
+
+def pool_node(forest, pool, n):
+    """node n's tokens [len, h, d] (float64, host) from a head-major pool"""
+    o = forest.token_offset[n]
+    return pool[:, o:o + forest.node(n).len].permute(1, 0, 2).double().cpu().numpy()
+
+
+def oracle_requests(forest, kp, vp, q, reqs):
+    """naive_attention (the oracle) for `reqs`, over a ForestData holding
+    just their paths' nodes, on the pools' bf16 values upcast to float64."""
+    nodes = sorted({n for r in reqs for n in forest.paths[r]})
+    loc = {n: i + 1 for i, n in enumerate(nodes)}
+    parent = [0] + [loc.get(forest.node(n).parent, 0) for n in nodes]
+    h = kp.shape[0]
+    z = np.zeros((0, h, forest.d))
+    keys = [z] + [pool_node(forest, kp, n) for n in nodes]
+    vals = [z] + [pool_node(forest, vp, n) for n in nodes]
+    paths = [tuple(loc[n] for n in forest.paths[r]) for r in reqs]
+    vis = [None] * (len(nodes) + 1)
+    for i, r in enumerate(reqs):
+        for n in forest.paths[r]:
+            c = forest.visible_count(n, r)
+            if c != forest.node(n).len:
+                vis[loc[n]] = vis[loc[n]] or {}
+                vis[loc[n]][i] = c
+    fd = OA.ForestData(parent, keys, vals, paths, vis)
+    return OA.naive_attention(q[list(reqs)].double().cpu().numpy(), fd)
+
+
+# ------------------------------------------------------------ cfg2 full size
+@pytest.fixture(scope="module")
+def cfg2_bench():
+    import torch
+    import bench
+    ns = bench.prepare("cfg2", torch.device("cuda", 0))
+    replay = ns.step.capture(ns.q_dev, ns.kp, ns.vp, ns.out)
+    replay()
+    replay()  # a second replay over the same workspace
+    torch.cuda.synchronize()
+    yield ns
+    del ns
+    torch.cuda.empty_cache()
+
+
+class TestCfg2BenchStep:
+    def test_plan_is_the_benchmarked_one(self, cfg2_bench):
+        ns = cfg2_bench
+        assert ns.forest.bs == 256 and ns.forest.total_tokens == 32768 + 256 * 512
+        assert ns.step.info.n_tc_groups > 0 and ns.step.info.n_gemv_groups == 256 and ns.step.info.n_merge > 0
+        assert ns.step.aux is not None and ns.budget in ns.tune_ms
+
+    def test_sampled_requests_vs_oracle(self, cfg2_bench):
+        import bench
+        ns = cfg2_bench
+        out = ns.out.double().cpu().numpy()
+        reqs = [0, 77, 128, 255]
+        ref = oracle_requests(ns.forest, ns.kp, ns.vp, ns.q_dev, reqs)
+        for i, r in enumerate(reqs):
+            close(out[r], ref[i], f"cfg2 request {r} vs oracle")
+            # the device float64 recomputation used below is the oracle's math
+            dev = bench.path_reference(ns.forest, ns.kp, ns.vp, ns.q_dev, r).cpu().numpy()
+            assert float(np.max(np.abs(dev - ref[i]))) <= 1e-10
+
+    def test_many_requests_vs_device_reference(self, cfg2_bench):
+        import bench
+        ns = cfg2_bench
+        rng = np.random.default_rng(0)
+        reqs = sorted(set(rng.choice(256, 64, replace=False).tolist()) | {0, 1, 254, 255})
+        for r in reqs:
+            ref = bench.path_reference(ns.forest, ns.kp, ns.vp, ns.q_dev, r)
+            close(ns.out[r].double().cpu().numpy(), ref.cpu().numpy(), f"cfg2 request {r}")
+
+    def test_bench_verify_passes(self, cfg2_bench):
+        import bench
+        assert bench.verify(cfg2_bench, cfg2_bench.out, n=16)["ok"]
+
+
+# ------------------------------------------------------------ cfg4 full size
+class TestCfg4LargeTrees:
+    def test_long_prefix_and_large_fanout_trees(self):
+        import torch
+        import bench
+        ns = bench.prepare("cfg4", torch.device("cuda", 0), budgets=[148])
+        ns.step(ns.q_dev, ns.kp, ns.vp, out=ns.out)
+        torch.cuda.synchronize()
+        f = ns.forest
+        assert bool(torch.isfinite(ns.out).all())
+        roots = [n.id for n in f.nodes[1:] if n.parent == 0]
+        longest = max(roots, key=lambda n: f.node(n).len)
+        widest = max(roots, key=lambda n: len(f.node(n).query_set))
+        assert f.node(longest).len > 100_000 and len(f.node(widest).query_set) > 300
+        rng = np.random.default_rng(4)
+        reqs = set()
+        for root in (longest, widest):
+            qs = list(f.node(root).query_set)
+            reqs |= {qs[0], qs[-1]} | set(rng.choice(qs, size=min(4, len(qs)), replace=False).tolist())
+        reqs |= set(rng.choice(f.bs, size=8, replace=False).tolist())
+        for r in sorted(reqs):
+            ref = bench.path_reference(f, ns.kp, ns.vp, ns.q_dev, r)
+            close(ns.out[r].double().cpu().numpy(), ref.cpu().numpy(), f"cfg4 request {r}")
+        # two of them through the oracle itself (the 128K-prefix tree's first request)
+        r0 = f.node(longest).query_set[0]
+        ref = oracle_requests(f, ns.kp, ns.vp, ns.q_dev, [r0])
+        close(ns.out[r0].double().cpu().numpy(), ref[0], "cfg4 128K-prefix request vs oracle")
+        del ns
+        torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------ sharded steps
+def _bf16_forest(spec, seed):
+    """forest + device pools / queries (bf16, drawn on the host, seeded)"""
+    import torch
+    f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, spec.h_kv, spec.d,
+                           visible=(spec.visible or [None] * spec.n_nodes)[1:])
+    gen = torch.Generator().manual_seed(seed)
+    sc = 1.0 / math.sqrt(spec.d)
+    T = f.total_tokens
+    kp = (torch.randn((spec.h_kv, T, spec.d), generator=gen) * sc).to(torch.bfloat16).cuda()
+    vp = (torch.randn((spec.h_kv, T, spec.d), generator=gen) * sc).to(torch.bfloat16).cuda()
+    q = (torch.randn((f.bs, spec.h_q, spec.d), generator=gen) * sc).to(torch.bfloat16).cuda()
+    return f, kp, vp, q
+
+
+class TestShardedSteps:
+    @pytest.mark.parametrize("world", [2, 4, 8])
+    def test_head_split(self, table, world):
+        """DecodeStep(head_begin, head_end) per rank over its pool slab;
+        all_gather_heads' reassembly (assemble_heads) of the rank outputs."""
+        import torch
+        spec = W.two_level(3000, 200, 72, h_q=32, h_kv=8, d=128, seed=world, tensors=False)
+        f, kp, vp, q = _bf16_forest(spec, world)
+        outs = []
+        for rank in range(world):
+            h0, h1 = PL.head_shard(8, world, rank)
+            plan = P.plan_device(f, 4, table, h1 - h0, 148)
+            st = DecodeStep(f, plan, 32, "bfloat16", head_begin=h0, head_end=h1)
+            outs.append(st(q[:, h0 * 4:h1 * 4].contiguous(), kp[h0:h1].contiguous(), vp[h0:h1].contiguous()))
+        full = PL.assemble_heads(torch.stack(outs)).double().cpu().numpy()
+        reqs = list(range(f.bs))
+        close(full, oracle_requests(f, kp, vp, q, reqs), f"head split x{world}")
+
+    @pytest.mark.parametrize("world", [2, 3, 4])
+    def test_tree_partition(self, table, world):
+        """tree_partition -> shard_trees -> per-rank sub-forest, plan and
+        pool -> scatter_requests, against the oracle on the whole forest."""
+        import torch
+        parent, length, paths = [0], [0], []
+        rng = np.random.default_rng(world)
+        for t in range(7):
+            root = len(parent)
+            parent.append(0)
+            length.append(int(rng.integers(300, 5000)))
+            for _ in range(int(rng.integers(1, 70))):
+                parent.append(root)
+                length.append(int(rng.integers(20, 400)))
+                paths.append((root, len(parent) - 1))
+        order = rng.permutation(len(paths))
+        paths = [paths[i] for i in order]  # interleave the trees' requests
+        spec = W.Spec(32, 8, 128, parent, length, None, None, paths, None, None)
+        f, kp, vp, q = _bf16_forest(spec, 10 + world)
+        part = PL.tree_partition(f, P.load_default_profile(), world, head_multiplicity=4)
+        shards = [PL.shard_trees(f, part, r) for r in range(world)]
+        outs = []
+        for s in shards:
+            sub = s.forest(8, 128)
+            skp, svp = s.slice_pool(f, sub, kp, vp)
+            sq = q[list(s.requests)].contiguous()
+            st = DecodeStep(sub, P.plan_device(sub, 4, P.load_default_profile(), 8, 148), 32, "bfloat16")
+            outs.append(st(sq, skp, svp))
+        full = PL.scatter_requests(outs, shards, f.bs).double().cpu().numpy()
+        close(full, oracle_requests(f, kp, vp, q, list(range(f.bs))), f"tree partition x{world}")
+
+
+# ------------------------------------------------------------ score extremes
+def _extreme_spec(seed, mode):
+    """two-level forest (root shared by 64 requests -> tensor-core kernel,
+    300-token suffixes -> suffix kernel) with bf16-exact adversarial keys.
+    'extreme': q = 1 everywhere, 1 % of the keys set to +-44.25 in every
+    coordinate (raw scores +-500.6 after 1/sqrt(128)), elsewhere N(0,1)/sqrt(d);
+    'peaked': queries scaled by 800 (scores ~ N(0, 6^2), a softmax
+    dominated by a few tokens of every slice)."""
+    rng = np.random.default_rng(seed)
+    spec = W.two_level(3000, 300, 64, h_q=32, h_kv=8, d=128, seed=seed)
+    if mode == "extreme":
+        spec.queries = np.ones_like(spec.queries)
+        for n in range(1, spec.n_nodes):
+            k = spec.keys[n]
+            hit = rng.random(k.shape[:2]) < 0.01
+            sign = np.where(rng.random(k.shape[:2]) < 0.5, -1.0, 1.0)
+            k[hit] = (44.25 * sign[hit])[:, None]
+        # the root holds no +500 key in kv head 0: that head's max frame
+        # lives in the suffixes while its root partial sits ~1000 below
+        root_k = spec.keys[1]
+        root_k[:, 0][root_k[:, 0, 0] > 40.0] = -44.25
+    else:
+        spec.queries = spec.queries * 800.0
+    return spec
+
+
+class TestScoreExtremes:
+    @pytest.mark.parametrize("mode", ["extreme", "peaked"])
+    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC])
+    def test_bf16_kernels(self, table, mode, flags):
+        import torch
+        spec = _extreme_spec(31, mode)
+        to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16)
+        specs = [(p, to(k), to(v)) for p, k, v, _ in spec.node_specs()]
+        qb = P.QueryBatch(to(spec.queries), spec.h_kv)
+        f = P.build_forest(specs, spec.paths, qb)
+        plan = P.plan_device(f, 4, table, 8, 148)
+        kp, vp = f.device_pool(torch.bfloat16)
+        step = DecodeStep(f, plan, 32, "bfloat16", flags=flags)
+        if flags == 0:
+            assert step.info.n_tc_groups > 0 and step.info.n_gemv_groups > 0
+        out = step(qb.queries.cuda(), kp, vp).double().cpu().numpy()
+        ref = oracle_requests(f, kp, vp, qb.queries.cuda(), list(range(f.bs)))
+        close(out, ref, f"{mode} flags={flags}")
+
+
+# ------------------------------------------------------------ other shapes
+class TestShapes:
+    def test_sixteen_q_heads_per_kv_head(self, table):
+        """g = 16 (128 q / 8 kv heads): the root on the tensor cores (8
+        requests per 128-row tile), the suffixes on the generic kernel."""
+        spec = W.two_level(1500, 180, 20, h_q=128, h_kv=8, d=128, seed=3, tensors=False)
+        f, kp, vp, q = _bf16_forest(spec, 3)
+        st = DecodeStep(f, P.plan_device(f, 16, table, 8, 148), 128, "bfloat16")
+        assert st.info.n_tc_groups > 0 and st.info.n_gen_groups > 0 and st.info.n_gemv_groups == 0
+        out = st(q, kp, vp).double().cpu().numpy()
+        close(out, oracle_requests(f, kp, vp, q, list(range(f.bs))), "g=16")
+
+    def test_paged_grow_matches_rebuilt_step(self, table):
+        """grow() on a paged step (the group records carry their slice start)."""
+        import torch
+        from paper_2505_17694_b200.paging import page_layout, paged_pools
+        bs, shared, cap, start, page = 20, 1024, 256, 150, 128
+        spec = W.two_level(shared, cap, bs, h_q=32, h_kv=8, d=128, seed=8, tensors=False)
+
+        def forest(vis):
+            return P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128,
+                                      visible=[None] + [{r: vis} for r in range(bs)])
+
+        f0 = forest(start)
+        gen = torch.Generator().manual_seed(5)
+        T = f0.total_tokens
+        kp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        vp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        q = (torch.randn((bs, 32, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        kx, vx, pt = paged_pools(f0, kp, vp, page, n_phys_pages=page_layout(f0, page)[1] + 3, generator=gen)
+        step = DecodeStep(f0, P.plan_device(f0, 4, table, 8, 148, page_size=page), 32, "bfloat16",
+                          concurrent=False, page_size=page, page_table=pt, pool_tokens=kx.shape[1])
+        for k in range(1, 4):
+            step.grow(1)
+            got = step(q, kx, vx)
+            assert all(f0.visible_count(2 + r, r) == start + k for r in range(bs))
+            f2 = forest(start + k)
+            ref = DecodeStep(f2, P.plan_device(f2, 4, table, 8, 148), 32, "bfloat16", concurrent=False)(q, kp, vp)
+            torch.cuda.synchronize()
+            assert torch.equal(got, ref), k
+
+    def test_plan_cache_cadence(self, table):
+        """PlanCache: grow in place between re-plans, re-plan every 4 steps;
+        every step equals a step built from scratch."""
+        import torch
+        from paper_2505_17694_b200.executor import PlanCache
+        bs, shared, cap, start = 12, 2048, 64, 40
+        spec = W.two_level(shared, cap, bs, h_q=32, h_kv=8, d=128, seed=9, tensors=False)
+
+        def forest(vis):
+            return P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128,
+                                      visible=[None] + [{r: vis} for r in range(bs)])
+
+        f = forest(start)
+        gen = torch.Generator().manual_seed(9)
+        kp = (torch.randn((8, f.total_tokens, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        vp = (torch.randn((8, f.total_tokens, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        q = (torch.randn((bs, 32, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        cache = PlanCache(32, table=table, replan_every=4, dtype="bfloat16", concurrent=False)
+        for k in range(10):
+            got = cache.get(f)(q, kp, vp)
+            fr = forest(start + k)
+            ref = DecodeStep(fr, P.plan_device(fr, 4, table, 8, 148), 32, "bfloat16", concurrent=False)(q, kp, vp)
+            torch.cuda.synchronize()
+            assert torch.equal(got, ref), k
+            cache.advance(1)
+        assert cache.replans == 3  # steps 0, 4, 8
