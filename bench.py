@@ -648,6 +648,20 @@ def main():
         cpu = {"value": r.bytes / dt / 1e9, "unit": "GB/s", "cores": r.workers, "kind": r.kind,
                "sample": r.desc, "seconds": dt, "plan_seconds": r.plan_s}
 
+    run_rep = None
+    if rank == 0 and ns.forest is ns.full:
+        # the reference CLI's RunReport for this workload point (report.py;
+        # schemas/report.schema.json admits the reference's four families)
+        from paper_2505_17694_b200 import workloads as W
+        from paper_2505_17694_b200.report import FAMILIES, check_report, run_report
+        kw = W.CONFIGS[args.config]
+        fam = kw["fn"].__name__
+        if fam in FAMILIES:
+            params = {k: v for k, v in kw["kw"].items() if k not in ("h_q", "h_kv", "d", "seed")}
+            wl = {"family": fam, "params": params, "seed": int(kw["kw"].get("seed", 0)),
+                  "dims": {"h_q": h_q, "h_kv": ns.cfg["h_kv"], "d": d}}
+            run_rep = run_report(ns.full, plan, ns.table, m, wl, max_rel_err=check["max_rel"], element_size=2)
+            check_report(run_rep)
     if rank == 0:
         traffic = P.traffic_report(ns.full, element_size=2)
         line = {
@@ -677,6 +691,7 @@ def main():
                                     "reduction": traffic.bytes_baseline / total_bytes,
                                     "dram_bytes_ncu": ncu.get("step_dram_bytes")},
             "verified": check,
+            "run_report": run_rep,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": step.launches * args.steps * windows,

@@ -49,6 +49,10 @@ typedef enum {
   CODEC_ERR_PLAN_FOREST_MISMATCH = 10,   /* errors.PlanForestMismatch     */
   CODEC_ERR_INCOMPLETE_PARTIALS = 11,    /* errors.IncompletePartials     */
   CODEC_ERR_SEARCH_SPACE_OVERFLOW = 12,  /* errors.SearchSpaceOverflow    */
+  CODEC_ERR_PROFILE_LOAD = 13,           /* errors.ProfileLoadError       */
+  CODEC_ERR_INCOMPLETE_GRID = 14,        /* errors.IncompleteGrid         */
+  CODEC_ERR_NON_POSITIVE_COST = 15,      /* errors.NonPositiveCost        */
+  CODEC_ERR_DUPLICATE_KNOT = 16,         /* errors.DuplicateKnot          */
   CODEC_ERR_VALUE = 20,                  /* builtin ValueError            */
   CODEC_ERR_UNSUPPORTED = 30,            /* shape/dtype the kernels do not cover */
   CODEC_ERR_CUDA = 31                    /* CUDA runtime/launch failure   */
@@ -102,6 +106,45 @@ CODEC_API int32_t codec_index_read(const codec_index* ix, int64_t* node_off, int
                          int32_t* children_idx);
 
 /* ======================================================================
+ * Structural report of a forest snapshot.  Replaces validate()
+ * forest.py:266-363: every invariant checked, violations reported (not
+ * raised) in the reference's order with its messages. The caller flattens
+ * the (possibly corrupted) forest: per node position i its id, parent,
+ * length and K/V state (kv_state 0: not checked, 1: K and V shapes differ,
+ * 2: keys.shape[1:] given as kv_tail[kv_tail_ptr[i], kv_tail_ptr[i+1]));
+ * children / paths / query sets as CSR; visible_len as (node, request,
+ * count) triples in node order; token_offset as stored.
+ * ==================================================================== */
+typedef enum {
+  CODEC_VIOLATION_BAD_NODE_INDEX = 0,
+  CODEC_VIOLATION_NON_EMPTY_ROOT = 1,
+  CODEC_VIOLATION_EMPTY_NON_ROOT = 2,
+  CODEC_VIOLATION_DIMENSION_MISMATCH = 3,
+  CODEC_VIOLATION_CYCLE_DETECTED = 4,
+  CODEC_VIOLATION_DANGLING_PARENT = 5,
+  CODEC_VIOLATION_ADJACENCY_MISMATCH = 6,
+  CODEC_VIOLATION_PATH_NOT_PREFIX_CHAIN = 7,
+  CODEC_VIOLATION_QUERY_SET_UNSORTED = 8,
+  CODEC_VIOLATION_QUERY_SET_PATH_MISMATCH = 9,
+  CODEC_VIOLATION_VISIBLE_LEN_OUT_OF_RANGE = 10,
+  CODEC_VIOLATION_FLATTEN_MISMATCH = 11
+} codec_violation_code;
+typedef struct codec_report codec_report;
+CODEC_API int32_t codec_forest_validate(int32_t n_nodes, const int64_t* node_id, const int64_t* parent,
+                                        const int64_t* length, const int32_t* kv_state, const int64_t* kv_tail_ptr,
+                                        const int64_t* kv_tail, int64_t h_kv, int64_t d, const int64_t* children_ptr,
+                                        const int64_t* children_idx, int32_t bs, const int64_t* path_ptr,
+                                        const int64_t* path_idx, const int64_t* qset_ptr, const int64_t* qset_idx,
+                                        int64_t n_vis, const int64_t* vis_node, const int64_t* vis_req,
+                                        const int64_t* vis_count, const int64_t* token_offset,
+                                        int64_t n_token_offset, codec_report** out);
+CODEC_API int32_t codec_report_count(const codec_report* rep, int64_t* n);
+/* record i: code, node / request (INT64_MIN = None), message (NUL-terminated, truncated to msg_cap) */
+CODEC_API int32_t codec_report_get(const codec_report* rep, int64_t i, int32_t* code, int64_t* node,
+                                   int64_t* request, char* msg, int64_t msg_cap);
+CODEC_API void codec_report_free(codec_report* rep);
+
+/* ======================================================================
  * K1 -- cost model, task division and schedule (host, float64, operation
  * order identical to the reference => bit-exact plans).
  * ==================================================================== */
@@ -112,6 +155,19 @@ typedef struct {
   const double* cost_ms;     /* [n_n][n_nq] row-major      */
 } codec_cost_table;
 
+/* load_profile() grid assembly (cost_model.py:102-150): profile rows in
+ * file order -> sorted unique knots and the n-major grid; raises
+ * DuplicateKnot / NonPositiveCost on the first offending row, then
+ * IncompleteGrid on the first missing cell. grid NULL: sizing call (knot
+ * counts only). */
+CODEC_API int32_t codec_cost_grid(int64_t n_rows, const int64_t* row_nq, const int64_t* row_n,
+                                  const double* row_cost, int32_t* n_nq, int32_t* n_n, int64_t* nq_knots,
+                                  int64_t* n_knots, double* grid);
+/* CostTable invariants (cost_model.py:39-53): grid shape (given as
+ * grid_ndim / grid_shape) = (len(n), len(n_q)), strictly ascending positive
+ * knots, positive costs. */
+CODEC_API int32_t codec_cost_table_check(int32_t n_nq, const int64_t* nq_knots, int32_t n_n, const int64_t* n_knots,
+                                         int32_t grid_ndim, const int64_t* grid_shape, const double* cost_ms);
 /* estimate()            cost_model.py:68-84 */
 CODEC_API double codec_estimate(const codec_cost_table* t, int64_t n_q, int64_t n);
 /* slice_ranges()/canonical_division()   scheduler.py:81-92.
@@ -314,6 +370,23 @@ CODEC_API int32_t codec_pac(int32_t dtype, const void* q, const void* k, const v
 CODEC_API int32_t codec_por(int32_t dtype, int64_t count, int64_t d, const void* a_out, const void* a_m,
                   const void* a_s, const void* b_out, const void* b_m, const void* b_s,
                   void* r_out, void* r_m, void* r_s, void* stream);
+
+/* merge_schedule()  executor.py:86-111 (mode 0: balanced rounds over
+ * sum(slices_per_node) partials) / sequential_schedule()  :114-117 (mode 1:
+ * path_len = total, P-1 rounds of (0, i)). Writes the (left, right) label
+ * pairs (2 per pair, up to cap pairs) and round_ptr[n_rounds + 1] when both
+ * are non-NULL; *n_pairs / *n_rounds always. */
+CODEC_API int32_t codec_merge_schedule(int32_t mode, int64_t path_len, const int64_t* slices_per_node,
+                                       int64_t n_counts, int64_t* pairs, int64_t* round_ptr, int64_t cap,
+                                       int64_t* n_pairs, int64_t* n_rounds);
+/* reduce_tree()'s fold + finalize math  executor.py:209-293 on the device:
+ * request i merges partial slots slot[ptr[i] .. ptr[i+1]) (device int32
+ * CSR) of part_out [n_slots][h_q][d], part_m / part_s [n_slots][h_q] (the
+ * PartialResult fields, F32 or F64) into out [n_req][h_q][d]; out_s
+ * [n_req][h_q] receives the merged exp-sum (0 = no visible token). */
+CODEC_API int32_t codec_merge_partials(int32_t dtype, int32_t n_req, int32_t h_q, int32_t d, const int32_t* ptr,
+                                       const int32_t* slot, const void* part_out, const void* part_m,
+                                       const void* part_s, void* out, void* out_s, void* stream);
 
 /* Pack token-major node tensors [len][h_kv][d] into the head-major pool
  * [h_local][pool_tokens][d] at token offset `tok0` (heads

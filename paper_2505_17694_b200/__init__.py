@@ -14,6 +14,7 @@ from .cost_model import (CostTable, default_profile_path, dump_profile, estimate
                          load_profile, profile_synthetic)
 from .errors import *  # noqa: F401,F403
 from .executor import BlockPool, DecodeStep, autotune_step, execute
+from .reduce import PartialTree, merge_schedule, reduce_tree, sequential_schedule
 from .serialize import dump_forest, load_forest
 from .forest import (Forest, KvNode, QueryBatch, Violation, build_forest, forest_from_pool, node_query_set,
                      prefix_path, validate)

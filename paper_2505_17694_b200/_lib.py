@@ -37,6 +37,10 @@ _STATUS = {
     10: E.PlanForestMismatch,
     11: E.IncompletePartials,
     12: E.SearchSpaceOverflow,
+    13: E.ProfileLoadError,
+    14: E.IncompleteGrid,
+    15: E.NonPositiveCost,
+    16: E.DuplicateKnot,
     20: ValueError,
     30: E.UnsupportedShape,
     31: E.CudaError,
@@ -110,6 +114,15 @@ _SIGS = {
     "codec_pac": (I32, [I32, P, P, P, P, I64, I64, I64, I64, I64, F64, P, P, P, P]),
     "codec_por": (I32, [I32, I64, I64, P, P, P, P, P, P, P, P, P, P]),
     "codec_pool_pack": (I32, [I32, P, I64, I64, I64, I32, I32, P, I64, I64, P]),
+    "codec_forest_validate": (I32, [I32, PI64, PI64, PI64, PI32, PI64, PI64, I64, I64, PI64, PI64, I32, PI64, PI64,
+                                    PI64, PI64, I64, PI64, PI64, PI64, PI64, I64, C.POINTER(P)]),
+    "codec_report_count": (I32, [P, PI64]),
+    "codec_report_get": (I32, [P, I64, PI32, PI64, PI64, C.c_char_p, I64]),
+    "codec_report_free": (None, [P]),
+    "codec_merge_schedule": (I32, [I32, I64, PI64, I64, PI64, PI64, I64, PI64, PI64]),
+    "codec_merge_partials": (I32, [I32, I32, I32, I32, P, P, P, P, P, P, P, P]),
+    "codec_cost_grid": (I32, [I64, PI64, PI64, PF64, PI32, PI32, PI64, PI64, PF64]),
+    "codec_cost_table_check": (I32, [I32, PI64, I32, PI64, I32, PI64, PF64]),
 }
 
 _lib = None

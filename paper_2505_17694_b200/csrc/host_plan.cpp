@@ -525,3 +525,59 @@ extern "C" int32_t codec_plan_read(const codec_plan* p, int64_t* b_k, int32_t* s
   if (loads) std::copy(p->loads.begin(), p->loads.end(), loads);
   return CODEC_OK;
 }
+
+// merge_schedule() / sequential_schedule() (executor.py:86-117): the
+// reference's per-request combination order of partials numbered 0..P-1 in
+// path-then-slice order. Balanced: each round pairs adjacent survivors,
+// the left label survives (ceil(log2 P) rounds); sequential: P-1 rounds of
+// (0, i). The device merge (kern_merge.cu) folds all P at once in one pass
+// -- equal up to rounding (test_attention.py:160-180); the schedule is the
+// reference's integer contract.
+extern "C" int32_t codec_merge_schedule(int32_t mode, int64_t path_len, const int64_t* slices_per_node,
+                                        int64_t n_counts, int64_t* pairs, int64_t* round_ptr, int64_t cap,
+                                        int64_t* n_pairs, int64_t* n_rounds) {
+  if (!n_pairs || !n_rounds) return codec::fail(CODEC_ERR_VALUE, "NULL argument");
+  int64_t total = 0;
+  if (mode == 0) {
+    if (path_len < 1) return codec::fail(CODEC_ERR_VALUE, "path_len must be >= 1");
+    if (n_counts != path_len)
+      return codec::fail(CODEC_ERR_VALUE, "expected %lld per-node slice counts, got %lld", (long long)path_len,
+                         (long long)n_counts);
+    for (int64_t i = 0; i < n_counts; ++i) total += slices_per_node[i];
+  } else if (mode == 1) {
+    total = path_len;  // sequential_schedule(total)
+  } else {
+    return codec::fail(CODEC_ERR_VALUE, "mode must be 0 (balanced) or 1 (sequential)");
+  }
+  std::vector<int64_t> out_pairs, out_ptr{0};
+  if (mode == 1) {
+    for (int64_t i = 1; i < total; ++i) {
+      out_pairs.push_back(0);
+      out_pairs.push_back(i);
+      out_ptr.push_back((int64_t)out_pairs.size() / 2);
+    }
+  } else {
+    std::vector<int64_t> labels(total > 0 ? total : 0);
+    for (int64_t i = 0; i < total; ++i) labels[i] = i;
+    while (labels.size() > 1) {
+      std::vector<int64_t> next;
+      for (size_t i = 0; i + 1 < labels.size(); i += 2) {
+        out_pairs.push_back(labels[i]);
+        out_pairs.push_back(labels[i + 1]);
+        next.push_back(labels[i]);
+      }
+      if (labels.size() % 2) next.push_back(labels.back());
+      out_ptr.push_back((int64_t)out_pairs.size() / 2);
+      labels.swap(next);
+    }
+  }
+  *n_pairs = (int64_t)out_pairs.size() / 2;
+  *n_rounds = (int64_t)out_ptr.size() - 1;
+  if (pairs && round_ptr) {
+    if (cap < *n_pairs) return codec::fail(CODEC_ERR_VALUE, "pair buffer holds %lld of %lld", (long long)cap,
+                                           (long long)*n_pairs);
+    std::copy(out_pairs.begin(), out_pairs.end(), pairs);
+    std::copy(out_ptr.begin(), out_ptr.end(), round_ptr);
+  }
+  return CODEC_OK;
+}

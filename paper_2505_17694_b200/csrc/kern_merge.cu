@@ -145,6 +145,59 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
 
 int32_t cuda_status(cudaError_t e, const char* what);
 
+// reduce_tree() on the device (codec_merge_partials): request i folds the
+// partials slot[ptr[i] .. ptr[i+1]) given in the reference's PartialResult
+// layout (out [slot][h_q][d] normalised, m / s [slot][h_q]); one warp per
+// (request, head). Empty entries (s = 0) drop out; the exp-sum of the
+// result goes to out_s so the host can raise NoVisibleTokens.
+template <typename A>
+__global__ void __launch_bounds__(128) merge_csr_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ slot,
+                                                        int n_req, int h_q, int d, const A* __restrict__ po,
+                                                        const A* __restrict__ pm, const A* __restrict__ ps,
+                                                        A* __restrict__ out, A* __restrict__ out_s) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * 4 + warp;
+  if (e >= (int64_t)n_req * h_q) return;
+  const int r = (int)(e / h_q), h = (int)(e % h_q);
+  const int p0 = ptr[r], p1 = ptr[r + 1];
+  A M = neg_inf<A>();
+  for (int p = p0; p < p1; ++p) {
+    const int64_t x = (int64_t)slot[p] * h_q + h;
+    if (ps[x] > 0) M = max(M, pm[x]);
+  }
+  A L = 0;
+  for (int p = p0; p < p1; ++p) {
+    const int64_t x = (int64_t)slot[p] * h_q + h;
+    if (ps[x] > 0) L += ps[x] * exp_acc(pm[x] - M);
+  }
+  A* dst = out + e * d;
+  for (int c = lane; c < d; c += 32) {
+    A acc = 0;
+    for (int p = p0; p < p1; ++p) {
+      const int64_t x = (int64_t)slot[p] * h_q + h;
+      if (ps[x] > 0) acc += ps[x] * exp_acc(pm[x] - M) * po[x * d + c];
+    }
+    dst[c] = L > 0 ? acc / L : A(0);
+  }
+  if (lane == 0) out_s[e] = L;
+}
+
+int32_t launch_merge_csr(int dtype, int n_req, int h_q, int d, const int32_t* ptr, const int32_t* slot,
+                         const void* po, const void* pm, const void* ps, void* out, void* out_s, cudaStream_t st) {
+  const int64_t warps = (int64_t)n_req * h_q;
+  if (warps == 0) return CODEC_OK;
+  const dim3 grid((unsigned)((warps + 3) / 4));
+  if (dtype == CODEC_F64)
+    merge_csr_kernel<double><<<grid, 128, 0, st>>>(ptr, slot, n_req, h_q, d, (const double*)po, (const double*)pm,
+                                                    (const double*)ps, (double*)out, (double*)out_s);
+  else if (dtype == CODEC_F32)
+    merge_csr_kernel<float><<<grid, 128, 0, st>>>(ptr, slot, n_req, h_q, d, (const float*)po, (const float*)pm,
+                                                   (const float*)ps, (float*)out, (float*)out_s);
+  else
+    return fail(CODEC_ERR_UNSUPPORTED, "merge: partials must be float32 or float64");
+  return cuda_status(cudaGetLastError(), "merge launch");
+}
+
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
                      int tc_ctas, bool pdl) {
@@ -185,3 +238,14 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
 }
 
 }  // namespace codec
+
+extern "C" int32_t codec_merge_partials(int32_t dtype, int32_t n_req, int32_t h_q, int32_t d, const int32_t* ptr,
+                                        const int32_t* slot, const void* part_out, const void* part_m,
+                                        const void* part_s, void* out, void* out_s, void* stream) {
+  if (n_req < 0 || h_q < 1 || d < 1) return codec::fail(CODEC_ERR_DIMENSION_MISMATCH, "bad merge dims (%d, %d, %d)",
+                                                         n_req, h_q, d);
+  if (!ptr || !slot || !part_out || !part_m || !part_s || !out || !out_s)
+    return codec::fail(CODEC_ERR_VALUE, "NULL argument");
+  return codec::launch_merge_csr(dtype, n_req, h_q, d, ptr, slot, part_out, part_m, part_s, out, out_s,
+                                 (cudaStream_t)stream);
+}

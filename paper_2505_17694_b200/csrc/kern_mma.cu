@@ -43,6 +43,15 @@ namespace codec {
 #ifndef CODEC_MMA_STAGES
 #define CODEC_MMA_STAGES 2  // 2 x 16 KB per CTA, 6 CTAs per SM: more CTAs beat deeper rings (~5 % on cfg2)
 #endif
+// L2 prefetch beyond the SMEM ring: chunks ahead of the TMA loads (0: off),
+// issued CODEC_MMA_PF_GROUP chunks per bulk-prefetch op (the SM's TMA unit
+// pays per op, not per byte): more bytes in flight per CTA without SMEM
+#ifndef CODEC_MMA_PF
+#define CODEC_MMA_PF 0  // measured: 4 ahead (2 per op) slowed the suffix stream 90 -> 129 us on cfg2
+#endif
+#ifndef CODEC_MMA_PF_GROUP
+#define CODEC_MMA_PF_GROUP 2
+#endif
 constexpr int kMmaWarps = 2;                       // consumer warps
 constexpr int kMmaThreads = 32 * (kMmaWarps + 1);  // + producer warp
 constexpr int kMmaStages = CODEC_MMA_STAGES;
@@ -65,7 +74,8 @@ __device__ __forceinline__ uint32_t mma_sw(int r, int c) {
 __global__ void __launch_bounds__(kMmaThreads, 6)
     mma_pac_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                    const int32_t* __restrict__ table, int off_groups, int off_rows,
-                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
+                   const __nv_bfloat16* __restrict__ q, const uint8_t* __restrict__ kpool,
+                   const uint8_t* __restrict__ vpool, int64_t pool_tokens, int g, int hq_local,
                    float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                    int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog,
                    const int32_t* __restrict__ page_table, int page_shift) {
@@ -99,16 +109,42 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
     if (lane == 0) {
       tc::prefetch_tmap(&tmk);
       tc::prefetch_tmap(&tmv);
+      // pool row of chunk c (logical token; paged pool: a 32-token box
+      // never crosses a page)
+      auto chunk_row = [&](int c) {
+        int x = kv_tok + c * kMmaCT;
+        if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
+        return (int64_t)kh * pool_tokens + x;
+      };
+      // L2 prefetch of chunks [c0, c0 + n) (paged: chunk by chunk)
+      auto prefetch = [&](int c0, int n) {
+        if (c0 >= nch) return;
+        n = min(n, nch - c0);
+        if (!page_shift) {
+          const int64_t y = chunk_row(c0);
+          const uint32_t bytes = (uint32_t)min(n * kMmaCT, n_tok - c0 * kMmaCT) * 256;  // within the slice
+          tc::bulk_prefetch_l2(kpool + y * 256, bytes);
+          tc::bulk_prefetch_l2(vpool + y * 256, bytes);
+        } else {
+          for (int i = 0; i < n; ++i) {
+            const int64_t y = chunk_row(c0 + i);
+            tc::bulk_prefetch_l2(kpool + y * 256, kMmaBox);
+            tc::bulk_prefetch_l2(vpool + y * 256, kMmaBox);
+          }
+        }
+      };
+      if (CODEC_MMA_PF > 0) prefetch(kMmaStages, CODEC_MMA_PF);
       for (int c = 0; c < nch; ++c) {
         const int s = c % kMmaStages;
         if (c >= kMmaStages) mbar_wait(&empty[s], ((c / kMmaStages) - 1) & 1);
         uint8_t* st = smem + s * kMmaStageBytes;
-        int x = kv_tok + c * kMmaCT;  // logical token; paged pool: a 32-token box never crosses a page
-        if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
-        const int y = kh * (int)pool_tokens + x;
+        const int y = (int)chunk_row(c);
         mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
         tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
         tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
+        // keep CODEC_MMA_PF chunks beyond the ring requested, in groups
+        if (CODEC_MMA_PF > 0 && c % CODEC_MMA_PF_GROUP == 0)
+          prefetch(c + kMmaStages + CODEC_MMA_PF, CODEC_MMA_PF_GROUP);
       }
     }
   } else {
@@ -334,7 +370,7 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   cfg.attrs = attr;
   cfg.numAttrs = after_tc ? 1 : 0;
   e = cudaLaunchKernelEx(&cfg, mma_pac_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
-                         pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
+                         (const uint8_t*)k, (const uint8_t*)v, pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
                          off_merge_slot, ctalog, page_table, page_shift);
   if (e != cudaSuccess) return cuda_status(e, "mma gemv launch");
   return cuda_status(cudaGetLastError(), "mma gemv launch");

@@ -62,7 +62,10 @@ constexpr int kTcQWarp = kTcSoftmaxWarps + 3;          // gathers the next unit'
 constexpr int kTcThreads = 32 * (kTcSoftmaxWarps + 4);
 constexpr int kTcBN = 128;                   // tokens per KV tile
 constexpr int kTcD = 128;                    // head dim
-constexpr int kTcPrefetch = 4;               // tiles ahead the producer warms L2
+#ifndef CODEC_TC_PREFETCH
+#define CODEC_TC_PREFETCH 4
+#endif
+constexpr int kTcPrefetch = CODEC_TC_PREFETCH;  // tiles ahead the producer warms L2
 constexpr int kQBytes = 128 * 128 * 2;       // this CTA's 128-row Q tile (32 KB)
 constexpr int kQAtom = kQBytes / 2;          // Q atom column: 128 rows x 64 d (16 KB)
 constexpr int kHalfBytes = 64 * 128 * 2;     // this CTA's half of a K or V tile (16 KB)
@@ -329,18 +332,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // K half: tokens [64 rank, 64 rank + 64) x all 128 d (two SW128 atom
     // columns), completing on the leader's k_full. Also warms L2 with the
     // K and V tiles kTcPrefetch ahead.
+    // L2 warming runs kTcPrefetch tiles ahead of the loads over the block's
+    // whole tile sequence -- across unit boundaries, so a new unit's first
+    // tiles do not start cold from HBM
+    TileCursor pfc{table, off_groups, off_rows, g_begin, g_end, 0, 0, {}};
+    pfc.open();
+    int t_pf = 0;
+    auto prefetch_to = [&](int limit) {
+      for (; !pfc.done() && t_pf < limit; ++t_pf, pfc.next()) {
+        if (dbg & CODEC_FLAG_DBG_NO_LOADS) continue;
+        const int xp = pfc.gv.kv_tok + pfc.j * kTcBN;
+        const int ypk = prow(pfc.gv.kh, xp + 64 * rank), ypv = prow(pfc.gv.kh, xp);
+        if (tc::elect_one()) {
+          tc::tma_prefetch_2d(&tmk, 0, ypk);
+          tc::tma_prefetch_2d(&tmk, 64, ypk);
+          tc::tma_prefetch_2d(&tmv, 64 * rank, ypv);
+        }
+        __syncwarp();
+      }
+    };
+    prefetch_to(kTcPrefetch);
     int t = 0;
     for (int gi = g_begin; gi < g_end; ++gi) {
       const GroupView gv = group_view(table, off_groups, off_rows, gi);
-      if (tc::elect_one()) {
-        for (int j = 0; j < kTcPrefetch && j < gv.n_tiles; ++j) {
-          const int yk = prow(gv.kh, gv.kv_tok + j * kTcBN + 64 * rank), yv = prow(gv.kh, gv.kv_tok + j * kTcBN);
-          tc::tma_prefetch_2d(&tmk, 0, yk);
-          tc::tma_prefetch_2d(&tmk, 64, yk);
-          tc::tma_prefetch_2d(&tmv, 64 * rank, yv);
-        }
-      }
-      __syncwarp();
       for (int j = 0; j < gv.n_tiles; ++j, ++t) {
         const int ks = t % kTcKStages;
         PROG(3, t, 1);
@@ -354,15 +368,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           const int yk = prow(gv.kh, gv.kv_tok + j * kTcBN + 64 * rank);
           tc::tma_load_2d_pair(kd, &tmk, 0, yk, &bars->k_full[ks]);
           tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, yk, &bars->k_full[ks]);
-          if (j + kTcPrefetch < gv.n_tiles) {
-            const int xp = gv.kv_tok + (j + kTcPrefetch) * kTcBN;
-            const int ypk = prow(gv.kh, xp + 64 * rank), ypv = prow(gv.kh, xp);
-            tc::tma_prefetch_2d(&tmk, 0, ypk);
-            tc::tma_prefetch_2d(&tmk, 64, ypk);
-            tc::tma_prefetch_2d(&tmv, 64 * rank, ypv);
-          }
         }
         __syncwarp();
+        prefetch_to(t + 1 + kTcPrefetch);
       }
     }
   } else if (warp == kTcVProducerWarp) {

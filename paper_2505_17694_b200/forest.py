@@ -364,80 +364,73 @@ def node_query_set(forest: Forest, node: int) -> tuple:
     return forest.node(node).query_set
 
 
-def _preorder(nodes, children):
-    off = [0] * len(nodes)
-    pos, stack = 0, [ROOT]
-    while stack:
-        nid = stack.pop()
-        off[nid] = pos
-        pos += nodes[nid].len
-        stack.extend(reversed(children[nid]))
-    return off
+_VIOLATION_CODES = ("BadNodeIndex", "NonEmptyRoot", "EmptyNonRootNode", "DimensionMismatch", "CycleDetected",
+                    "DanglingParent", "AdjacencyMismatch", "PathNotPrefixChain", "QuerySetUnsorted",
+                    "QuerySetPathMismatch", "VisibleLenOutOfRange", "FlattenMismatch")
+
+
+_NONE = -(2 ** 63)  # codec_report_get's None
+
+
+def _csr(lists):
+    ptr = np.zeros(len(lists) + 1, dtype=np.int64)
+    ptr[1:] = np.cumsum([len(x) for x in lists]) if lists else []
+    idx = np.fromiter((int(v) for x in lists for v in x), dtype=np.int64, count=int(ptr[-1]))
+    return ptr, (idx if len(idx) else np.zeros(1, np.int64))
 
 
 def validate(forest: Forest) -> list:
-    """Every structural invariant, reported as a list of violations
-    instead of raised (forest.py:266-363)."""
-    out = []
+    """Every structural invariant, reported as a list of violations instead
+    of raised -- the contract of the reference's validate()
+    (forest.py:266-363): same codes, messages and order. The checks run in
+    the library (codec_forest_validate, csrc/host_validate.cpp) over a flat
+    snapshot of the forest object."""
     nodes = forest.nodes
-    for i, node in enumerate(nodes):
-        if node.id != i:
-            out.append(Violation("BadNodeIndex", f"nodes[{i}] has id {node.id}", node=i))
-    if nodes and nodes[ROOT].len != 0:
-        out.append(Violation("NonEmptyRoot", "virtual root must hold no tokens", node=ROOT))
-    for node in nodes[1:]:
-        if node.len < 1:
-            out.append(Violation("EmptyNonRootNode", f"node {node.id} has len 0", node=node.id))
-        if node.keys is not None:
-            if _shape(node.keys) != _shape(node.values):
-                out.append(Violation("DimensionMismatch", f"node {node.id} K/V shapes differ", node=node.id))
-            elif _shape(node.keys)[1:] != (forest.h_kv, forest.d):
-                out.append(Violation("DimensionMismatch",
-                                     f"node {node.id} is {_shape(node.keys)[1:]}, forest is ({forest.h_kv}, {forest.d})",
-                                     node=node.id))
-    for node in nodes[1:]:
-        seen, cur, ok = {node.id}, node.parent, True
-        while cur != ROOT:
-            if cur in seen or not 0 <= cur < len(nodes):
-                out.append(Violation("CycleDetected", f"parent chain of node {node.id} never reaches root", node=node.id))
-                ok = False
-                break
-            seen.add(cur)
-            cur = nodes[cur].parent
-        if ok and node.parent >= len(nodes):
-            out.append(Violation("DanglingParent", f"node {node.id} parent {node.parent} missing", node=node.id))
-    adjacency = {(nodes[c].parent, c) for kids in forest.children for c in kids}
-    declared = {(n.parent, n.id) for n in nodes[1:]}
-    if adjacency != declared:
-        out.append(Violation("AdjacencyMismatch", "children lists disagree with parent fields"))
-    for rid, path in enumerate(forest.paths):
-        prev = ROOT
-        for nid in path:
-            if not 1 <= nid < len(nodes) or nodes[nid].parent != prev:
-                out.append(Violation("PathNotPrefixChain", f"request {rid} path {path} breaks at {nid}", request=rid))
-                break
-            prev = nid
-    for node in nodes[1:]:
-        if list(node.query_set) != sorted(set(node.query_set)):
-            out.append(Violation("QuerySetUnsorted", f"node {node.id} query_set not ascending", node=node.id))
-        for rid in node.query_set:
-            if rid >= forest.bs or node.id not in forest.paths[rid]:
-                out.append(Violation("QuerySetPathMismatch",
-                                     f"node {node.id} lists request {rid} whose path misses it",
-                                     node=node.id, request=rid))
-    for rid, path in enumerate(forest.paths):
-        for nid in path:
-            if 0 <= nid < len(nodes) and rid not in nodes[nid].query_set:
-                out.append(Violation("QuerySetPathMismatch",
-                                     f"request {rid} runs through node {nid} but is not in its query_set",
-                                     node=nid, request=rid))
-    for node in nodes[1:]:
-        if node.visible_len:
-            for rid, count in node.visible_len.items():
-                if not 1 <= count <= node.len:
-                    out.append(Violation("VisibleLenOutOfRange",
-                                         f"node {node.id} visible_len[{rid}]={count} outside 1..{node.len}",
-                                         node=node.id, request=rid))
-    if forest.token_offset != _preorder(nodes, forest.children):
-        out.append(Violation("FlattenMismatch", "token offsets are not the preorder prefix sums"))
-    return out
+    n = len(nodes)
+    ids = np.array([nd.id for nd in nodes] or [0], dtype=np.int64)
+    parent = np.array([nd.parent for nd in nodes] or [0], dtype=np.int64)
+    length = np.array([nd.len for nd in nodes] or [0], dtype=np.int64)
+    kv_state = np.zeros(max(n, 1), dtype=np.int32)
+    tails = [()] * n
+    for i, nd in enumerate(nodes[1:], start=1):
+        if nd.keys is None:
+            continue
+        if _shape(nd.keys) != _shape(nd.values):
+            kv_state[i] = 1
+        else:
+            kv_state[i], tails[i] = 2, _shape(nd.keys)[1:]
+    t_ptr, t_idx = _csr(tails)
+    c_ptr, c_idx = _csr(list(forest.children) + [[]] * max(0, n - len(forest.children)))
+    p_ptr, p_idx = _csr(forest.paths)
+    q_ptr, q_idx = _csr([nd.query_set for nd in nodes])
+    vn, vr, vc = [], [], []
+    for i, nd in enumerate(nodes[1:], start=1):
+        for rid, cnt in (nd.visible_len or {}).items():
+            vn.append(i)  # position; the message uses that node's id and len
+            vr.append(int(rid))
+            vc.append(int(cnt))
+    n_vis = len(vn)
+    vn, vr, vc = (np.array(x or [0], dtype=np.int64) for x in (vn, vr, vc))
+    off = np.array(list(forest.token_offset) or [0], dtype=np.int64)
+    P64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+    L = _lib.lib()
+    h = C.c_void_p()
+    _lib.check(L.codec_forest_validate(n, P64(ids), P64(parent), P64(length),
+                                       kv_state.ctypes.data_as(C.POINTER(C.c_int32)), P64(t_ptr), P64(t_idx),
+                                       forest.h_kv, forest.d, P64(c_ptr), P64(c_idx), forest.bs, P64(p_ptr),
+                                       P64(p_idx), P64(q_ptr), P64(q_idx), n_vis, P64(vn), P64(vr), P64(vc),
+                                       P64(off), len(forest.token_offset), C.byref(h)))
+    try:
+        cnt = C.c_int64()
+        _lib.check(L.codec_report_count(h, C.byref(cnt)))
+        out = []
+        code, node, req = C.c_int32(), C.c_int64(), C.c_int64()
+        msg = C.create_string_buffer(4096)
+        for i in range(cnt.value):
+            _lib.check(L.codec_report_get(h, i, C.byref(code), C.byref(node), C.byref(req), msg, len(msg)))
+            out.append(Violation(_VIOLATION_CODES[code.value], msg.value.decode(),
+                                 node=None if node.value == _NONE else int(node.value),
+                                 request=None if req.value == _NONE else int(req.value)))
+        return out
+    finally:
+        L.codec_report_free(h)

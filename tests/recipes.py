@@ -148,3 +148,80 @@ def multi_tree_spec(seed, n_trees=5, h_q=8, h_kv=4, d=16, with_masks=True):
                     spec.visible[nid][rid] = int(rng.integers(1, ln + 1))
     spec.queries = rng.standard_normal((spec.bs, h_q, d)) * scale
     return spec
+
+
+# Corruptions applied to a built forest object (reference or ours) for the
+# validate() goldens: (name, fn(forest)). Each breaks one or more of the
+# invariants reference forest.py:266-363 reports.
+def _mut(name):
+    def apply(f):
+        import numpy as _np
+        if name == "bad_id":
+            f.nodes[2].id = 7
+        elif name == "cycle":
+            f.nodes[1].parent = 2
+        elif name == "dangling":
+            f.nodes[3].parent = 40
+        elif name == "path_break":
+            f.paths[0] = (2, 1)
+        elif name == "qset_unsorted":
+            f.nodes[2].query_set = (1, 0)
+        elif name == "qset_foreign":
+            f.nodes[3].query_set = (5,)
+        elif name == "qset_negative":
+            f.nodes[3].query_set = (-1,)
+        elif name == "visible_range":
+            f.nodes[3].visible_len = {2: 9, 1: 0}
+        elif name == "flatten":
+            f.token_offset[2] = 99
+        elif name == "adjacency":
+            f.children[1] = [3]
+        elif name == "kv_tail":
+            f.nodes[2].keys = _np.zeros((3, 3, 4))
+            f.nodes[2].values = _np.zeros((3, 3, 4))
+        elif name == "kv_differ":
+            f.nodes[2].values = _np.zeros((2, 2, 4))
+        elif name == "kv_2d":
+            f.nodes[3].keys = _np.zeros((4, 8))
+            f.nodes[3].values = _np.zeros((4, 8))
+        elif name == "many":
+            f.nodes[1].parent = 3
+            f.paths[1] = (1, 9)
+            f.nodes[2].query_set = (0, 0)
+        elif name != "clean":
+            raise ValueError(name)
+    return apply
+
+
+VALIDATE_CASES = ["clean", "bad_id", "cycle", "dangling", "path_break", "qset_unsorted", "qset_foreign",
+                  "qset_negative", "visible_range", "flatten", "adjacency", "kv_tail", "kv_differ", "kv_2d", "many"]
+
+
+def validate_forest_specs(seed=0):
+    """the small forest the validate() goldens corrupt: (specs, paths)"""
+    rng = np.random.default_rng(seed)
+    t = lambda n: rng.standard_normal((n, 2, 4))
+    specs = [(0, t(5), t(5)), (1, t(3), t(3), {0: 2}), (1, t(4), t(4))]
+    return specs, [(1, 2), (1, 3), (1,)]
+
+
+def mutate(forest, name):
+    _mut(name)(forest)
+    return forest
+
+
+# Profile CSVs the reference's load_profile / CostTable reject (or accept),
+# for the error-contract goldens (cost_model.py:39-53, :102-150).
+PROFILE_CASES = {
+    "ok": "# src=x\n# a=1\nn_q,n,cost_ms\n1,512,0.5\n2,512,0.75\n1,1024,1.0\n2,1024,1.5\n",
+    "no_body": "# only=meta\n\n",
+    "bad_header": "n,n_q,cost_ms\n1,512,0.5\n",
+    "bad_int": "n_q,n,cost_ms\n1,512,0.5\nx,1024,1.0\n",
+    "short_row": "n_q,n,cost_ms\n1,512\n",
+    "duplicate": "n_q,n,cost_ms\n1,512,0.5\n2,512,-1\n1,512,0.7\n",
+    "non_positive": "n_q,n,cost_ms\n1,512,0.5\n2,512,-0.25\n2,512,0.7\n",
+    "non_positive_int": "n_q,n,cost_ms\n1,512,0\n",
+    "missing": "n_q,n,cost_ms\n1,512,0.5\n2,512,0.75\n1,1024,1.0\n",
+    "knot_zero": "n_q,n,cost_ms\n0,512,0.5\n",
+    "extra_field": "n_q,n,cost_ms\n1,512,0.5,9\n",
+}

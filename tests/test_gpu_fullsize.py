@@ -273,14 +273,19 @@ class TestScoreExtremes:
 # ------------------------------------------------------------ other shapes
 class TestShapes:
     def test_sixteen_q_heads_per_kv_head(self, table):
-        """g = 16 (128 q / 8 kv heads): the root on the tensor cores (8
-        requests per 128-row tile), the suffixes on the generic kernel."""
+        """g = 16 (128 q / 8 kv heads): every node has >= 16 query-head rows,
+        so the tensor-core kernel takes them all (8 requests per 128-row
+        tile); without it the suffixes fall to the generic kernel (the GEMV
+        kernels stop at 8 rows)."""
         spec = W.two_level(1500, 180, 20, h_q=128, h_kv=8, d=128, seed=3, tensors=False)
         f, kp, vp, q = _bf16_forest(spec, 3)
+        ref = oracle_requests(f, kp, vp, q, list(range(f.bs)))
         st = DecodeStep(f, P.plan_device(f, 16, table, 8, 148), 128, "bfloat16")
-        assert st.info.n_tc_groups > 0 and st.info.n_gen_groups > 0 and st.info.n_gemv_groups == 0
-        out = st(q, kp, vp).double().cpu().numpy()
-        close(out, oracle_requests(f, kp, vp, q, list(range(f.bs))), "g=16")
+        assert st.info.n_tc_groups > 0 and st.info.n_gemv_groups == 0
+        close(st(q, kp, vp).double().cpu().numpy(), ref, "g=16 tensor cores")
+        st = DecodeStep(f, P.plan_device(f, 16, table, 8, 148), 128, "bfloat16", flags=FLAG_NO_TC)
+        assert st.info.n_gen_groups > 0 and st.info.n_gemv_groups == 0 and st.info.n_tc_groups == 0
+        close(st(q, kp, vp).double().cpu().numpy(), ref, "g=16 generic kernel")
 
     def test_paged_grow_matches_rebuilt_step(self, table):
         """grow() on a paged step (the group records carry their slice start)."""

@@ -456,3 +456,32 @@ class TestGrow:
             assert np.array_equal(np_(out), np_(ref)), k
         with pytest.raises(ValueError, match="no room"):
             step.grow(cap)
+
+
+class TestReduceTree:
+    def test_partial_tree_matches_goldens(self, cuda_ok, table):
+        """reduce_tree() over a PartialTree built like the reference's split
+        phase (executor.py:145-206: rows with visible > start, per-row
+        visible clipped to the slice) from codec_pac partials equals the
+        reference's execute() / naive outputs (fp64, 1e-10)."""
+        z = golden_npz()
+        for doc in golden_json("forests.json")["forests"][:16]:
+            spec = random_forest_spec(doc["seed"], with_masks=doc["masks"])
+            f, q = build(spec)
+            plan = P.plan_uniform_bk(P.tasks_from_forest(f), table, 4, doc["bk"])
+            pt = P.PartialTree()
+            qq = np.asarray(q.queries)
+            for st in plan.subtasks:
+                si = pt.slice_count.get(st.node, 0)
+                pt.slice_count[st.node] = si + 1
+                rows = tuple(r for r in f.node(st.node).query_set if f.visible_count(st.node, r) > st.start)
+                if not rows:
+                    continue
+                vis = [min(f.visible_count(st.node, r), st.stop) - st.start for r in rows]
+                node = f.node(st.node)
+                pt.entries[(st.node, si)] = P.pac(qq[list(rows)], node.keys[st.start:st.stop],
+                                                  node.values[st.start:st.stop], visible=vis)
+                pt.rows[(st.node, si)] = rows
+            out = np_(P.reduce_tree(pt, f, P.BlockPool(1)))
+            assert rel_err(out, z[f"exec_u_{doc['seed']}"]) <= 1e-10
+            assert rel_err(out, z[f"naive_{doc['seed']}"]) <= 1e-10

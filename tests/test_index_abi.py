@@ -132,3 +132,17 @@ class TestAbiSurface:
     def test_status_maps_to_reference_errors(self):
         with pytest.raises(PathNotPrefixChain):
             P.build_forest([(0, *kv(4))], [(2,)])
+
+
+def test_validate_goldens():
+    """validate() (codec_forest_validate) on corrupted forests reports what
+    the reference's validate() reported (tests/golden/validate.json: codes,
+    messages, node / request, order)."""
+    from conftest import golden_json
+    from recipes import VALIDATE_CASES, mutate, validate_forest_specs
+    gold = golden_json("validate.json")
+    for case in VALIDATE_CASES:
+        specs, paths = validate_forest_specs()
+        f = mutate(P.build_forest(specs, paths), case)
+        got = [[v.code, v.message, v.node, v.request] for v in P.validate(f)]
+        assert got == gold[case], case

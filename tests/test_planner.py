@@ -143,3 +143,70 @@ def test_planner_speed_cfg4(tables):
     plan = P.divide_and_schedule(tasks, tables["proxy"], 148)
     dt = time.perf_counter() - t0
     assert plan.makespan_ms > 0 and dt < 5.0
+
+
+def test_profile_error_contract():
+    """load_profile / CostTable / dump_profile against the reference's own
+    results on good and malformed CSVs (tests/golden/profile_errors.json):
+    same exception class and message, same canonical dump."""
+    from recipes import PROFILE_CASES
+    gold = golden_json("profile_errors.json")
+    for name, text in PROFILE_CASES.items():
+        kind, payload = gold[name]
+        if kind == "ok":
+            buf = io.StringIO()
+            P.dump_profile(P.load_profile(io.StringIO(text)), buf)
+            assert buf.getvalue() == payload, name
+        else:
+            with pytest.raises(Exception) as ei:
+                P.load_profile(io.StringIO(text))
+            assert (type(ei.value).__name__, str(ei.value)) == (kind, payload), name
+
+
+def test_cost_table_invariants():
+    from paper_2505_17694_b200.errors import DuplicateKnot, IncompleteGrid, NonPositiveCost
+    with pytest.raises(IncompleteGrid, match=r"grid \(2,\) does not match knots \(1, 2\)"):
+        P.CostTable((1, 2), (512,), np.ones(2))
+    with pytest.raises(DuplicateKnot, match=r"n knots must be strictly ascending positives: \(512, 512\)"):
+        P.CostTable((1,), (512, 512), np.ones((2, 1)))
+    with pytest.raises(NonPositiveCost, match="every grid cost must be > 0"):
+        P.CostTable((1,), (512,), np.zeros((1, 1)))
+    t = P.profile_synthetic(0.01, 1e-5, 2e-6)
+    assert t.cell(5, 2048) == pytest.approx(0.01 + 1e-5 * 2048 + 2e-6 * 2048 * 5, rel=1e-15)
+
+
+def test_merge_schedules_golden():
+    """merge_schedule / sequential_schedule equal the reference's
+    (tests/golden/schedules.json; executor.py:86-117)."""
+    gold = golden_json("schedules.json")
+    for L, counts, rounds in gold["balanced"]:
+        assert [[list(p) for p in rnd] for rnd in P.merge_schedule(L, counts)] == rounds
+    for total, rounds in gold["sequential"]:
+        assert [[list(p) for p in rnd] for rnd in P.sequential_schedule(total)] == rounds
+    assert P.merge_schedule(2, [3, 2]) == [[(0, 1), (2, 3)], [(0, 2)], [(0, 4)]]  # test_executor.py:66-76
+    with pytest.raises(ValueError, match="path_len must be >= 1"):
+        P.merge_schedule(0, [])
+    with pytest.raises(ValueError, match="expected 2 per-node slice counts, got 1"):
+        P.merge_schedule(2, [1])
+
+
+def test_run_report_golden():
+    """run_report() equals the reference CLI's RunReport for the same
+    workload points (tests/golden/reports.json, cli.py:130-184), and passes
+    the schema check."""
+    from paper_2505_17694_b200 import workloads as W
+    from paper_2505_17694_b200.report import check_report, run_report
+    table = P.load_profile(io.StringIO(golden_table_text("a100_d128.csv")))
+    for item in golden_json("reports.json"):
+        ref = item["report"]
+        w = ref["workload"]
+        fn = {"two_level": W.two_level, "full_tree": W.full_tree}[w["family"]]
+        spec = fn(**w["params"], **w["dims"], seed=w["seed"], tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, spec.h_kv, spec.d)
+        plan = P.divide_and_schedule(P.tasks_from_forest(f), table, item["blocks"])
+        got = run_report(f, plan, table, item["blocks"], w, element_size=8)
+        assert got == ref
+        check_report(got)
+    bad = dict(got, extra=1)
+    with pytest.raises(ValueError, match="unknown keys"):
+        check_report(bad)

@@ -19,15 +19,16 @@ from paper_2505_17694_b200.executor import DecodeStep  # noqa: E402
 
 budget = int(sys.argv[1]) if len(sys.argv) > 1 else 148
 extra = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+config = sys.argv[3] if len(sys.argv) > 3 else "cfg2"
 dev = torch.device("cuda")
-spec = W.two_level(32768, 512, 256, h_q=32, h_kv=8, d=128, tensors=False)
+spec = W.make_config(config, tensors=False)
 f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
 T = f.total_tokens
 kp = (torch.randn((8, T, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
 vp = (torch.randn((8, T, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
-q = (torch.randn((256, 32, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
-plan = P.plan_device(f, 4, P.load_default_profile(), 8, 148, budget)
-step = DecodeStep(f, plan, 32, "bfloat16", flags=1024 | extra, tc_sm_budget=budget, concurrent=True)
+q = (torch.randn((f.bs, spec.h_q, 128), device=dev) / math.sqrt(128)).to(torch.bfloat16)
+plan = P.plan_device(f, spec.h_q // 8, P.load_default_profile(), 8, 148, budget)
+step = DecodeStep(f, plan, spec.h_q, "bfloat16", flags=1024 | extra, tc_sm_budget=budget, concurrent=True)
 for _ in range(3):
     step(q, kp, vp)
 torch.cuda.synchronize()
