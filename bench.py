@@ -502,11 +502,13 @@ def main():
     total_bytes = work_full["unique_kv_bytes"]
     value = total_bytes / (ms * 1e-3) / 1e9
     g = ns.g
-    tc_rows = sum(n.len for n in ns.forest.nodes[1:] if len(n.query_set) * g >= 16)
-    kv_tc = tc_rows * ns.h_local * d * 2 * 2
+    from paper_2505_17694_b200.scheduler import node_kernel
+    on_tc = [n for n in ns.forest.nodes[1:] if n.query_set and
+             node_kernel(len(n.query_set) * g, len(n.query_set), not (args.flags & 524288)) == "tc"]
+    kv_tc = sum(n.len for n in on_tc) * ns.h_local * d * 2 * 2
     kernels = {}
     if "tc" in phases:
-        fl = sum(n.len * len(n.query_set) for n in ns.forest.nodes[1:] if len(n.query_set) * g >= 16) * hq_local * 4 * d
+        fl = sum(n.len * len(n.query_set) for n in on_tc) * hq_local * 4 * d
         ach = fl / (phases["tc"] * 1e-3) / 1e12
         sms_tc = int(min(budget, ns.sms))
         # timed inside >= 2 s windows of back-to-back steps: the sustained

@@ -269,6 +269,8 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_DBG_NO_LOADS 32768 /* TC producers skip the K/V TMA loads: timing only, wrong output (debug) */
 #define CODEC_FLAG_DBG_ISSUER_ONLY 131072 /* TC kernel runs only its MMA issuer, no waits: timing only (debug) */
 #define CODEC_FLAG_MERGE_NO_PDL 262144 /* launch the merge plainly after the suffix kernel (measurement) */
+#define CODEC_FLAG_NO_MULTI 524288 /* lightly shared slices on the tensor-core (or per-request) kernels instead of
+                                       the multi-request mma.sync kernel */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
 
 typedef struct codec_table codec_table;
@@ -290,6 +292,8 @@ typedef struct {
   int32_t max_merge;                                   /* most partials of one merged (request, head) */
   int32_t n_merge_fused;                               /* further merge entries (after the n_merge) that the
                                                           suffix kernel folds into its own output */
+  int32_t n_multi_groups, off_multi;                   /* lightly shared slices (2..32/g requests) on the
+                                                          multi-request mma.sync kernel */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

@@ -10,6 +10,7 @@ namespace codec {
 constexpr int kKindTc = 0;       // tcgen05 shared-node kernel (bf16, d = 128)
 constexpr int kKindGemv = 1;     // CUDA-core warp-shuffle GEMV kernel
 constexpr int kKindGeneric = 2;  // any dtype / head dim (small or odd shapes)
+constexpr int kKindMulti = 3;    // multi-request mma.sync kernel: 2..kMultiRows/g requests of one slice
 
 // a group record: 8 int32
 constexpr int kGroupInts = 8;
@@ -29,7 +30,13 @@ constexpr int kGrpHead = 7;     // TC: local kv head of the unit
 constexpr int kRowInts = 4;
 
 // minimum query-head rows for a subtask to take the tensor-core kernel
+// (without the multi-request kernel: CODEC_FLAG_NO_MULTI, or shapes it
+// does not cover)
 constexpr int kTcMinRows = 16;
+// with the multi-request kernel: slices of up to kMultiMaxRows query-head
+// rows take it (in groups of kMultiRows rows), larger ones the tensor cores
+constexpr int kMultiRows = 32;
+constexpr int kMultiMaxRows = 64;
 // query-head rows of one tensor-core group (M = 256: one 128-row tile per
 // CTA of a cta_group::2 pair)
 constexpr int kTcGroupRows = 256;

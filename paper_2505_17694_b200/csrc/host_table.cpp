@@ -182,6 +182,12 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
                        (d == 64 || d == 128 || d == 256) && g <= 8 && !(dims->flags & CODEC_FLAG_NO_GEMV);
   const int32_t tc_reqs = tc_ok ? std::max(1, kTcGroupRows / g) : 0;
   const int32_t gemv_rows = g <= 4 ? 4 : 8;
+  // lightly shared slices (2+ requests, <= kMultiMaxRows query-head rows):
+  // the multi-request mma.sync kernel streams them once for all requests
+  const bool multi_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
+                        !(dims->flags & (CODEC_FLAG_NO_MULTI | CODEC_FLAG_GEMV_SIMT | CODEC_FLAG_NO_GEMV));
+  const int32_t multi_reqs = std::max(1, kMultiRows / g);
+  const int64_t tc_min_rows = multi_ok ? kMultiMaxRows + 1 : kTcMinRows;
 
   // ---- rows and slots
   struct Grp {
@@ -211,9 +217,12 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     if (live.empty()) continue;
     int kind;
     int32_t per;
-    if (tc_ok && ((int64_t)live.size() * g >= kTcMinRows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
+    if (tc_ok && ((int64_t)live.size() * g >= tc_min_rows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
       kind = kKindTc;
       per = tc_reqs;
+    } else if (multi_ok && live.size() >= 2) {
+      kind = kKindMulti;
+      per = multi_reqs;
     } else if (gemv_ok) {
       kind = kKindGemv;
       per = 1;
@@ -483,6 +492,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   }
   emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
   emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
+  emit_groups(kKindMulti, in.n_multi_groups, in.off_multi);
   in.off_rows = (int32_t)blob.size();
   in.n_rows = (int32_t)(rows.size() / 4);
   blob.insert(blob.end(), rows.begin(), rows.end());

@@ -338,6 +338,211 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3m: lightly shared nodes -- a slice shared by 2..32/g requests (<= 32
+// query-head rows) -- on the same warp-level tensor cores, so the node's
+// K/V streams from HBM ONCE for all of them (the single-request kernel
+// above would stream it once per request; the tcgen05 kernel would pad the
+// rows to 256). The rows are split across consumer warps by columns: warp
+// w owns query-head rows [8w, 8w + 8) of the group (n = 8 of m16n8k16) and
+// runs every token of every stage for them, so each warp's (m, l, O^T) is
+// final at the end -- no cross-warp merge. Rows of different requests see
+// different visible counts (masks): the per-column limit masks the scores.
+constexpr int kMultiWarps = 4;                          // consumer warps (<= 32 rows)
+constexpr int kMultiThreads = 32 * (kMultiWarps + 1);   // + producer warp
+constexpr int kMultiStages = 4;                         // fewer CTAs per SM than K3: a deeper ring
+constexpr int kMultiSmem = kMultiStages * kMmaStageBytes + 1024 + 2 * kMultiStages * 8;
+
+__global__ void __launch_bounds__(kMultiThreads, 3)
+    mma_multi_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                     const int32_t* __restrict__ table, int off_groups, int off_rows,
+                     const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
+                     float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
+                     const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ done) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMultiStages * kMmaStageBytes);
+  uint64_t* empty = full + kMultiStages;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t* grp = table + off_groups + blockIdx.x * kGroupInts;
+  const int kh = blockIdx.y;
+  const int32_t* rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
+  const int n_req = grp[kGrpNRows];
+  const int n_cols = n_req * g;
+  const int nbw = (n_cols + 7) >> 3;  // busy consumer warps
+  const int nch = (grp[kGrpMaxVis] + kMmaCT - 1) / kMmaCT;
+  const int kv_tok = grp[kGrpKvTok];
+
+  if (tid == 0) {
+    for (int s = 0; s < kMultiStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nbw);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kMultiWarps) {
+    // ---------------- producer: one lane streams 32-token K and V boxes
+    if (lane == 0) {
+      tc::prefetch_tmap(&tmk);
+      tc::prefetch_tmap(&tmv);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c % kMultiStages;
+        if (c >= kMultiStages) mbar_wait(&empty[s], ((c / kMultiStages) - 1) & 1);
+        uint8_t* st = smem + s * kMmaStageBytes;
+        int x = kv_tok + c * kMmaCT;  // paged pool: a 32-token box never crosses a page
+        if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
+        const int y = kh * (int)pool_tokens + x;
+        mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
+        tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
+        tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
+      }
+    }
+  } else if (warp < nbw) {
+    // ---------------- consumer warp: query-head rows [8 warp, 8 warp + 8)
+    const int gid = lane >> 2, tig = lane & 3;
+    const float cscale = 1.4426950408889634f * rsqrtf((float)kMmaD);
+    const int c0 = 8 * warp;
+    uint32_t qf[8][2];  // B fragments of Q^T: k = d, n = row c0 + gid
+    {
+      const int col = c0 + gid, ridx = col / g;
+      const bool hv = col < n_cols;
+      const int req = hv ? rows[ridx * kRowInts] : 0;
+      const uint32_t* qp =
+          reinterpret_cast<const uint32_t*>(q + ((int64_t)req * hq_local + kh * g + col % g) * kMmaD);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        qf[ks][0] = hv ? __ldg(qp + ks * 8 + tig) : 0u;
+        qf[ks][1] = hv ? __ldg(qp + ks * 8 + 4 + tig) : 0u;
+      }
+    }
+    // visible tokens of this lane's two score columns (0: padding column)
+    const int ca = c0 + 2 * tig, cb = ca + 1;
+    const int lim_a = ca < n_cols ? rows[(ca / g) * kRowInts + 1] : 0;
+    const int lim_b = cb < n_cols ? rows[(cb / g) * kRowInts + 1] : 0;
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m_run[2] = {neg_inf<float>(), neg_inf<float>()};
+    float l_run[2] = {0.f, 0.f};
+    const int mat = lane >> 3, rr = lane & 7;
+    for (int c = 0; c < nch; ++c) {
+      const int s = c % kMultiStages;
+      mbar_wait(&full[s], (c / kMultiStages) & 1);
+      const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + kMmaBox;
+#pragma unroll
+      for (int u = 0; u < kMmaCT / 16; ++u) {
+        const int wrow = 16 * u;
+        const int tk_qk = wrow + rr + ((mat & 1) << 3), ck_qk = mat >> 1;
+        const int tk_pv = wrow + rr + ((mat >> 1) << 3), ck_pv = mat & 1;
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          uint32_t a[4];
+          ldsm_x4(kb + mma_sw(tk_qk, 2 * ks + ck_qk), a);
+          hmma(sc, a, qf[ks][0], qf[ks][1]);
+        }
+        // sc[0]: (token gid, col a), [1]: (gid, col b), [2]: (gid+8, a), [3]: (gid+8, b)
+        const int t0 = c * kMmaCT + wrow + gid;
+        sc[0] = t0 < lim_a ? sc[0] * cscale : neg_inf<float>();
+        sc[1] = t0 < lim_b ? sc[1] * cscale : neg_inf<float>();
+        sc[2] = t0 + 8 < lim_a ? sc[2] * cscale : neg_inf<float>();
+        sc[3] = t0 + 8 < lim_b ? sc[3] * cscale : neg_inf<float>();
+        float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        // lazy rescale (threshold 2^8, as in K3)
+        const bool n0 = mx0 > m_run[0] + 8.f, n1 = mx1 > m_run[1] + 8.f;
+        if (__any_sync(0xffffffffu, n0 || n1)) {
+          const float a0 = n0 ? fast_exp2(m_run[0] - mx0) : 1.f;
+          const float a1 = n1 ? fast_exp2(m_run[1] - mx1) : 1.f;
+          l_run[0] *= a0;
+          l_run[1] *= a1;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            acc[i][0] *= a0;
+            acc[i][2] *= a0;
+            acc[i][1] *= a1;
+            acc[i][3] *= a1;
+          }
+          if (n0) m_run[0] = mx0;
+          if (n1) m_run[1] = mx1;
+        }
+        const bool d0 = m_run[0] == neg_inf<float>(), d1 = m_run[1] == neg_inf<float>();
+        const float p0 = d0 ? 0.f : fast_exp2(sc[0] - m_run[0]);
+        const float p1 = d1 ? 0.f : fast_exp2(sc[1] - m_run[1]);
+        const float p2 = d0 ? 0.f : fast_exp2(sc[2] - m_run[0]);
+        const float p3 = d1 ? 0.f : fast_exp2(sc[3] - m_run[1]);
+        l_run[0] += p0 + p2;
+        l_run[1] += p1 + p3;
+        const uint32_t b0 = movm_t(pack2_bf16(p0, p1)), b1 = movm_t(pack2_bf16(p2, p3));
+#pragma unroll
+        for (int dm = 0; dm < 8; ++dm) {
+          uint32_t a[4];
+          ldsm_x4_t(vb + mma_sw(tk_pv, 2 * dm + ck_pv), a);
+          hmma(acc[dm], a, b0, b1);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l_run[0] += __shfl_xor_sync(0xffffffffu, l_run[0], o);
+      l_run[1] += __shfl_xor_sync(0xffffffffu, l_run[1], o);
+    }
+    // every consumer is past the ring: stage (m, l, O^T) of this warp's 8
+    // rows there, then write each row as one 512-byte warp store
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * nbw) : "memory");
+    float* wm = reinterpret_cast<float*>(smem) + warp * (16 + 8 * kMmaD);
+    if (gid == 0) {
+      wm[2 * tig] = m_run[0];
+      wm[2 * tig + 1] = m_run[1];
+      wm[8 + 2 * tig] = l_run[0];
+      wm[8 + 2 * tig + 1] = l_run[1];
+    }
+#pragma unroll
+    for (int dm = 0; dm < 8; ++dm) {
+      const int dd = 16 * dm + gid;
+      wm[16 + (2 * tig) * kMmaD + dd] = acc[dm][0];
+      wm[16 + (2 * tig + 1) * kMmaD + dd] = acc[dm][1];
+      wm[16 + (2 * tig) * kMmaD + dd + 8] = acc[dm][2];
+      wm[16 + (2 * tig + 1) * kMmaD + dd + 8] = acc[dm][3];
+    }
+    __syncwarp();
+    for (int j = 0; j < 8; ++j) {
+      const int col = c0 + j;
+      if (col >= n_cols) break;
+      const int32_t* row = rows + (col / g) * kRowInts;
+      const int req = row[0], slot = row[2], qh = kh * g + col % g;
+      const float M = wm[j], L = wm[8 + j], inv = 1.f / L;
+      const float4 o4 = reinterpret_cast<const float4*>(wm + 16 + j * kMmaD)[lane];
+      const float4 r4 = make_float4(o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
+      if (slot < 0) {
+        reinterpret_cast<float4*>(out + ((int64_t)req * hq_local + qh) * kMmaD)[lane] = r4;
+      } else {
+        const int64_t ei = (int64_t)slot * hq_local + qh;
+        reinterpret_cast<float4*>(part_o + ei * kMmaD)[lane] = r4;
+        if (lane == 0) {
+          part_ml[2 * ei] = M * 0.69314718055994530942f;  // natural-log units
+          part_ml[2 * ei + 1] = L;
+        }
+      }
+    }
+  }
+  // completion count for the merge (it may start before this grid ends)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0 && done) atomicAdd(done, 1);
+}
+
 int32_t cuda_status(cudaError_t e, const char* what);
 int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows);
 
@@ -376,4 +581,34 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   return cuda_status(cudaGetLastError(), "mma gemv launch");
 }
 
+}  // namespace codec
+
+namespace codec {
+int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
+                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
+                         void* part_o, void* part_ml, cudaStream_t st, bool pdl, const int32_t* page_table,
+                         int page_shift, int32_t* done) {
+  if (n_groups == 0) return CODEC_OK;
+  if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "multi-request suffix kernel needs <= 8 query heads per kv head");
+  CUtensorMap mk, mv;
+  CODEC_TRY(encode_pool_rows_map(&mk, k, (int64_t)h_local * pool_tokens, kMmaCT));
+  CODEC_TRY(encode_pool_rows_map(&mv, v, (int64_t)h_local * pool_tokens, kMmaCT));
+  cudaError_t e = cudaFuncSetAttribute(mma_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMultiSmem);
+  if (e != cudaSuccess) return cuda_status(e, "multi smem attribute");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_groups, h_local);
+  cfg.blockDim = dim3(kMultiThreads);
+  cfg.dynamicSmemBytes = kMultiSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, mma_multi_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
+                         pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, page_table,
+                         page_shift, done);
+  if (e != cudaSuccess) return cuda_status(e, "multi launch");
+  return cuda_status(cudaGetLastError(), "multi launch");
+}
 }  // namespace codec

@@ -25,6 +25,10 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
                         long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift);
+int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
+                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
+                         void* part_o, void* part_ml, cudaStream_t st, bool pdl, const int32_t* page_table,
+                         int page_shift, int32_t* done);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -155,8 +159,10 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   const bool do_tc = info->n_tc_groups && !(dims->flags & CODEC_FLAG_SKIP_TC);
   const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
   const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
-  if (do_tc && (dims->kv_dtype != CODEC_BF16 || d != 128))
-    return fail(CODEC_ERR_UNSUPPORTED, "tensor-core groups need bf16, d = 128");
+  const bool do_multi = info->n_multi_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
+  if ((do_tc || do_multi) && (dims->kv_dtype != CODEC_BF16 || d != 128 || g > 128))
+    return fail(CODEC_ERR_UNSUPPORTED, "tensor-core / multi-request groups need bf16, d = 128");
+  if (do_multi && g > 8) return fail(CODEC_ERR_UNSUPPORTED, "multi-request groups need <= 8 query heads per kv head");
   // The mma.sync suffix kernel is launched right after the TC kernel on the
   // same stream with programmatic dependent launch: its CTAs start on the
   // SMs the TC grid leaves once every TC CTA is resident (the TC grid gets
@@ -194,18 +200,27 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
     if (cudaEventRecord(fj->fork, st) != cudaSuccess || cudaStreamWaitEvent(side, fj->fork, 0) != cudaSuccess)
       return fail(CODEC_ERR_CUDA, "fork failed");
   }
-  // TC completion counter: the first word of the workspace's reserved tail
+  // completion counter of the TC and multi-request CTAs (the merge may
+  // start before those grids end): the first word of the workspace tail
   int64_t ml_bytes = (int64_t)info->n_slots * hq_local * 2 * elem;
   ml_bytes = (ml_bytes + 255) / 256 * 256;
   int32_t* tc_done = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + o_bytes + ml_bytes);
-  const bool pdl = mma_gemv && do_tc && info->n_merge_fused == 0 && !kev;
-  if (do_tc && cudaMemsetAsync(tc_done, 0, sizeof(int32_t), st) != cudaSuccess)
+  const int done_target = (do_tc ? 2 * info->n_tc_blocks : 0) + (do_multi ? info->n_multi_groups * h_local : 0);
+  // early (programmatic) launches of the kernels after the TC kernel; not
+  // with the fused merge, which reads the TC partials from the suffix kernel
+  const bool early = info->n_merge_fused == 0 && !kev;
+  const bool pdl = mma_gemv && (do_tc || do_multi) && early;
+  if (done_target && cudaMemsetAsync(tc_done, 0, sizeof(int32_t), st) != cudaSuccess)
     return fail(CODEC_ERR_CUDA, "tc counter reset");
   if (kev) CODEC_TRY(kev_record(timer, 0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
                         dims->flags, ctalog, dims->page_table, page_shift, tc_done));
   if (kev) CODEC_TRY(kev_record(timer, 1, st));
+  if (do_multi)
+    CODEC_TRY(launch_mma_multi(table_dev, info->n_multi_groups, info->off_multi, info->off_rows, q, k, v,
+                               dims->pool_tokens, g, h_local, out, part_o, part_ml, st, do_tc && early,
+                               dims->page_table, page_shift, tc_done));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
@@ -224,7 +239,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   }
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st,
-                           do_tc ? tc_done : nullptr, 2 * info->n_tc_blocks,
+                           done_target ? tc_done : nullptr, done_target,
                            mma_gemv && !fork && !kev && !(dims->flags & CODEC_FLAG_SKIP_GEMV) &&
                                !(dims->flags & CODEC_FLAG_MERGE_NO_PDL)));
   if (kev) {

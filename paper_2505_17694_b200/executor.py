@@ -35,6 +35,7 @@ from .forest import Forest, QueryBatch, dtype_code
 FLAG_NO_TC = 1
 FLAG_FORCE_TC = 2
 FLAG_NO_GEMV = 4
+FLAG_NO_MULTI = 524288
 
 
 @dataclass
@@ -164,7 +165,8 @@ class DecodeStep:
     def launches(self) -> int:
         """Kernels one call launches (for the bench's gpu_launches)."""
         i = self.info
-        return int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) + int(bool(i.n_merge))
+        return (int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) +
+                int(bool(i.n_multi_groups)) + int(bool(i.n_merge)))
 
     def __call__(self, q, k_pool, v_pool, out=None, stream=None):
         """q [bs, h_q_local, d] and the pools [h_local, pool_tokens, d] in
@@ -228,7 +230,8 @@ class DecodeStep:
         i, blob = self.info, self.blob_host
         leaf = {n.id for n in self.forest.nodes[1:] if not self.forest.children[n.id]}
         touched, grown = [], {}
-        for off, count in ((i.off_gemv, i.n_gemv_groups), (i.off_gen, i.n_gen_groups)):
+        for off, count in ((i.off_gemv, i.n_gemv_groups), (i.off_gen, i.n_gen_groups),
+                           (i.off_multi, i.n_multi_groups)):
             for gidx in range(count):
                 rec = off + 8 * gidx
                 node = int(blob[rec + 5])

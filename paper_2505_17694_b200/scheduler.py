@@ -137,6 +137,7 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
+MULTI_MAX_ROWS = 64  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
 
@@ -160,29 +161,45 @@ def concat_plans(plans) -> DivisionPlan:
                         cost_l_ms=plans[0].cost_l_ms, search_truncated=any(p.search_truncated for p in plans))
 
 
+def node_kernel(rows: int, n_requests: int, multi: bool = True) -> str:
+    """Which kernel runs a slice with `rows` query-head rows of
+    `n_requests` requests (host_table.cpp's routing for bf16, d = 128,
+    g <= 8): "tc" (tcgen05 shared-node kernel), "multi" (multi-request
+    mma.sync kernel) or "suffix" (single-request mma.sync kernel)."""
+    if rows > (MULTI_MAX_ROWS if multi else TC_MIN_ROWS - 1):
+        return "tc"
+    if multi and n_requests >= 2:
+        return "multi"
+    return "suffix"
+
+
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
-                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT, page_size: int = 0) -> DivisionPlan:
-    """The B200 plan of one decode step. Shared nodes (>= TC_MIN_ROWS query-
-    head rows per chunk) stay whole here: on the tensor cores every KV tile
-    costs the same (an M=256 MMA pair whatever the rows), so the device
-    balancer in the task table (host_table.cpp) divides them itself --
-    stream-K over the CTA pairs, per kv head, into equal tile ranges with
-    the row chunks of a slice in lockstep. Unshared nodes stay whole too
-    (their suffix CTAs are hardware-scheduled and stream at HBM speed
-    regardless of order). Returns one plan over both, in the reference's
-    DivisionPlan form (any reference plan is accepted by execute() as well;
-    its slices then bound the device pieces). With a paged pool
-    (page_size > 0, paging.py) suffix nodes stay whole: a slice must start
-    on a 32-token chunk boundary of its node."""
+                tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT, page_size: int = 0,
+                multi: bool = True) -> DivisionPlan:
+    """The B200 plan of one decode step. Shared nodes (more than
+    MULTI_MAX_ROWS query-head rows per chunk; TC_MIN_ROWS with multi=False)
+    stay whole here: on the tensor cores every KV tile costs the same (an
+    M=256 MMA pair whatever the rows), so the device balancer in the task
+    table (host_table.cpp) divides them itself -- stream-K over the CTA
+    pairs, per kv head, into equal tile ranges with the row chunks of a
+    slice in lockstep. Lightly shared and unshared nodes go to the mma.sync
+    kernels (multi-request / single-request), whose CTAs are
+    hardware-scheduled and stream at HBM speed regardless of order; long
+    ones are cut into slices of <= SUFFIX_SLICE tokens. Returns one plan
+    over both, in the reference's DivisionPlan form (any reference plan is
+    accepted by execute() as well; its slices then bound the device
+    pieces). With a paged pool (page_size > 0, paging.py) those nodes stay
+    whole: a slice must start on a 32-token chunk boundary of its node."""
     tasks = device_tasks(forest, group_size)
-    tc = [t for t in tasks if t.n_q >= TC_MIN_ROWS]
-    gv = [t for t in tasks if t.n_q < TC_MIN_ROWS]
+    g = int(group_size)
+    tc = [t for t in tasks if node_kernel(t.n_q, t.n_q // g, multi) == "tc"]
+    gv = [t for t in tasks if node_kernel(t.n_q, t.n_q // g, multi) != "tc"]
     pairs = max(1, (tc_sm_budget or sm_count) // TC_CTAS_PER_BLOCK)
     plans = []
     if tc:
         plans.append(plan_uniform_bk(tc, table, pairs, 1))
-    # suffix-kernel tasks: one CTA streams a slice at a few tens of GB/s, so
-    # long ones (a lightly shared 128K-token root in cfg4) are cut into
+    # mma.sync-kernel tasks: one CTA streams a slice at a few tens of GB/s,
+    # so long ones (a lightly shared 128K-token root in cfg4) are cut into
     # slices of <= SUFFIX_SLICE tokens that run on separate CTAs
     by_bk = {}
     for t in gv:

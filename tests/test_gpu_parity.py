@@ -13,7 +13,7 @@ from recipes import PAC_SHAPES, pac_inputs, random_forest_spec
 from oracle import attention as OA
 import paper_2505_17694_b200 as P
 from paper_2505_17694_b200 import workloads as W
-from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_TC, DecodeStep
+from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_MULTI, FLAG_NO_TC, DecodeStep
 
 pytestmark = pytest.mark.gpu
 
@@ -215,7 +215,7 @@ def d128_forest(seed, with_masks):
 
 
 class TestBf16Kernels:
-    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC])
+    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC, FLAG_NO_MULTI, FLAG_NO_TC | FLAG_NO_MULTI])
     def test_random_forests(self, cuda_ok, table, flags):
         for seed in range(24):
             spec = d128_forest(seed, with_masks=(seed % 2 == 1))
@@ -485,3 +485,52 @@ class TestReduceTree:
             out = np_(P.reduce_tree(pt, f, P.BlockPool(1)))
             assert rel_err(out, z[f"exec_u_{doc['seed']}"]) <= 1e-10
             assert rel_err(out, z[f"naive_{doc['seed']}"]) <= 1e-10
+
+
+class TestMultiRequestKernel:
+    @pytest.mark.parametrize("g", [1, 2, 4, 8])
+    def test_lightly_shared_nodes(self, cuda_ok, table, g):
+        """Nodes shared by 2..16 requests (<= 64 query-head rows) on the
+        multi-request mma.sync kernel, ragged visible counts per request
+        inside a group (per-column masks), against the oracle and against
+        the same plan with the kernel off (tensor-core / per-request)."""
+        import torch
+        rng = np.random.default_rng(40 + g)
+        h_kv = 4
+        parent, length, paths, vis = [0], [0], [], [None]
+        for t in range(6):
+            root = len(parent)
+            parent.append(0)
+            length.append(int(rng.integers(100, 3000)))
+            vis.append(None)
+            for _ in range(int(rng.integers(2, 17))):
+                parent.append(root)
+                length.append(int(rng.integers(5, 200)))
+                vis.append(None)
+                paths.append((root, len(parent) - 1))
+        bs = len(paths)
+        for r, (root, leaf) in enumerate(paths):  # ragged visibility in the shared roots
+            if rng.random() < 0.4:
+                vis[root] = vis[root] or {}
+                vis[root][r] = int(rng.integers(1, length[root] + 1))
+        spec = W.Spec(h_kv * g, h_kv, 128, parent, length, None, None, paths, None, vis)
+        f = P.forest_from_pool(parent[1:], length[1:], paths, h_kv, 128, visible=vis[1:])
+        gen = torch.Generator().manual_seed(g)
+        T = f.total_tokens
+        kp = (torch.randn((h_kv, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        vp = (torch.randn((h_kv, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        q = (torch.randn((bs, h_kv * g, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        plan = P.plan_device(f, g, table, h_kv, 148)
+        multi = DecodeStep(f, plan, h_kv * g, "bfloat16")
+        assert multi.info.n_multi_groups > 0
+        got = np_(multi(q, kp, vp))
+        off = np_(DecodeStep(f, plan, h_kv * g, "bfloat16", flags=FLAG_NO_MULTI)(q, kp, vp))
+        z = np.zeros((0, h_kv, 128))
+        node = lambda pool, n: pool[:, f.token_offset[n]:f.token_offset[n] + length[n]].permute(1, 0, 2).double().cpu().numpy()
+        fd = OA.ForestData(parent, [z] + [node(kp, n) for n in range(1, len(parent))],
+                           [z] + [node(vp, n) for n in range(1, len(parent))], paths, vis)
+        ref = OA.naive_attention(q.double().cpu().numpy(), fd)
+        assert_bf16_close(got, ref)
+        assert_bf16_close(off, ref)
+        # the same inputs, the same step: bit-repeatable
+        assert np.array_equal(np_(multi(q, kp, vp)), got)
