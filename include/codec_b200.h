@@ -271,6 +271,8 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_MERGE_NO_PDL 262144 /* launch the merge plainly after the suffix kernel (measurement) */
 #define CODEC_FLAG_NO_MULTI 524288 /* lightly shared slices on the tensor-core (or per-request) kernels instead of
                                        the multi-request mma.sync kernel */
+#define CODEC_FLAG_COUNTED_MERGE 1048576 /* partial producers count per merge entry and the merge starts each entry
+                                            as soon as it is complete (opt-in: measured no faster on cfg2/cfg3) */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
 
 typedef struct codec_table codec_table;
@@ -294,6 +296,8 @@ typedef struct {
                                                           suffix kernel folds into its own output */
   int32_t n_multi_groups, off_multi;                   /* lightly shared slices (2..32/g requests) on the
                                                           multi-request mma.sync kernel */
+  int32_t off_entry_of;                                /* [bs][h_local] merge entry of (request, kv head), -1 none */
+  int32_t reserved1;
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

@@ -504,6 +504,15 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   blob.insert(blob.end(), merge_ptr.begin(), merge_ptr.end());
   in.off_merge_slot = (int32_t)blob.size();
   blob.insert(blob.end(), merge_slot.begin(), merge_slot.end());
+  // (request, local kv head) -> merge entry (-1: the head's only partial is
+  // written straight to the output): partial producers count themselves in
+  // per-entry counters the merge waits on
+  {
+    std::vector<int32_t> entry_of((size_t)bs * h_local, -1);
+    for (size_t e = 0; e < merge_req.size(); ++e) entry_of[merge_req[e]] = (int32_t)e;
+    in.off_entry_of = (int32_t)blob.size();
+    blob.insert(blob.end(), entry_of.begin(), entry_of.end());
+  }
   while (blob.size() % 4) blob.push_back(0);
   in.blob_len = (int64_t)blob.size();
   in.n_slots = n_slots;
@@ -513,7 +522,10 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   o_bytes = (o_bytes + 255) / 256 * 256;
   // partial outputs, partial (m, l), then 256 reserved bytes
   int64_t ml_bytes = ((int64_t)n_slots * hq_local * 2 * elem + 255) / 256 * 256;
-  in.workspace_bytes = o_bytes + ml_bytes + 256;
+  // partial outputs, partial (m, l), a 256-byte block (TC completion
+  // counter), then one int32 readiness counter per merge entry
+  const int64_t cnt_bytes = ((int64_t)merge_req.size() * 4 + 255) / 256 * 256;
+  in.workspace_bytes = o_bytes + ml_bytes + 256 + cnt_bytes;
   *out = t;
   return CODEC_OK;
 }

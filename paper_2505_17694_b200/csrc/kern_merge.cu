@@ -95,8 +95,27 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
                                                        int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
                                                        const float* __restrict__ part_ml, float* __restrict__ out,
-                                                       const int32_t* tc_done, int tc_ctas) {
-  wait_tc_done(tc_done, tc_ctas);
+                                                       const int32_t* tc_done, int tc_ctas, const int32_t* cnt) {
+  if (cnt) {
+    // counted mode: no wait for whole grids -- this entry merges as soon
+    // as its partial producers (TC epilogue rows, suffix / multi CTAs, all
+    // resident already: this grid launched after the last of them started)
+    // counted g rows per partial in, so the merge overlaps the tail of the
+    // other kernels instead of following it
+    if (threadIdx.x == 0 && blockIdx.x < n_merge) {
+      const int need = g * (table[off_ptr + blockIdx.x + 1] - table[off_ptr + blockIdx.x]);
+      int v;
+      for (int it = 0;; ++it) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt + blockIdx.x) : "memory");
+        if (v >= need) break;
+        if (it > (1 << 24)) __trap();  // a count that never arrives is a bug: trap, do not hang
+        __nanosleep(128);
+      }
+    }
+    __syncthreads();
+  } else {
+    wait_tc_done(tc_done, tc_ctas);
+  }
   constexpr int kMax = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -200,7 +219,7 @@ int32_t launch_merge_csr(int dtype, int n_req, int h_q, int d, const int32_t* pt
 
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas, bool pdl) {
+                     int tc_ctas, bool pdl, const int32_t* cnt) {
   if (in.n_merge == 0) return CODEC_OK;
   const int h_local = in.h_local, g = hq_local / h_local;
   dim3 grid(in.n_merge, (g + 3) / 4);
@@ -224,7 +243,7 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
     cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, merge128_kernel, table, in.off_merge_req, in.off_merge_ptr,
                                        in.off_merge_slot, in.n_merge, g, h_local, (const float*)part_o,
-                                       (const float*)part_ml, (float*)out, tc_done, tc_ctas);
+                                       (const float*)part_ml, (float*)out, tc_done, tc_ctas, cnt);
     if (e != cudaSuccess) return cuda_status(e, "merge launch");
     return cuda_status(cudaGetLastError(), "merge launch");
   }

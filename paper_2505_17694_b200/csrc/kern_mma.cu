@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
                    const uint8_t* __restrict__ vpool, int64_t pool_tokens, int g, int hq_local,
                    float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                    int off_merge_ptr, int off_merge_slot, long long* __restrict__ ctalog,
-                   const int32_t* __restrict__ page_table, int page_shift) {
+                   const int32_t* __restrict__ page_table, int page_shift, const int32_t* __restrict__ entry_of,
+                   int32_t* __restrict__ cnt) {
   const long long t_start = ctalog ? global_ns() : 0;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge may be scheduled early (it waits)
   extern __shared__ uint8_t smem_raw[];
@@ -331,6 +332,15 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         }
       }
     }
+    // readiness count of the merge entry of (req, kv head): g rows landed
+    if (cnt && slot >= 0 && fz < 0) {
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kMmaWarps) : "memory");
+      if (tid == 0) {
+        const int e = __ldg(entry_of + (int64_t)req * (hq_local / g) + kh);
+        if (e >= 0) atomicAdd(cnt + e, g);
+      }
+    }
   }
   if (ctalog) {
     __syncthreads();
@@ -351,18 +361,22 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
 constexpr int kMultiWarps = 4;                          // consumer warps (<= 32 rows)
 constexpr int kMultiThreads = 32 * (kMultiWarps + 1);   // + producer warp
 constexpr int kMultiStages = 4;                         // fewer CTAs per SM than K3: a deeper ring
-constexpr int kMultiSmem = kMultiStages * kMmaStageBytes + 1024 + 2 * kMultiStages * 8;
+constexpr int kMultiCT = 32;                            // tokens per stage (two 16-token steps per warp)
+constexpr int kMultiBox = kMultiCT * 256;               // one box: kMultiCT whole token rows
+constexpr int kMultiStageBytes = 2 * kMultiBox;         // K box + V box
+constexpr int kMultiSmem = kMultiStages * kMultiStageBytes + 1024 + 2 * kMultiStages * 8;
 
 __global__ void __launch_bounds__(kMultiThreads, 3)
     mma_multi_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                      const int32_t* __restrict__ table, int off_groups, int off_rows,
                      const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                      float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
-                     const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ done) {
+                     const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ done,
+                     const int32_t* __restrict__ entry_of, int32_t* __restrict__ cnt) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMultiStages * kMmaStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMultiStages * kMultiStageBytes);
   uint64_t* empty = full + kMultiStages;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
   const int n_req = grp[kGrpNRows];
   const int n_cols = n_req * g;
   const int nbw = (n_cols + 7) >> 3;  // busy consumer warps
-  const int nch = (grp[kGrpMaxVis] + kMmaCT - 1) / kMmaCT;
+  const int nch = (grp[kGrpMaxVis] + kMultiCT - 1) / kMultiCT;
   const int kv_tok = grp[kGrpKvTok];
 
   if (tid == 0) {
@@ -392,13 +406,13 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
       for (int c = 0; c < nch; ++c) {
         const int s = c % kMultiStages;
         if (c >= kMultiStages) mbar_wait(&empty[s], ((c / kMultiStages) - 1) & 1);
-        uint8_t* st = smem + s * kMmaStageBytes;
-        int x = kv_tok + c * kMmaCT;  // paged pool: a 32-token box never crosses a page
+        uint8_t* st = smem + s * kMultiStageBytes;
+        int x = kv_tok + c * kMultiCT;  // paged pool: a 32-token box never crosses a page
         if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
         const int y = kh * (int)pool_tokens + x;
-        mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
+        mbar_arrive_expect_tx(&full[s], kMultiStageBytes);
         tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
-        tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
+        tc::tma_load_3d(st + kMultiBox, &tmv, 0, 0, y, &full[s]);
       }
     }
   } else if (warp < nbw) {
@@ -432,9 +446,9 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
     for (int c = 0; c < nch; ++c) {
       const int s = c % kMultiStages;
       mbar_wait(&full[s], (c / kMultiStages) & 1);
-      const uint32_t kb = smem_u32(smem + s * kMmaStageBytes), vb = kb + kMmaBox;
+      const uint32_t kb = smem_u32(smem + s * kMultiStageBytes), vb = kb + kMultiBox;
 #pragma unroll
-      for (int u = 0; u < kMmaCT / 16; ++u) {
+      for (int u = 0; u < kMultiCT / 16; ++u) {
         const int wrow = 16 * u;
         const int tk_qk = wrow + rr + ((mat & 1) << 3), ck_qk = mat >> 1;
         const int tk_pv = wrow + rr + ((mat >> 1) << 3), ck_pv = mat & 1;
@@ -446,7 +460,7 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
           hmma(sc, a, qf[ks][0], qf[ks][1]);
         }
         // sc[0]: (token gid, col a), [1]: (gid, col b), [2]: (gid+8, a), [3]: (gid+8, b)
-        const int t0 = c * kMmaCT + wrow + gid;
+        const int t0 = c * kMultiCT + wrow + gid;
         sc[0] = t0 < lim_a ? sc[0] * cscale : neg_inf<float>();
         sc[1] = t0 < lim_b ? sc[1] * cscale : neg_inf<float>();
         sc[2] = t0 + 8 < lim_a ? sc[2] * cscale : neg_inf<float>();
@@ -534,6 +548,14 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
           part_ml[2 * ei] = M * 0.69314718055994530942f;  // natural-log units
           part_ml[2 * ei + 1] = L;
         }
+        if (cnt) {  // readiness count of the merge entry of (req, kv head): one row landed
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {
+            const int e = __ldg(entry_of + (int64_t)req * (hq_local / g) + kh);
+            if (e >= 0) atomicAdd(cnt + e, 1);
+          }
+        }
       }
     }
   }
@@ -549,7 +571,8 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift) {
+                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift,
+                        const int32_t* entry_of, int32_t* cnt) {
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "mma suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
@@ -576,7 +599,7 @@ int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int 
   cfg.numAttrs = after_tc ? 1 : 0;
   e = cudaLaunchKernelEx(&cfg, mma_pac_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
                          (const uint8_t*)k, (const uint8_t*)v, pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, off_merge_ptr,
-                         off_merge_slot, ctalog, page_table, page_shift);
+                         off_merge_slot, ctalog, page_table, page_shift, entry_of, cnt);
   if (e != cudaSuccess) return cuda_status(e, "mma gemv launch");
   return cuda_status(cudaGetLastError(), "mma gemv launch");
 }
@@ -587,12 +610,12 @@ namespace codec {
 int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                          const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                          void* part_o, void* part_ml, cudaStream_t st, bool pdl, const int32_t* page_table,
-                         int page_shift, int32_t* done) {
+                         int page_shift, int32_t* done, const int32_t* entry_of, int32_t* cnt) {
   if (n_groups == 0) return CODEC_OK;
   if (g > 8) return fail(CODEC_ERR_UNSUPPORTED, "multi-request suffix kernel needs <= 8 query heads per kv head");
   CUtensorMap mk, mv;
-  CODEC_TRY(encode_pool_rows_map(&mk, k, (int64_t)h_local * pool_tokens, kMmaCT));
-  CODEC_TRY(encode_pool_rows_map(&mv, v, (int64_t)h_local * pool_tokens, kMmaCT));
+  CODEC_TRY(encode_pool_rows_map(&mk, k, (int64_t)h_local * pool_tokens, kMultiCT));
+  CODEC_TRY(encode_pool_rows_map(&mv, v, (int64_t)h_local * pool_tokens, kMultiCT));
   cudaError_t e = cudaFuncSetAttribute(mma_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMultiSmem);
   if (e != cudaSuccess) return cuda_status(e, "multi smem attribute");
   cudaLaunchConfig_t cfg = {};
@@ -607,7 +630,7 @@ int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int
   cfg.numAttrs = pdl ? 1 : 0;
   e = cudaLaunchKernelEx(&cfg, mma_multi_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q,
                          pool_tokens, g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, page_table,
-                         page_shift, done);
+                         page_shift, done, entry_of, cnt);
   if (e != cudaSuccess) return cuda_status(e, "multi launch");
   return cuda_status(cudaGetLastError(), "multi launch");
 }

@@ -66,6 +66,12 @@ constexpr int kTcD = 128;                    // head dim
 #define CODEC_TC_PREFETCH 4
 #endif
 constexpr int kTcPrefetch = CODEC_TC_PREFETCH;  // tiles ahead the producer warms L2
+// K half-tiles as ONE 3-D TMA box (64 d x 64 tokens x 2 halves = both SW128
+// atom columns) instead of one 2-D box per atom column: the SM's TMA unit
+// pays ~190 clk per op whatever its size
+#ifndef CODEC_TC_K3D
+#define CODEC_TC_K3D 1
+#endif
 constexpr int kQBytes = 128 * 128 * 2;       // this CTA's 128-row Q tile (32 KB)
 constexpr int kQAtom = kQBytes / 2;          // Q atom column: 128 rows x 64 d (16 KB)
 constexpr int kHalfBytes = 64 * 128 * 2;     // this CTA's half of a K or V tile (16 KB)
@@ -219,7 +225,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                   const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, int hq_local,
                   float* __restrict__ out, float* __restrict__ part_o, float* __restrict__ part_ml,
                   long long* __restrict__ trace, int dbg_flags, long long* __restrict__ ctalog,
-                  const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ tc_done) {
+                  const int32_t* __restrict__ page_table, int page_shift, int32_t* __restrict__ tc_done,
+                  const int32_t* __restrict__ entry_of, int32_t* __restrict__ cnt) {
   const long long t_start = ctalog ? global_ns() : 0;
 #ifdef CODEC_TC_DEBUG
   // timing-only ablations (tools/tc_ablate.py); compiled out of the product
@@ -344,8 +351,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const int xp = pfc.gv.kv_tok + pfc.j * kTcBN;
         const int ypk = prow(pfc.gv.kh, xp + 64 * rank), ypv = prow(pfc.gv.kh, xp);
         if (tc::elect_one()) {
+#if CODEC_TC_K3D
+          tc::tma_prefetch_3d(&tmk, 0, ypk, 0);
+#else
           tc::tma_prefetch_2d(&tmk, 0, ypk);
           tc::tma_prefetch_2d(&tmk, 64, ypk);
+#endif
           tc::tma_prefetch_2d(&tmv, 64 * rank, ypv);
         }
         __syncwarp();
@@ -366,8 +377,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           if (leader) mbar_arrive_expect_tx(&bars->k_full[ks], 2 * kHalfBytes);
           uint8_t* kd = smem + kOffK + ks * kHalfBytes;
           const int yk = prow(gv.kh, gv.kv_tok + j * kTcBN + 64 * rank);
+#if CODEC_TC_K3D
+          tc::tma_load_3d_pair(kd, &tmk, 0, yk, 0, &bars->k_full[ks]);  // both atom columns, one op
+#else
           tc::tma_load_2d_pair(kd, &tmk, 0, yk, &bars->k_full[ks]);
           tc::tma_load_2d_pair(kd + kKAtom, &tmk, 64, yk, &bars->k_full[ks]);
+#endif
         }
         __syncwarp();
         prefetch_to(t + 1 + kTcPrefetch);
@@ -889,6 +904,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
             named_sync(12, 128);
           }
+          // readiness count of the merge entry of (req, kv head): every
+          // thread's stores of the group fenced, then one arrival per row
+          if (cnt) {
+            __threadfence();
+            named_sync(12, 128);
+            if (valid && slot >= 0) {
+              const int e = __ldg(entry_of + (int64_t)req * (hq_local / g) + gv.kh);
+              if (e >= 0) atomicAdd(cnt + e, 1);
+            }
+          }
           // the staging reads / writes (generic proxy) before the Q warp's
           // next TMA load into this buffer (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -998,6 +1023,30 @@ int32_t encode_pool_rows_map(CUtensorMap* map, const void* pool, int64_t rows, u
   return CODEC_OK;
 }
 
+// The pool viewed as [2 halves][rows][64 d] (strides 128 B, 256 B): one box
+// {64 d, box_rows, 2} lands as the two K-major SW128 atom columns
+// [half][row][64] the MMA descriptors expect
+int32_t encode_pool_halves_map(CUtensorMap* map, const void* pool, int64_t rows, uint32_t box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !p)
+      return fail(CODEC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)kTcD * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CODEC_ERR_CUDA, "cuTensorMapEncodeTiled (halves) failed (%d)", (int)r);
+  return CODEC_OK;
+}
+
 constexpr int kTraceLen = 17 * 2 * 64 + 2 * 2048;
 static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one per process
 
@@ -1028,7 +1077,7 @@ static int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_loca
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
                   cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift,
-                  int32_t* tc_done) {
+                  int32_t* tc_done, const int32_t* entry_of, int32_t* cnt) {
   const bool trace = (flags & CODEC_FLAG_TRACE) != 0;
   if (trace && !g_trace) {
     if (cudaMalloc(&g_trace, kTraceLen * sizeof(long long)) != cudaSuccess) return fail(CODEC_ERR_CUDA, "trace alloc");
@@ -1036,7 +1085,11 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
   }
   if (in.n_tc_groups == 0 || in.n_tc_blocks == 0) return CODEC_OK;
   CUtensorMap mk, mv, mq;
+#if CODEC_TC_K3D
+  CODEC_TRY(encode_pool_halves_map(&mk, k, (int64_t)h_local * pool_tokens, 64));  // K half: 64 tokens, both atoms
+#else
   CODEC_TRY(encode_pool_map(&mk, k, (int64_t)h_local * pool_tokens, 64));      // K half: 64 tokens
+#endif
   CODEC_TRY(encode_pool_map(&mv, v, (int64_t)h_local * pool_tokens, kTcBN));   // V half: 64 d columns
   CODEC_TRY(encode_q_map(&mq, q, bs, h_local * g, g));
   cudaError_t e = cudaFuncSetAttribute(tc_pac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
@@ -1046,7 +1099,7 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
                                                    (const __nv_bfloat16*)q, pool_tokens, g, h_local * g,
                                                    (float*)out, (float*)part_o, (float*)part_ml,
                                                    trace ? g_trace : nullptr, flags, ctalog, page_table, page_shift,
-                                                   tc_done);
+                                                   tc_done, entry_of, cnt);
   return cuda_status(cudaGetLastError(), "tc launch");
 }
 

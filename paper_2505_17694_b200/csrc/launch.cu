@@ -15,7 +15,7 @@ namespace codec {
 int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
                   cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift,
-                  int32_t* tc_done);
+                  int32_t* tc_done, const int32_t* entry_of, int32_t* cnt);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
@@ -24,17 +24,18 @@ int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_grou
 int32_t launch_mma_gemv(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                         const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                         void* part_o, void* part_ml, int off_merge_ptr, int off_merge_slot, cudaStream_t st,
-                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift);
+                        long long* ctalog, bool after_tc, const int32_t* page_table, int page_shift,
+                        const int32_t* entry_of, int32_t* cnt);
 int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q,
                          const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                          void* part_o, void* part_ml, cudaStream_t st, bool pdl, const int32_t* page_table,
-                         int page_shift, int32_t* done);
+                         int page_shift, int32_t* done, const int32_t* entry_of, int32_t* cnt);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas, bool pdl);
+                     int tc_ctas, bool pdl, const int32_t* cnt);
 int32_t cuda_status(cudaError_t e, const char* what);
 }  // namespace codec
 
@@ -210,21 +211,35 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   // with the fused merge, which reads the TC partials from the suffix kernel
   const bool early = info->n_merge_fused == 0 && !kev;
   const bool pdl = mma_gemv && (do_tc || do_multi) && early;
-  if (done_target && cudaMemsetAsync(tc_done, 0, sizeof(int32_t), st) != cudaSuccess)
+  // Counted merge (opt-in): every partial producer (TC epilogue rows, mma.sync
+  // suffix / multi CTAs) bumps its merge entry's counter after its stores,
+  // and each merge CTA starts as soon as its entry is complete -- the merge
+  // overlaps the other kernels' tail. Only when all producers are those
+  // kernels (no CUDA-core GEMV / generic groups, no fused merge, the
+  // merge128 kernel) and nothing is skipped.
+  const int n_entries = info->n_merge + info->n_merge_fused;
+  const bool counted = (dims->flags & CODEC_FLAG_COUNTED_MERGE) && info->n_merge > 0 && dims->kv_dtype == CODEC_BF16 &&
+                       d == 128 && info->max_merge <= 16 &&
+                       !do_gen && (!do_gemv || mma_gemv) && info->n_merge_fused == 0 &&
+                       !(dims->flags & (CODEC_FLAG_SKIP_TC | CODEC_FLAG_SKIP_GEMV | CODEC_FLAG_SKIP_GENERIC));
+  int32_t* cnt = counted ? tc_done + 64 : nullptr;  // the tail's 256-byte block, then the counters
+  const int32_t* entry_of = table_dev + info->off_entry_of;
+  const size_t tail_bytes = 256 + (counted ? (size_t)n_entries * 4 : 0);
+  if ((done_target || counted) && cudaMemsetAsync(tc_done, 0, tail_bytes, st) != cudaSuccess)
     return fail(CODEC_ERR_CUDA, "tc counter reset");
   if (kev) CODEC_TRY(kev_record(timer, 0, st));
   if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
-                        dims->flags, ctalog, dims->page_table, page_shift, tc_done));
+                        dims->flags, ctalog, dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (kev) CODEC_TRY(kev_record(timer, 1, st));
   if (do_multi)
     CODEC_TRY(launch_mma_multi(table_dev, info->n_multi_groups, info->off_multi, info->off_rows, q, k, v,
                                dims->pool_tokens, g, h_local, out, part_o, part_ml, st, do_tc && early,
-                               dims->page_table, page_shift, tc_done));
+                               dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
                               dims->pool_tokens, g, h_local, out, part_o, part_ml, info->off_merge_ptr,
-                              info->off_merge_slot, st, ctalog, pdl, dims->page_table, page_shift));
+                              info->off_merge_slot, st, ctalog, pdl, dims->page_table, page_shift, entry_of, cnt));
   else if (do_gemv)
     CODEC_TRY(launch_gemv(dims->kv_dtype, d, info->gemv_rows, table_dev, info->n_gemv_groups, info->off_gemv,
                           info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, side,
@@ -240,8 +255,9 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st,
                            done_target ? tc_done : nullptr, done_target,
-                           mma_gemv && !fork && !kev && !(dims->flags & CODEC_FLAG_SKIP_GEMV) &&
-                               !(dims->flags & CODEC_FLAG_MERGE_NO_PDL)));
+                           (mma_gemv || do_multi || counted) && !fork && !kev &&
+                               !(dims->flags & CODEC_FLAG_SKIP_GEMV) && !(dims->flags & CODEC_FLAG_MERGE_NO_PDL),
+                           cnt));
   if (kev) {
     CODEC_TRY(kev_record(timer, 3, st));
     ++timer->n;

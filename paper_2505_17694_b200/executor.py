@@ -61,6 +61,35 @@ def _plan_arrays(plan):
     return t_node, t_nq, s_task, s_start, s_stop, s_block
 
 
+def table_for(forest: Forest, plan, dims):
+    """(codec_table_info, int32 blob) of a plan expanded for the device
+    (codec_table_build): host-only, no GPU needed."""
+    t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
+    P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+    L = _lib.lib()
+    h = C.c_void_p()
+    _lib.check(L.codec_table_build(forest._index, C.byref(dims), len(t_node), P(t_node, C.c_int64),
+                                   P(t_nq, C.c_int64), len(s_task), P(s_task, C.c_int32),
+                                   P(s_start, C.c_int64), P(s_stop, C.c_int64), P(s_block, C.c_int32),
+                                   C.byref(h)))
+    try:
+        info = _lib.TableInfo()
+        _lib.check(L.codec_table_info_get(h, C.byref(info)))
+        blob = np.zeros(max(info.blob_len, 4), dtype=np.int32)
+        _lib.check(L.codec_table_copy(h, P(blob, C.c_int32)))
+    finally:
+        L.codec_table_free(h)
+    return info, blob
+
+
+def make_dims(forest: Forest, h_q: int, dtype="bfloat16", head_begin=0, head_end=None, flags=0, sm_count=148,
+              tc_sm_budget=0, page_size=0, page_table_ptr=None, pool_tokens=None):
+    return _lib.Dims(forest.bs, int(h_q), forest.h_kv, forest.d, int(head_begin),
+                     forest.h_kv if head_end is None else int(head_end), dtype_code(dtype), int(flags),
+                     int(pool_tokens) if pool_tokens is not None else max(forest.total_tokens, 1), int(sm_count),
+                     int(tc_sm_budget), int(page_size), 0, page_table_ptr)
+
+
 class DecodeStep:
     """A plan expanded into a device task table for one forest, dtype and
     kv-head shard. Call with device queries [bs, h_q_local, d] and the
@@ -97,21 +126,7 @@ class DecodeStep:
         # GEMV/generic kernels run on an aux stream, concurrently with the
         # tensor-core kernel (event fork/join inside the library)
         self.aux = torch.cuda.Stream(self.device) if concurrent and torch.cuda.is_available() else None
-        t_node, t_nq, s_task, s_start, s_stop, s_block = _plan_arrays(plan)
-        P = lambda a, t: a.ctypes.data_as(C.POINTER(t))
-        L = _lib.lib()
-        h = C.c_void_p()
-        _lib.check(L.codec_table_build(forest._index, C.byref(self.dims), len(t_node), P(t_node, C.c_int64),
-                                       P(t_nq, C.c_int64), len(s_task), P(s_task, C.c_int32),
-                                       P(s_start, C.c_int64), P(s_stop, C.c_int64), P(s_block, C.c_int32),
-                                       C.byref(h)))
-        try:
-            self.info = _lib.TableInfo()
-            _lib.check(L.codec_table_info_get(h, C.byref(self.info)))
-            blob = np.zeros(max(self.info.blob_len, 4), dtype=np.int32)
-            _lib.check(L.codec_table_copy(h, P(blob, C.c_int32)))
-        finally:
-            L.codec_table_free(h)
+        self.info, blob = table_for(forest, plan, self.dims)
         self.blob_host = blob
         self.table = torch.from_numpy(blob).to(self.device)
         # partials, then a 256-byte tail whose first word is the TC kernel's

@@ -64,7 +64,9 @@ def test_random_forests_all_budgets(seed):
     table = P.load_default_profile()
     for budget in (148, 120, 96, 64, 40):
         plan = P.plan_device(f, 4, table, 8, 148, budget)
-        step = DecodeStep(f, plan, 32, "bfloat16", tc_sm_budget=budget, concurrent=True)
+        # the opt-in per-entry counted merge on alternate budgets
+        flags = 1048576 if budget in (120, 64) else 0
+        step = DecodeStep(f, plan, 32, "bfloat16", tc_sm_budget=budget, concurrent=True, flags=flags)
         a = step(q, kp, vp)
         b = step(q, kp, vp)
         torch.cuda.synchronize()

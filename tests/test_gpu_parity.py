@@ -215,7 +215,8 @@ def d128_forest(seed, with_masks):
 
 
 class TestBf16Kernels:
-    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC, FLAG_NO_MULTI, FLAG_NO_TC | FLAG_NO_MULTI])
+    @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC, FLAG_NO_MULTI, FLAG_NO_TC | FLAG_NO_MULTI,
+                                       1048576, FLAG_FORCE_TC | 1048576])
     def test_random_forests(self, cuda_ok, table, flags):
         for seed in range(24):
             spec = d128_forest(seed, with_masks=(seed % 2 == 1))

@@ -28,10 +28,14 @@ def suffix_alone(ns, n=20):
     return e0.elapsed_time(e1) / n
 
 
+if os.environ.get("SUFFIX_SLICE"):
+    from paper_2505_17694_b200 import scheduler
+    scheduler.SUFFIX_SLICE = int(os.environ["SUFFIX_SLICE"])
 for cfg in sys.argv[1:] or ["cfg2"]:
-    ns = bench.prepare(cfg, torch.device("cuda", 0))
+    ns = bench.prepare(cfg, torch.device("cuda", 0), flags=int(os.environ.get("FLAGS", "0")))
     best = min(ns.tune_ms.values())
     print(json.dumps({"lib": os.path.basename(os.environ.get("CODEC_B200_LIB", "default")), "config": cfg,
+                      "suffix_slice": os.environ.get("SUFFIX_SLICE"), "flags": os.environ.get("FLAGS"),
                       "best_ms": best, "budget": ns.budget, "suffix_alone_ms": round(suffix_alone(ns), 4),
                       "tune_ms": ns.tune_ms}), flush=True)
     del ns
