@@ -36,7 +36,10 @@ constexpr int kTcMinRows = 16;
 // with the multi-request kernel: slices of up to kMultiMaxRows query-head
 // rows take it (in groups of kMultiRows rows), larger ones the tensor cores
 constexpr int kMultiRows = 32;
-constexpr int kMultiMaxRows = 64;
+#ifndef CODEC_MULTI_MAX_ROWS
+#define CODEC_MULTI_MAX_ROWS 64
+#endif
+constexpr int kMultiMaxRows = CODEC_MULTI_MAX_ROWS;
 // query-head rows of one tensor-core group (M = 256: one 128-row tile per
 // CTA of a cta_group::2 pair)
 constexpr int kTcGroupRows = 256;

@@ -87,10 +87,10 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
   }
 }
 
-// d = 128, fp32 partials, <= 16 partials per request: the (m, l) pairs are
-// loaded first, then the output vectors four partials at a time with all
-// four loads in flight (float4 per lane), so the merge costs a few memory
-// latencies instead of one per partial.
+// d = 128, fp32 partials, any number of partials per entry: the (m, l)
+// pairs 32 at a time across the lanes, then the output vectors four
+// partials at a time with all four loads in flight (float4 per lane), so
+// the merge costs a few memory latencies instead of one per partial.
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
@@ -116,45 +116,56 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
   } else {
     wait_tc_done(tc_done, tc_ctas);
   }
-  constexpr int kMax = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const int k = blockIdx.y * 4 + warp;
   if (i >= n_merge || k >= g) return;
   const int hq_local = g * h_local;
   const int code = table[off_req + i], req = code / h_local, qh = (code % h_local) * g + k;
-  const int p0 = table[off_ptr + i], np = min(table[off_ptr + i + 1] - p0, kMax);
+  const int p0 = table[off_ptr + i], np = table[off_ptr + i + 1] - p0;
   const int32_t* slots = table + off_slot + p0;
-  // lane p (< np) fetches partial p's (m, l); the max is a warp reduction
-  float2 mlp = make_float2(neg_inf<float>(), 0.f);
-  int64_t ep = 0;
-  if (lane < np) {
-    ep = (int64_t)slots[lane] * hq_local + qh;
-    mlp = __ldg(reinterpret_cast<const float2*>(part_ml) + ep);
-  }
-  float M = mlp.y > 0 ? mlp.x : neg_inf<float>();
-  M = warp_max(M);
-  const float wl = mlp.y > 0 ? mlp.y * __expf(mlp.x - M) : 0.f;
-  const float L = warp_sum(wl);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int b = 0; b < np; b += 4) {
-    float4 o[4];
-    float w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int p = b + k;
-      w[k] = __shfl_sync(0xffffffffu, wl, p & 31);
-      const int64_t e = __shfl_sync(0xffffffffu, ep, p & 31);
-      o[k] = (p < np && w[k] > 0) ? __ldg(reinterpret_cast<const float4*>(part_o + e * 128) + lane)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+  // pass 1: the max over all partials, 32 (m, l) pairs per round in flight
+  float M = neg_inf<float>();
+  for (int b = 0; b < np; b += 32) {
+    if (b + lane < np) {
+      const float2 ml = __ldg(reinterpret_cast<const float2*>(part_ml) + (int64_t)slots[b + lane] * hq_local + qh);
+      if (ml.y > 0) M = fmaxf(M, ml.x);
     }
+  }
+  M = warp_max(M);
+  // pass 2: weights (lane p of round b holds partial b + p), then the
+  // output vectors four partials at a time with all four loads in flight
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int b = 0; b < np; b += 32) {
+    float wl = 0.f;
+    int64_t ep = 0;
+    if (b + lane < np) {
+      ep = (int64_t)slots[b + lane] * hq_local + qh;
+      const float2 ml = __ldg(reinterpret_cast<const float2*>(part_ml) + ep);
+      wl = ml.y > 0 ? ml.y * __expf(ml.x - M) : 0.f;
+    }
+    L += warp_sum(wl);
+    const int nb = min(32, np - b);
+    for (int c = 0; c < nb; c += 4) {
+      float4 o[4];
+      float w[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float ww = (b + k < np) ? w[k] : 0.f;
-      acc.x += ww * o[k].x;
-      acc.y += ww * o[k].y;
-      acc.z += ww * o[k].z;
-      acc.w += ww * o[k].w;
+      for (int u = 0; u < 4; ++u) {
+        const int p = c + u;
+        w[u] = __shfl_sync(0xffffffffu, wl, p & 31);
+        const int64_t e = __shfl_sync(0xffffffffu, ep, p & 31);
+        o[u] = (p < nb && w[u] > 0) ? __ldg(reinterpret_cast<const float4*>(part_o + e * 128) + lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float ww = (c + u < nb) ? w[u] : 0.f;
+        acc.x += ww * o[u].x;
+        acc.y += ww * o[u].y;
+        acc.z += ww * o[u].z;
+        acc.w += ww * o[u].w;
+      }
     }
   }
   const float inv = 1.f / L;
@@ -228,7 +239,7 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
                                              in.n_merge, g, h_local, d, (const A*)part_o, (const A*)part_ml,    \
                                              (A*)out, tc_done, tc_ctas)
   if (d > 512) return fail(CODEC_ERR_UNSUPPORTED, "head dim %d > 512", d);
-  if (dtype != CODEC_F64 && d == 128 && in.max_merge <= 16) {
+  if (dtype != CODEC_F64 && d == 128) {
     // after the suffix kernel on the same stream: programmatic dependent
     // launch, so the merge CTAs are resident when it retires (they wait in
     // griddepcontrol.wait, then for the TC counter)

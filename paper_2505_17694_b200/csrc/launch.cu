@@ -219,7 +219,7 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
   // merge128 kernel) and nothing is skipped.
   const int n_entries = info->n_merge + info->n_merge_fused;
   const bool counted = (dims->flags & CODEC_FLAG_COUNTED_MERGE) && info->n_merge > 0 && dims->kv_dtype == CODEC_BF16 &&
-                       d == 128 && info->max_merge <= 16 &&
+                       d == 128 &&
                        !do_gen && (!do_gemv || mma_gemv) && info->n_merge_fused == 0 &&
                        !(dims->flags & (CODEC_FLAG_SKIP_TC | CODEC_FLAG_SKIP_GEMV | CODEC_FLAG_SKIP_GENERIC));
   int32_t* cnt = counted ? tc_done + 64 : nullptr;  // the tail's 256-byte block, then the counters

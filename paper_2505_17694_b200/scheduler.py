@@ -140,6 +140,8 @@ TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core k
 MULTI_MAX_ROWS = 64  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
+SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into
+SUFFIX_WAVES = 2        # suffix-grid CTA waves (of 6 CTAs per SM) plan_device aims for
 
 
 def concat_plans(plans) -> DivisionPlan:
@@ -198,12 +200,19 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     plans = []
     if tc:
         plans.append(plan_uniform_bk(tc, table, pairs, 1))
-    # mma.sync-kernel tasks: one CTA streams a slice at a few tens of GB/s,
-    # so long ones (a lightly shared 128K-token root in cfg4) are cut into
-    # slices of <= SUFFIX_SLICE tokens that run on separate CTAs
+    # mma.sync-kernel tasks: one CTA streams a slice at only a few tens of
+    # GB/s (bytes in flight per CTA are bounded by its SMEM ring), so the
+    # machine needs many CTAs: long slices are cut so the suffix grids hold
+    # >= SUFFIX_WAVES waves of CTAs (6 per SM), never below
+    # SUFFIX_SLICE_MIN tokens (each slice adds a partial to merge) nor above
+    # SUFFIX_SLICE (a lightly shared 128K-token root in cfg4)
+    work = sum(t.n for t in gv) * h_local
+    target = max(1, sm_count * 6 * SUFFIX_WAVES)
+    slice_len = min(SUFFIX_SLICE, max(SUFFIX_SLICE_MIN, -(-work // target)))
+    slice_len = -(-slice_len // 64) * 64
     by_bk = {}
     for t in gv:
-        by_bk.setdefault(1 if page_size else max(1, -(-t.n // SUFFIX_SLICE)), []).append(t)
+        by_bk.setdefault(1 if page_size else max(1, -(-t.n // slice_len)), []).append(t)
     for bk in sorted(by_bk):
         plans.append(plan_uniform_bk(by_bk[bk], table, len(by_bk[bk]) * bk, bk))
     return concat_plans(plans)

@@ -28,6 +28,9 @@ def suffix_alone(ns, n=20):
     return e0.elapsed_time(e1) / n
 
 
+if os.environ.get("MULTI_MAX_ROWS"):  # must match the library's -DCODEC_MULTI_MAX_ROWS
+    from paper_2505_17694_b200 import scheduler
+    scheduler.MULTI_MAX_ROWS = int(os.environ["MULTI_MAX_ROWS"])
 if os.environ.get("SUFFIX_SLICE"):
     from paper_2505_17694_b200 import scheduler
     scheduler.SUFFIX_SLICE = int(os.environ["SUFFIX_SLICE"])

@@ -36,6 +36,8 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1
 def kernel_key(name):
     if "tc_pac" in name:
         return "tc"
+    if "mma_multi" in name:
+        return "multi"
     if "mma_pac" in name or "gemv_pac" in name:
         return "gemv"
     if "merge" in name:
@@ -68,21 +70,31 @@ def summarise(rep):
 
 
 def main():
-    cfg, reps = sys.argv[1], sys.argv[2:]
+    """ncu_summary.py CONFIG TC_SM_BUDGET REP..."""
+    cfg, budget, reps = sys.argv[1], int(sys.argv[2]), sys.argv[3:]
     path = ROOT / "profiles" / "ncu_summary.json"
     allj = json.loads(path.read_text()) if path.exists() else {}
-    cur = allj.get(cfg, {})
+    cur = {}
     for rep in reps:
         cur.update(summarise(rep))
+    kernels = [k for k in cur if isinstance(cur[k], dict)]
+    cur["tc_sm_budget"] = budget
+    cur["step_dram_bytes"] = sum(cur[k].get("dram_bytes", 0) for k in kernels)
+    cur["capture"] = ("ncu --set full --clock-control none, one decode step of bench.prepare(cfg) at the "
+                      "benchmarked tensor-core SM budget; kernels serialised by the profiler")
     allj[cfg] = cur
     path.write_text(json.dumps(allj, indent=1) + "\n")
     lines = [f"# ncu --set full summary ({cfg})", "",
              "| kernel | duration us | DRAM bytes | DRAM % | tensor % (active) | XU % | FMA % | regs | grid |",
              "|---|---|---|---|---|---|---|---|---|"]
     for k, r in cur.items():
+        if not isinstance(r, dict):
+            continue
         lines.append(f"| {k} ({r.get('kernel')}) | {r.get('duration', 0):.1f} | {r.get('dram_bytes', 0):.4g} | "
                      f"{r.get('dram_pct', 0):.1f} | {r.get('tensor_pct_active', 0):.1f} | {r.get('xu_pct', 0):.1f} | "
                      f"{r.get('fma_pct', 0):.1f} | {r.get('regs', 0):.0f} | {r.get('grid', 0):.0f} |")
+    lines += ["", f"tensor-core SM budget {budget}; step DRAM bytes {cur['step_dram_bytes']:.4g} "
+              f"(kernels serialised by ncu, cold caches)"]
     (ROOT / "profiles" / f"ncu_summary_{cfg}.md").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 

@@ -14,13 +14,44 @@
 
 using namespace codec;
 
-__global__ void blocker(volatile int* flag, int n_block) {
+// pattern 0: SMs with smid < n_block stay blocked; pattern 1: the free SMs
+// are spread evenly over the smid range. hammer: blocked SMs read an
+// L2-resident buffer in a loop instead of sleeping (L2 / fabric traffic).
+__global__ void blocker(volatile int* flag, int n_block, int n_sm, int pattern, int hammer, const uint4* l2buf,
+                        unsigned long long* sink) {
   extern __shared__ uint8_t smem[];
-  if (blockIdx.x >= n_block) return;
-  if (threadIdx.x == 0) {
-    smem[0] = 1;
-    while (*flag == 0) __nanosleep(1000);
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const int n_free = n_sm - n_block;
+  bool blocked;
+  if (pattern == 0) {
+    blocked = (int)smid < n_block;
+  } else {
+    blocked = true;  // free iff smid == floor(i * n_sm / n_free) for some i
+    const int i = (int)(((long long)smid * n_free + n_sm - 1) / n_sm);
+    if (i < n_free && (int)((long long)i * n_sm / n_free) == (int)smid) blocked = false;
   }
+  if (!blocked) return;
+  if (!hammer) {
+    if (threadIdx.x == 0) {
+      smem[0] = 1;
+      while (*flag == 0) __nanosleep(1000);
+    }
+    return;
+  }
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  const int n = (32 << 20) / 16;
+  for (int it = 0;; ++it) {
+    for (int i = threadIdx.x + blockIdx.x * 64; i < n; i += blockDim.x * 4096) {
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const uint4 v = __ldcg(l2buf + ((i + k * 1024) % n));
+        acc.x ^= v.x;
+      }
+    }
+    if ((it & 15) == 0 && *flag) break;
+  }
+  if (acc.x == 0x12345) *sink = acc.x;
 }
 
 __global__ void stream(const uint8_t* __restrict__ src, size_t per_cta, int stages, int box, int copies,
@@ -69,6 +100,8 @@ int main(int argc, char** argv) {
   const int stages = argc > 3 ? atoi(argv[3]) : 2;
   const int box = argc > 4 ? atoi(argv[4]) : 16384;
   const int copies = argc > 5 ? atoi(argv[5]) : 1;
+  const int pattern = argc > 6 ? atoi(argv[6]) : 0;
+  const int hammer = argc > 7 ? atoi(argv[7]) : 0;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t total = (size_t)4 << 30;
@@ -95,7 +128,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e1);
   for (int rep = 0; rep < 3; ++rep) {
     *flag = 0;
-    blocker<<<sms, 32, bsmem, sa>>>(dflag, sms - N);
+    blocker<<<sms, hammer ? 512 : 32, bsmem, sa>>>(dflag, sms - N, sms, pattern, hammer, (const uint4*)buf, sink);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) { printf("blocker: %s\n", cudaGetErrorString(err)); return 1; }
     // give the blockers time to become resident
@@ -112,8 +145,8 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double bytes = (double)per_cta * ctas;
-    if (rep) printf("N=%d ctas/SM=%d stages=%d box=%d copies=%d: %.3f ms  %.0f GB/s  %.1f GB/s per SM\n", N, per_sm,
-                    stages, box, copies, ms, bytes / ms / 1e6, bytes / ms / 1e6 / N);
+    if (rep) printf("N=%d ctas/SM=%d stages=%d box=%d copies=%d pattern=%d hammer=%d: %.3f ms  %.0f GB/s  %.1f GB/s per SM\n",
+                    N, per_sm, stages, box, copies, pattern, hammer, ms, bytes / ms / 1e6, bytes / ms / 1e6 / N);
   }
   return 0;
 }
