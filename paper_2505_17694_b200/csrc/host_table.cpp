@@ -291,8 +291,16 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     // lane = rank of the group among the TC groups of its KV slice
     std::map<std::pair<int32_t, int32_t>, std::vector<int32_t>> by_slice;  // (kv_tok, len) -> groups
     for (int32_t gi : tcg) by_slice[{groups[gi].kv_tok, groups[gi].len}].push_back(gi);
+    // Slices with more lanes first: every lane then walks the slices it
+    // shares with lane 0 as a PREFIX of lane 0's sequence, at the same
+    // positions -- pair k of every lane reads the same K/V tiles at the same
+    // time (one HBM read, L2 hits for the others) even when slices have
+    // different lane counts (cfg4: 1..7 lanes; pool order re-read ~4 GB).
+    std::vector<std::pair<std::pair<int32_t, int32_t>, std::vector<int32_t>>> slices(by_slice.begin(), by_slice.end());
+    std::stable_sort(slices.begin(), slices.end(),
+                     [](const auto& a, const auto& b) { return a.second.size() > b.second.size(); });
     std::vector<std::vector<int32_t>> lanes;
-    for (auto& kv : by_slice) {
+    for (auto& kv : slices) {
       auto v = kv.second;
       std::stable_sort(v.begin(), v.end(), [&](int32_t a, int32_t b) { return groups[a].row_begin < groups[b].row_begin; });
       for (size_t c = 0; c < v.size(); ++c) {

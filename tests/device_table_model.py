@@ -6,12 +6,14 @@ library's task tables against it, record for record.
 The rule ("Device balancer"): every tensor-core (TC) group is
 (plan subtask, chunk of <= 256/g requests); a unit = (TC group, kv head) of
 ceil(max_visible / 128) KV tiles. Units are laid out in lanes (lane c = the
-c-th row chunk of every KV slice, slices in (pool token, length) order, then
-heads). With P CTA pairs, every pair gets T = ceil(W / P) tiles: lane c runs
+c-th row chunk of every KV slice, then heads). With P CTA pairs, every pair gets T = ceil(W / P) tiles: lane c runs
 on floor(W_c / T) pairs of its own -- pair k of a lane takes tiles
 [k T, (k + 1) T) of the lane's unit sequence -- and the lane tails (what
 does not fill a whole pair) are pooled in lane order and cut into T-tile
-pieces for the remaining pairs. Pieces never cross units."""
+pieces for the remaining pairs. Pieces never cross units. Slices are
+taken in order of decreasing lane count (then pool order), so every lane's
+sequence is a prefix of lane 0's: pair k of every lane reads the same K/V
+tiles at the same time."""
 from __future__ import annotations
 
 MULTI_ROWS, MULTI_MAX_ROWS, TC_MIN_ROWS, TC_ROWS = 32, 64, 16, 256
@@ -72,7 +74,9 @@ def tc_pieces(forest, plan, g, h_local, sms=148, budget=0, multi=True, force_tc=
     for x in tcg:
         by_slice.setdefault((x[1], x[2]), []).append(x)
     lanes = []
-    for key in sorted(by_slice):
+    # slices with more lanes first (stable over pool order): the lanes'
+    # sequences are prefixes of lane 0's, aligned position for position
+    for key in sorted(sorted(by_slice), key=lambda k: -len(by_slice[k])):
         for c, x in enumerate(sorted(by_slice[key], key=lambda y: y[4])):
             if len(lanes) <= c:
                 lanes.append([])
