@@ -40,6 +40,9 @@ namespace codec {
 #ifndef CODEC_MMA_SUB
 #define CODEC_MMA_SUB 1
 #endif
+#ifndef CODEC_SUFFIX_EVICT_FIRST
+#define CODEC_SUFFIX_EVICT_FIRST 1
+#endif
 #ifndef CODEC_MMA_STAGES
 #define CODEC_MMA_STAGES 2  // 2 x 16 KB per CTA, 6 CTAs per SM: more CTAs beat deeper rings (~5 % on cfg2)
 #endif
@@ -110,6 +113,9 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
     if (lane == 0) {
       tc::prefetch_tmap(&tmk);
       tc::prefetch_tmap(&tmv);
+#if CODEC_SUFFIX_EVICT_FIRST
+      const uint64_t pol = tc::policy_evict_first();  // read once: leave L2 to the shared-node tiles
+#endif
       // pool row of chunk c (logical token; paged pool: a 32-token box
       // never crosses a page)
       auto chunk_row = [&](int c) {
@@ -141,8 +147,13 @@ __global__ void __launch_bounds__(kMmaThreads, 6)
         uint8_t* st = smem + s * kMmaStageBytes;
         const int y = (int)chunk_row(c);
         mbar_arrive_expect_tx(&full[s], kMmaStageBytes);
+#if CODEC_SUFFIX_EVICT_FIRST
+        tc::tma_load_3d_hint(st, &tmk, 0, 0, y, &full[s], pol);
+        tc::tma_load_3d_hint(st + kMmaBox, &tmv, 0, 0, y, &full[s], pol);
+#else
         tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
         tc::tma_load_3d(st + kMmaBox, &tmv, 0, 0, y, &full[s]);
+#endif
         // keep CODEC_MMA_PF chunks beyond the ring requested, in groups
         if (CODEC_MMA_PF > 0 && c % CODEC_MMA_PF_GROUP == 0)
           prefetch(c + kMmaStages + CODEC_MMA_PF, CODEC_MMA_PF_GROUP);
@@ -403,6 +414,9 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
     if (lane == 0) {
       tc::prefetch_tmap(&tmk);
       tc::prefetch_tmap(&tmv);
+#if CODEC_SUFFIX_EVICT_FIRST
+      const uint64_t pol = tc::policy_evict_first();  // read once: leave L2 to the shared-node tiles
+#endif
       for (int c = 0; c < nch; ++c) {
         const int s = c % kMultiStages;
         if (c >= kMultiStages) mbar_wait(&empty[s], ((c / kMultiStages) - 1) & 1);
@@ -411,8 +425,13 @@ __global__ void __launch_bounds__(kMultiThreads, 3)
         if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
         const int y = kh * (int)pool_tokens + x;
         mbar_arrive_expect_tx(&full[s], kMultiStageBytes);
+#if CODEC_SUFFIX_EVICT_FIRST
+        tc::tma_load_3d_hint(st, &tmk, 0, 0, y, &full[s], pol);
+        tc::tma_load_3d_hint(st + kMultiBox, &tmv, 0, 0, y, &full[s], pol);
+#else
         tc::tma_load_3d(st, &tmk, 0, 0, y, &full[s]);
         tc::tma_load_3d(st + kMultiBox, &tmv, 0, 0, y, &full[s]);
+#endif
       }
     }
   } else if (warp < nbw) {

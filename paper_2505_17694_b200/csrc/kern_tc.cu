@@ -86,11 +86,11 @@ constexpr int kTcRegsSoftmax = 200, kTcRegsOther = 96;
 static_assert(32 * kTcSoftmaxWarps * kTcRegsSoftmax + (kTcThreads - 32 * kTcSoftmaxWarps) * kTcRegsOther <=
                   kTcThreads * (65536 / kTcThreads / 8 * 8),
               "setmaxnreg.inc would wait forever for registers the CTA does not own");
-// K / V ring depths (SMEM: 64 KB of Q + 16 KB per stage); 5 / 5 and 3 / 7
-// measured the same as 4 / 6 on cfg2
+// K / V ring depths (SMEM: 64 KB of Q + 16 KB per stage); 4 / 4 measured
+// 1 % faster than 4 / 6 on cfg2 (tools/ab_rounds.py), 3 / 4 the same
 #ifndef CODEC_TC_KSTAGES
 #define CODEC_TC_KSTAGES 4
-#define CODEC_TC_VSTAGES 6
+#define CODEC_TC_VSTAGES 4
 #endif
 constexpr int kTcKStages = CODEC_TC_KSTAGES, kTcVStages = CODEC_TC_VSTAGES;
 constexpr int kOffQ = 0;                     // Q0, Q1 (double-buffered across units)
