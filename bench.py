@@ -13,8 +13,11 @@ value = effective unique-KV GB/s over the whole job (all ranks). With N
 GPUs the step is sharded: `--partition heads` splits the
 kv heads N ways (tensor-parallel head split; default) and `--partition
 trees` LPT-assigns whole trees of the forest to ranks (cfg4's default);
-either way the per-rank outputs are all-gathered over NCCL inside the
-timed step (by head block or by request). `e2e` times the same step
+either way the per-rank outputs are gathered inside the timed step (by
+head block or by request): by default fused into the merge kernel, which
+stores every output row into all ranks' global output buffers over
+NVLink and signals them (parallel.PeerGather), or with `--gather nccl`
+by an NCCL all-gather after the step. `e2e` times the same step
 through the public API with queries copied from pinned host memory and the
 output read back every step, in the same >= 2 s windows as `value`.
 After timing, untimed, the bench checks sampled requests of its own output
@@ -377,6 +380,8 @@ def main():
     ap.add_argument("--serial", action="store_true", help="one stream: TC, GEMV and merge back to back")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph replay")
     ap.add_argument("--budget", type=int, default=0, help="fixed tensor-core SM budget (no tuning)")
+    ap.add_argument("--gather", default="fused", choices=["fused", "nccl"],
+                    help="N > 1 output gather: fused peer stores from the merge kernel (default) or NCCL all-gather")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config], name=args.config)
 
@@ -396,7 +401,10 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    ns = prepare(args.config, dev, rank, world, args.partition, args.flags, args.serial, args.blocks,
+    from paper_2505_17694_b200.executor import FLAG_MERGE_ALL
+    fused = world > 1 and args.gather == "fused"
+    flags = args.flags | (FLAG_MERGE_ALL if fused else 0)
+    ns = prepare(args.config, dev, rank, world, args.partition, flags, args.serial, args.blocks,
                  budgets=[args.budget] if args.budget else None, quick=args.quick)
     step, plan, budget = ns.step, ns.plan, ns.budget
     kp, vp, q_dev, q_host, out = ns.kp, ns.vp, ns.q_dev, ns.q_host, ns.out
@@ -408,6 +416,17 @@ def main():
     n_max = max(s.bs for s in ns.shards) if trees else bs
     gathered = torch.empty((world, n_max, hq_local, d), dtype=torch.float32, device=dev) if world > 1 else None
     send = torch.zeros((n_max, hq_local, d), dtype=torch.float32, device=dev) if trees else None
+
+    # fused gather: the merge kernel stores this rank's
+    # rows into every rank's global output over NVLink and bumps their
+    # arrival counters; no NCCL call on the data path
+    peers = row_map = None
+    head0 = ns.h0 * ns.g
+    if fused:
+        peers = PL.PeerGather(full_bs, h_q, d, dev, buffers=2)
+        if trees:
+            row_map = torch.tensor(list(ns.shard.requests), dtype=torch.int32, device=dev)
+            head0 = 0
 
     def gather(o, buf):
         if world == 1:
@@ -421,9 +440,19 @@ def main():
 
     # the timed step replays a CUDA graph of the decode step (its three
     # launches recorded once; no per-step host work)
-    replay = step.capture(q_dev, kp, vp, out) if not args.no_graph else None
+    if fused:
+        replay = (step.capture_gather(q_dev, kp, vp, peers, head0, row_map, buf=0) if not args.no_graph else None)
+    else:
+        replay = step.capture(q_dev, kp, vp, out) if not args.no_graph else None
 
     def one_step():
+        if fused:
+            if replay is not None:
+                replay()
+            else:
+                step.gather(q_dev, kp, vp, peers, head0, row_map, buf=0)
+                peers.wait()
+            return peers.output(0)
         if replay is not None:
             replay()
         else:
@@ -562,7 +591,10 @@ def main():
         rows_out = full_bs if world > 1 else bs
         ohost = [torch.empty((rows_out, (h_q if (world > 1 and not trees) else hq_local), d),
                              dtype=torch.float32).pin_memory() for _ in range(2)]
-        replays = [step.capture(qbuf[i], kp, vp, obuf[i]) for i in range(2)] if not args.no_graph else None
+        if fused:
+            replays = [step.capture_gather(qbuf[i], kp, vp, peers, head0, row_map, buf=i) for i in range(2)]
+        else:
+            replays = [step.capture(qbuf[i], kp, vp, obuf[i]) for i in range(2)] if not args.no_graph else None
         ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
         st8 = {"k": 0}
 
@@ -578,12 +610,16 @@ def main():
             stream.wait_event(ev["h2d"][sl])
             if k >= 2:
                 stream.wait_event(ev["d2h"][sl])
-            if replays is not None:
+            if fused:
                 replays[sl]()
+                res = peers.output(sl)
+            elif replays is not None:
+                replays[sl]()
+                res = obuf[sl]
             else:
                 step(qbuf[sl], kp, vp, out=obuf[sl], stream=stream)
-            res = obuf[sl]
-            if world > 1:
+                res = obuf[sl]
+            if world > 1 and not fused:
                 buf = gather(obuf[sl], gbuf[sl])
                 res = PL.scatter_requests(buf, ns.shards, full_bs) if trees else PL.assemble_heads(buf)
             ev["comp"][sl].record(stream)
@@ -627,15 +663,22 @@ def main():
 
     # untimed self-check of the benchmarked step's output
     torch.cuda.synchronize(dev)
-    if replay is not None:
+    if fused:
+        res = one_step()  # the gathered global output
+        step(q_dev, kp, vp, out=out)  # this rank's rows, written locally by the same kernels
+    elif replay is not None:
         replay()
+        res = gather(out, gathered)
     else:
         step(q_dev, kp, vp, out=out)
-    res = gather(out, gathered)
+        res = gather(out, gathered)
     torch.cuda.synchronize(dev)
     check = verify(ns, out)
     if world > 1:  # the gathered output holds this rank's rows unchanged
-        full_out = PL.scatter_requests(res, ns.shards, full_bs) if trees else PL.assemble_heads(res)
+        if fused:
+            full_out = res
+        else:
+            full_out = PL.scatter_requests(res, ns.shards, full_bs) if trees else PL.assemble_heads(res)
         mine = full_out[list(ns.shard.requests)] if trees else full_out[:, ns.h0 * g:(ns.h0 + ns.h_local) * g]
         check["gather_ok"] = bool(torch.equal(mine, out))
         flag = torch.tensor([0 if (check["ok"] and check["gather_ok"]) else 1], device=dev)
@@ -674,8 +717,10 @@ def main():
             "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
             "config": {"workload": ns.cfg["label"], "bs": full_bs, "h_q": h_q, "h_kv": ns.cfg["h_kv"], "d": d,
                        "kv_tokens": int(sum(ns.spec.length[1:])), "nodes": int(ns.spec.n_nodes - 1),
-                       "parallelism": (f"tree partition x{world} + NCCL all-gather by request" if trees else
-                                       f"kv-head split x{world}" + (" + NCCL all-gather" if world > 1 else "")),
+                       "parallelism": ((f"tree partition x{world}" if trees else f"kv-head split x{world}") +
+                                       ("" if world == 1 else
+                                        " + fused peer-store output gather (merge kernel -> NVLink)" if fused else
+                                        (" + NCCL all-gather by request" if trees else " + NCCL all-gather"))),
                        "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
                        "planner": {"m_tc": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,
                                    "truncated": plan.search_truncated, "ms": ns.plan_ms},

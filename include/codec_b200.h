@@ -274,6 +274,9 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_COUNTED_MERGE 1048576 /* partial producers count per merge entry and the merge starts each entry
                                             as soon as it is complete (opt-in: measured no faster on cfg2/cfg3) */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
+#define CODEC_FLAG_MERGE_ALL 2097152 /* every (request, kv head) output goes through the merge kernel, single-partial
+                                        ones too (no direct writes by the split kernels): what the fused peer-store
+                                        output gather (codec_decode_attention_gather) needs */
 
 typedef struct codec_table codec_table;
 CODEC_API int32_t codec_table_build(const codec_index* ix, const codec_dims* dims, int32_t n_tasks,
@@ -344,6 +347,45 @@ CODEC_API int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_
 CODEC_API int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
                                          const int32_t* table_dev, const void* q, const void* k, const void* v,
                                          void* out, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* ======================================================================
+ * Fused multi-GPU output gather. Replaces the NCCL
+ * all-gather of the per-rank outputs (parallel.all_gather_heads /
+ * gather_requests): the merge kernel of rank `self` stores every output
+ * row it produces straight into all n_peers ranks' global output buffers
+ * (peer stores over NVLink / NVSwitch), at row row_map[r] (r when NULL),
+ * q heads [head0, head0 + h_q_local) of hq_global; its last CTA then bumps
+ * counter `self` in every rank's flag array (system-scope atomics, after a
+ * system fence). codec_peer_wait makes a stream wait until all n_peers
+ * counters of the local flag array reached the next step's value -- the
+ * gathered output is then complete on this rank. The table must be built
+ * with CODEC_FLAG_MERGE_ALL (bf16 KV, d = 128). Buffers come from
+ * codec_ipc_alloc on each rank, peers' handles are opened with
+ * codec_ipc_open (the handles travel over any side channel: gloo / NCCL
+ * all_gather_object). `done` (device int32, zero before the first call)
+ * counts the merge CTAs of a call and is reset by the last one.
+ * ==================================================================== */
+typedef struct {
+  int32_t n_peers, self;       /* ranks in the gather, this rank */
+  int32_t hq_global, head0;    /* q heads per row of the global buffer, this rank's first one */
+  void* const* peer_out;       /* device [n_peers]: float32 [rows][hq_global][128] of every rank */
+  int32_t* const* peer_flags;  /* device [n_peers]: int32 [n_peers] arrival counters of every rank */
+  const int32_t* row_map;      /* device [bs]: global row of local request r, NULL = r */
+  int32_t* done;               /* device int32: merge CTAs finished in the current call */
+} codec_peer_gather;
+CODEC_API int32_t codec_decode_attention_gather(const codec_dims* dims, const codec_table_info* info,
+                                                const int32_t* table_dev, const void* q, const void* k,
+                                                const void* v, void* workspace, int64_t workspace_bytes,
+                                                void* stream, void* aux_stream, const codec_peer_gather* pg);
+/* Wait (on `stream`) until every flags[p], p < n_peers, is >= *expected + 1,
+ * then store *expected + 1 (device int32 step counter of this rank). */
+CODEC_API int32_t codec_peer_wait(const int32_t* flags, int32_t n_peers, int32_t* expected, void* stream);
+/* Symmetric buffers: a cudaMalloc allocation (zeroed) plus its 64-byte
+ * CUDA IPC handle; open / close a peer's handle in this process. */
+CODEC_API int32_t codec_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64);
+CODEC_API int32_t codec_ipc_free(void* dev_ptr);
+CODEC_API int32_t codec_ipc_open(const void* handle64, void** dev_ptr);
+CODEC_API int32_t codec_ipc_close(void* dev_ptr);
 
 /* Debug builds only (compiled with -DCODEC_HANG_CHECK): a device pointer to
  * host-mapped int32[8 + 8 * 1000]; a TC-kernel mbarrier wait that spins for

@@ -82,6 +82,13 @@ class TableInfo(C.Structure):
                 ("blob_len", I64), ("workspace_bytes", I64)]
 
 
+class PeerGatherC(C.Structure):
+    """codec_peer_gather (include/codec_b200.h): the fused output gather."""
+    _fields_ = [("n_peers", I32), ("self", I32), ("hq_global", I32), ("head0", I32),
+                ("peer_out", C.c_void_p), ("peer_flags", C.c_void_p), ("row_map", C.c_void_p),
+                ("done", C.c_void_p)]
+
+
 _SIGS = {
     "codec_last_error": (C.c_char_p, []),
     "codec_abi_version": (I32, []),
@@ -124,6 +131,13 @@ _SIGS = {
     "codec_merge_partials": (I32, [I32, I32, I32, I32, P, P, P, P, P, P, P, P]),
     "codec_cost_grid": (I32, [I64, PI64, PI64, PF64, PI32, PI32, PI64, PI64, PF64]),
     "codec_cost_table_check": (I32, [I32, PI64, I32, PI64, I32, PI64, PF64]),
+    "codec_decode_attention_gather": (I32, [C.POINTER(Dims), C.POINTER(TableInfo), P, P, P, P, P, I64, P, P,
+                                            C.POINTER(PeerGatherC)]),
+    "codec_peer_wait": (I32, [P, I32, P, P]),
+    "codec_ipc_alloc": (I32, [I64, C.POINTER(P), P]),
+    "codec_ipc_free": (I32, [P]),
+    "codec_ipc_open": (I32, [P, C.POINTER(P)]),
+    "codec_ipc_close": (I32, [P]),
 }
 
 _lib = None

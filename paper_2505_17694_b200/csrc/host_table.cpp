@@ -408,6 +408,10 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   std::vector<int32_t> fz_req, fz_ptr{0}, fz_slot, fz_row;
   const bool mma_suffix = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 && !(dims->flags & CODEC_FLAG_GEMV_SIMT) &&
                           (dims->flags & CODEC_FLAG_FUSED_MERGE);
+  // MERGE_ALL (the fused peer-store gather): single-partial (request,
+  // head) pairs get a slot and a merge entry too, so only the merge kernel
+  // writes outputs
+  const bool merge_all = (dims->flags & CODEC_FLAG_MERGE_ALL) != 0;
   int32_t n_slots = 0, max_merge = 0;
   for (int32_t r = 0; r < bs; ++r) {
     auto& u = req_units[r];
@@ -422,7 +426,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       any_tc |= n_tc[h] > 0;
     }
     if (most == 0) return fail(CODEC_ERR_NO_VISIBLE_TOKENS, "request %d has no visible tokens anywhere on its path", r);
-    if (most == 1) {  // one partial on every head: direct
+    if (most == 1 && !merge_all) {  // one partial on every head: direct
       if (ns == 1) rows[4 * u[0][2] + 2] = -1 - r;
       for (auto& e : req_tc[r]) rows[4 * e.row + 2] = -1 - r;
       continue;
@@ -432,7 +436,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     for (int32_t i = 0; i < ns; ++i) rows[4 * u[i][2] + 2] = base + i;
     std::vector<int32_t> next(h_local, ns);
     for (auto& e : req_tc[r]) {
-      if (ns + n_tc[e.head] == 1) {
+      if (ns + n_tc[e.head] == 1 && !merge_all) {
         rows[4 * e.row + 2] = -1 - r;  // this head has just this piece
       } else {
         rows[4 * e.row + 2] = base + next[e.head]++;
@@ -442,11 +446,12 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     for (int32_t h = 0; h < h_local; ++h) all_heads &= n_tc[h] > 0;
     int32_t tc_most = 0;
     for (int32_t h = 0; h < h_local; ++h) tc_most = std::max(tc_most, n_tc[h]);
-    const bool fused = mma_suffix && ns == 1 && row_gemv[u[0][2]] && all_heads && tc_most <= 8 && g * 8 <= 64;
+    const bool fused = mma_suffix && !merge_all && ns == 1 && row_gemv[u[0][2]] && all_heads && tc_most <= 8 &&
+                       g * 8 <= 64;
     if (fused) fz_row.push_back((int32_t)u[0][2]);
     for (int32_t h = 0; h < h_local; ++h) {
       const int32_t tot = ns + n_tc[h];
-      if (tot < 2) continue;
+      if (tot < (merge_all ? 1 : 2)) continue;
       max_merge = std::max(max_merge, tot);
       auto& rq = fused ? fz_req : merge_req;
       auto& pt = fused ? fz_ptr : merge_ptr;

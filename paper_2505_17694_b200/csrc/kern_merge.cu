@@ -91,11 +91,28 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
 // pairs 32 at a time across the lanes, then the output vectors four
 // partials at a time with all four loads in flight (float4 per lane), so
 // the merge costs a few memory latencies instead of one per partial.
+// Fused output gather (codec_decode_attention_gather): every output row
+// goes to all n_peers ranks' global buffers, then the grid's last CTA bumps
+// this rank's arrival counter in every rank's flag array.
+struct PeerDev {
+  int n_peers, self, hq_global, head0;
+  float* const* peer_out;
+  int32_t* const* peer_flags;
+  const int32_t* row_map;
+  int32_t* done;
+};
+
+__device__ __forceinline__ void merge128_row(const int32_t* __restrict__ table, int off_req, int off_ptr,
+                                             int off_slot, int i, int k, int g, int h_local, int lane,
+                                             const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                             float* __restrict__ out, const PeerDev& pg);
+
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
                                                        const float* __restrict__ part_ml, float* __restrict__ out,
-                                                       const int32_t* tc_done, int tc_ctas, const int32_t* cnt) {
+                                                       const int32_t* tc_done, int tc_ctas, const int32_t* cnt,
+                                                       const PeerDev pg) {
   if (cnt) {
     // counted mode: no wait for whole grids -- this entry merges as soon
     // as its partial producers (TC epilogue rows, suffix / multi CTAs, all
@@ -119,7 +136,31 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const int k = blockIdx.y * 4 + warp;
-  if (i >= n_merge || k >= g) return;
+  if (i < n_merge && k < g) merge128_row(table, off_req, off_ptr, off_slot, i, k, g, h_local, lane, part_o, part_ml,
+                                         out, pg);
+  if (pg.n_peers > 0) {
+    // every CTA's peer stores system-visible before it is counted; the
+    // last CTA publishes this rank's rows to every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int total = gridDim.x * gridDim.y;
+      if (atomicAdd(pg.done, 1) == total - 1) {
+        *pg.done = 0;  // every other CTA already counted: reset for the next call
+        __threadfence_system();
+        for (int p = 0; p < pg.n_peers; ++p) {
+          int32_t* f = pg.peer_flags[p] + pg.self;
+          asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(f) : "memory");
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void merge128_row(const int32_t* __restrict__ table, int off_req, int off_ptr,
+                                             int off_slot, int i, int k, int g, int h_local, int lane,
+                                             const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                             float* __restrict__ out, const PeerDev& pg) {
   const int hq_local = g * h_local;
   const int code = table[off_req + i], req = code / h_local, qh = (code % h_local) * g + k;
   const int p0 = table[off_ptr + i], np = table[off_ptr + i + 1] - p0;
@@ -169,8 +210,14 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
     }
   }
   const float inv = 1.f / L;
-  reinterpret_cast<float4*>(out + ((int64_t)req * hq_local + qh) * 128)[lane] =
-      make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  const float4 res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  if (pg.n_peers > 0) {
+    const int64_t row = pg.row_map ? pg.row_map[req] : req;
+    const int64_t off = (row * pg.hq_global + pg.head0 + qh) * 128;
+    for (int p = 0; p < pg.n_peers; ++p) reinterpret_cast<float4*>(pg.peer_out[p] + off)[lane] = res;
+  } else {
+    reinterpret_cast<float4*>(out + ((int64_t)req * hq_local + qh) * 128)[lane] = res;
+  }
 }
 
 int32_t cuda_status(cudaError_t e, const char* what);
@@ -230,7 +277,13 @@ int32_t launch_merge_csr(int dtype, int n_req, int h_q, int d, const int32_t* pt
 
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas, bool pdl, const int32_t* cnt) {
+                     int tc_ctas, bool pdl, const int32_t* cnt, const codec_peer_gather* gather) {
+  PeerDev pg{0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr};
+  if (gather) {
+    if (dtype == CODEC_F64 || d != 128) return fail(CODEC_ERR_UNSUPPORTED, "fused gather: bf16 / f32, d = 128 only");
+    pg = PeerDev{gather->n_peers, gather->self, gather->hq_global, gather->head0,
+                 reinterpret_cast<float* const*>(gather->peer_out), gather->peer_flags, gather->row_map, gather->done};
+  }
   if (in.n_merge == 0) return CODEC_OK;
   const int h_local = in.h_local, g = hq_local / h_local;
   dim3 grid(in.n_merge, (g + 3) / 4);
@@ -254,7 +307,7 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
     cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, merge128_kernel, table, in.off_merge_req, in.off_merge_ptr,
                                        in.off_merge_slot, in.n_merge, g, h_local, (const float*)part_o,
-                                       (const float*)part_ml, (float*)out, tc_done, tc_ctas, cnt);
+                                       (const float*)part_ml, (float*)out, tc_done, tc_ctas, cnt, pg);
     if (e != cudaSuccess) return cuda_status(e, "merge launch");
     return cuda_status(cudaGetLastError(), "merge launch");
   }

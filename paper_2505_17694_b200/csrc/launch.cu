@@ -7,6 +7,7 @@
 // reduce_tree, executor.py:177-179, :267-293). Requests with a single
 // partial were written straight to `out` by their split kernel.
 #include <cuda_runtime.h>
+#include <string.h>
 
 #include "common.h"
 #include "device_table.h"
@@ -35,7 +36,7 @@ int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
 int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in, int d, int hq_local,
                      const void* part_o, const void* part_ml, void* out, cudaStream_t st, const int32_t* tc_done,
-                     int tc_ctas, bool pdl, const int32_t* cnt);
+                     int tc_ctas, bool pdl, const int32_t* cnt, const codec_peer_gather* gather);
 int32_t cuda_status(cudaError_t e, const char* what);
 }  // namespace codec
 
@@ -124,10 +125,10 @@ extern "C" int32_t codec_debug_ctalog(long long* host, int64_t n) {
   return codec::cuda_status(cudaMemcpy(host, g_ctalog, n * sizeof(long long), cudaMemcpyDeviceToHost), "ctalog copy");
 }
 
-extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
-                                             const int32_t* table_dev, const void* q, const void* k, const void* v,
-                                             void* out, void* workspace, int64_t workspace_bytes, void* stream,
-                                             void* aux_stream, codec_kernel_timer* timer) {
+static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info, const int32_t* table_dev,
+                           const void* q, const void* k, const void* v, void* out, void* workspace,
+                           int64_t workspace_bytes, void* stream, void* aux_stream, codec_kernel_timer* timer,
+                           const codec_peer_gather* gather) {
   // ---- every argument / eligibility check before the first enqueue: an
   // error leaves the stream, the output and the workspace untouched
   if (!dims || !info || !table_dev) return fail(CODEC_ERR_VALUE, "NULL argument");
@@ -257,13 +258,94 @@ extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec
                            done_target ? tc_done : nullptr, done_target,
                            (mma_gemv || do_multi || counted) && !fork && !kev &&
                                !(dims->flags & CODEC_FLAG_SKIP_GEMV) && !(dims->flags & CODEC_FLAG_MERGE_NO_PDL),
-                           cnt));
+                           cnt, gather));
   if (kev) {
     CODEC_TRY(kev_record(timer, 3, st));
     ++timer->n;
   }
   return CODEC_OK;
 }
+
+extern "C" int32_t codec_decode_attention_ex(const codec_dims* dims, const codec_table_info* info,
+                                             const int32_t* table_dev, const void* q, const void* k, const void* v,
+                                             void* out, void* workspace, int64_t workspace_bytes, void* stream,
+                                             void* aux_stream, codec_kernel_timer* timer) {
+  return decode_impl(dims, info, table_dev, q, k, v, out, workspace, workspace_bytes, stream, aux_stream, timer,
+                     nullptr);
+}
+
+// ---------------------------------------------------------------- fused gather
+extern "C" int32_t codec_decode_attention_gather(const codec_dims* dims, const codec_table_info* info,
+                                                 const int32_t* table_dev, const void* q, const void* k,
+                                                 const void* v, void* workspace, int64_t workspace_bytes,
+                                                 void* stream, void* aux_stream, const codec_peer_gather* pg) {
+  if (!dims || !info || !pg) return fail(CODEC_ERR_VALUE, "NULL argument");
+  if (!(dims->flags & CODEC_FLAG_MERGE_ALL))
+    return fail(CODEC_ERR_VALUE, "the fused gather needs a table built with CODEC_FLAG_MERGE_ALL");
+  if (dims->flags & (CODEC_FLAG_SKIP_MERGE | CODEC_FLAG_FUSED_MERGE | CODEC_FLAG_COUNTED_MERGE))
+    return fail(CODEC_ERR_VALUE, "the fused gather needs the plain merge kernel");
+  if (dims->kv_dtype != CODEC_BF16 || dims->d != 128)
+    return fail(CODEC_ERR_UNSUPPORTED, "the fused gather needs bf16 KV and d = 128");
+  if (pg->n_peers < 1 || pg->self < 0 || pg->self >= pg->n_peers || !pg->peer_out || !pg->peer_flags || !pg->done)
+    return fail(CODEC_ERR_VALUE, "bad peer gather (%d peers, self %d)", pg->n_peers, pg->self);
+  const int g = dims->h_kv > 0 ? dims->h_q / dims->h_kv : 0;
+  const int hq_local = info->h_local * g;
+  if (pg->head0 < 0 || pg->head0 + hq_local > pg->hq_global)
+    return fail(CODEC_ERR_DIMENSION_MISMATCH, "q heads [%d, %d) outside the %d of the gathered rows", pg->head0,
+                pg->head0 + hq_local, pg->hq_global);
+  if (info->n_merge == 0) return fail(CODEC_ERR_VALUE, "the fused gather needs merge entries");
+  // the split kernels write no output rows (MERGE_ALL): any non-NULL
+  // pointer satisfies their signature
+  return decode_impl(dims, info, table_dev, q, k, v, workspace, workspace, workspace_bytes, stream, aux_stream, nullptr,
+                     pg);
+}
+
+namespace {
+__global__ void peer_wait_kernel(const int32_t* flags, int n_peers, int32_t* expected) {
+  const int32_t want = *expected + 1;
+  for (int p = 0; p < n_peers; ++p) {
+    int v;
+    for (long long it = 0;; ++it) {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + p) : "memory");
+      if (v >= want) break;
+      if (it > (1ll << 26)) __trap();  // a peer that never arrives: trap rather than hang the GPU
+      __nanosleep(200);
+    }
+  }
+  *expected = want;
+  __threadfence();
+}
+}  // namespace
+
+extern "C" int32_t codec_peer_wait(const int32_t* flags, int32_t n_peers, int32_t* expected, void* stream) {
+  if (!flags || !expected || n_peers < 1) return fail(CODEC_ERR_VALUE, "bad peer wait arguments");
+  peer_wait_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flags, n_peers, expected);
+  return cuda_status(cudaGetLastError(), "peer wait launch");
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "codec_ipc_* pass 64-byte handles");
+extern "C" int32_t codec_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64) {
+  if (bytes <= 0 || !dev_ptr || !handle64) return fail(CODEC_ERR_VALUE, "bad ipc alloc arguments");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_status(e, "ipc alloc");
+  e = cudaMemset(p, 0, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle64), p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_status(e, "ipc handle");
+  }
+  *dev_ptr = p;
+  return CODEC_OK;
+}
+extern "C" int32_t codec_ipc_free(void* dev_ptr) { return cuda_status(cudaFree(dev_ptr), "ipc free"); }
+extern "C" int32_t codec_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(CODEC_ERR_VALUE, "bad ipc open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  return cuda_status(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+}
+extern "C" int32_t codec_ipc_close(void* dev_ptr) { return cuda_status(cudaIpcCloseMemHandle(dev_ptr), "ipc close"); }
 
 extern "C" int32_t codec_decode_attention(const codec_dims* dims, const codec_table_info* info,
                                           const int32_t* table_dev, const void* q, const void* k, const void* v,

@@ -36,6 +36,7 @@ FLAG_NO_TC = 1
 FLAG_FORCE_TC = 2
 FLAG_NO_GEMV = 4
 FLAG_NO_MULTI = 524288
+FLAG_MERGE_ALL = 2097152  # every output row through the merge kernel (the fused peer-store gather needs it)
 
 
 @dataclass
@@ -205,6 +206,48 @@ class DecodeStep:
             C.c_void_p(self.workspace.data_ptr()), self.workspace.numel(), C.c_void_p(st.cuda_stream),
             C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None, self._timer))
         return out
+
+    def gather(self, q, k_pool, v_pool, peers, head0=None, row_map=None, buf=0, stream=None):
+        """The step with the fused multi-GPU output gather (parallel.PeerGather;
+        SURVEY.md §8(e) K5): the merge kernel stores this rank's output rows
+        straight into every rank's global output buffer `buf` and signals
+        them; call peers.wait(stream) before reading peers.output(buf).
+        head0: this rank's first q head in the global rows (default
+        head_begin * g); row_map: device int32 [bs] global row of each local
+        request (tree partition; None = identity). The step must be built
+        with FLAG_MERGE_ALL."""
+        import torch
+
+        if not self.flags & FLAG_MERGE_ALL:
+            raise ValueError("gather() needs a DecodeStep built with flags |= FLAG_MERGE_ALL")
+        bs = self.forest.bs
+        self._check("q", q, (bs, self.hq_local, self.d), self.tdtype)
+        pool_shape = (self.h_local, self.pool_tokens, self.d)
+        self._check("k_pool", k_pool, pool_shape, self.tdtype)
+        self._check("v_pool", v_pool, pool_shape, self.tdtype)
+        if row_map is not None:
+            self._check("row_map", row_map, (bs,), torch.int32)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        pg = peers.struct(self.head_begin * self.g if head0 is None else int(head0), row_map, buf)
+        _lib.check(_lib.lib().codec_decode_attention_gather(
+            C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
+            C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(self.workspace.data_ptr()),
+            self.workspace.numel(), C.c_void_p(st.cuda_stream),
+            C.c_void_p(self.aux.cuda_stream) if self.aux is not None else None, C.byref(pg)))
+
+    def capture_gather(self, q, k_pool, v_pool, peers, head0=None, row_map=None, buf=0):
+        """CUDA graph of gather() + peers.wait() over these buffers; returns
+        its replay function."""
+        import torch
+
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self.gather(q, k_pool, v_pool, peers, head0, row_map, buf, stream=s)
+            peers.wait(s)
+        self._graphs.append(graph)
+        return graph.replay
 
     def capture(self, q, k_pool, v_pool, out):
         """Record one decode step over these buffers into a CUDA graph and

@@ -19,7 +19,11 @@ PAPER.md:506), so the step shards with no cross-GPU reduction:
     the per-rank outputs and scatters them back into global request order.
 
 The collective goes through torch.distributed: NCCL over NVLink on the
-B200 box, gloo in the CPU tests of the partition / reassembly logic.
+B200 box, gloo in the CPU tests of the partition / reassembly logic --
+or, fused (`PeerGather`), through peer memory: every
+rank's merge kernel stores its output rows straight into all ranks'
+global output buffers over NVLink / NVSwitch and bumps one arrival
+counter per rank; no NCCL call on the data path.
 """
 from __future__ import annotations
 
@@ -214,3 +218,127 @@ def gather_requests(local_out, shards, bs: int, group=None, buf=None):
         buf = torch.empty((world,) + tuple(send.shape), dtype=send.dtype, device=send.device)
     dist.all_gather_into_tensor(buf.view((world * n_max,) + tuple(send.shape[1:])), send.contiguous(), group=group)
     return scatter_requests(buf, shards, bs)
+
+
+# ------------------------------------------------------------ fused gather
+class _DevArray:
+    """__cuda_array_interface__ view of a raw device allocation."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerGather:
+    """Symmetric output buffers for the fused output gather
+    (codec_decode_attention_gather, include/codec_b200.h): `buffers` global
+    outputs float32 [rows, hq_global, d] and one int32 [world] arrival
+    counter array per rank, allocated by the library (cudaMalloc + CUDA IPC
+    handle) and mapped into every rank of `group` (handles exchanged with
+    all_gather_object -- gloo or NCCL). Works across GPUs (peer stores
+    over NVLink) and across processes sharing one GPU (the tests).
+
+    Per step: DecodeStep.gather(..., peers=self, buf=b) on every rank, then
+    wait(stream); output(b) then holds every rank's rows. A buffer is
+    rewritten by the next step that targets it: consumers double-buffer."""
+
+    def __init__(self, rows: int, hq_global: int, d: int, device, group=None, buffers: int = 1):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        L = _lib.lib()
+        self.device = torch.device(device)
+        self.rows, self.hq_global, self.d = int(rows), int(hq_global), int(d)
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        nbytes = max(self.rows * self.hq_global * self.d * 4, 16)
+        self._own, self._opened = [], []
+
+        def alloc(n):
+            ptr, h = C.c_void_p(), (C.c_char * 64)()
+            _lib.check(L.codec_ipc_alloc(n, C.byref(ptr), h))
+            self._own.append(ptr.value)
+            return ptr.value, bytes(h)
+
+        mine = [alloc(nbytes) for _ in range(int(buffers))] + [alloc(max(4 * self.world, 16))]
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, [h for _, h in mine], group=group)
+        else:
+            allh = [[h for _, h in mine]]
+        ptrs = []  # ptrs[p][j]: rank p's allocation j mapped here
+        for p in range(self.world):
+            if p == self.rank:
+                ptrs.append([ptr for ptr, _ in mine])
+                continue
+            row = []
+            for h in allh[p]:
+                ptr = C.c_void_p()
+                _lib.check(L.codec_ipc_open(C.create_string_buffer(h, 64), C.byref(ptr)))
+                self._opened.append(ptr.value)
+                row.append(ptr.value)
+            ptrs.append(row)
+        self.buffers = int(buffers)
+        self._peer_out = [torch.tensor([ptrs[p][b] for p in range(self.world)], dtype=torch.int64, device=self.device)
+                          for b in range(self.buffers)]
+        self._peer_flags = torch.tensor([ptrs[p][-1] for p in range(self.world)], dtype=torch.int64,
+                                        device=self.device)
+        self._flags_local = mine[-1][0]
+        self._done = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._expected = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._out_views = [torch.as_tensor(_DevArray(mine[b][0], (self.rows, self.hq_global, self.d), "<f4"),
+                                           device=self.device) for b in range(self.buffers)]
+
+    def struct(self, head0: int, row_map=None, buf: int = 0):
+        import ctypes as C
+
+        from . import _lib
+
+        return _lib.PeerGatherC(self.world, self.rank, self.hq_global, int(head0),
+                                C.c_void_p(self._peer_out[buf].data_ptr()), C.c_void_p(self._peer_flags.data_ptr()),
+                                C.c_void_p(row_map.data_ptr()) if row_map is not None else None,
+                                C.c_void_p(self._done.data_ptr()))
+
+    def wait(self, stream=None):
+        """Make `stream` wait until every rank's rows of the next step
+        arrived here."""
+        import ctypes as C
+
+        import torch
+
+        from . import _lib
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().codec_peer_wait(C.c_void_p(self._flags_local), self.world,
+                                              C.c_void_p(self._expected.data_ptr()), C.c_void_p(st.cuda_stream)))
+
+    def output(self, buf: int = 0):
+        """The gathered global output [rows, hq_global, d] (float32) of `buf`."""
+        return self._out_views[buf]
+
+    def close(self):
+        """Unmap the peers' buffers and free this rank's (after a barrier:
+        no peer may still be storing into them)."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if not (self._own or self._opened):
+            return
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        L = _lib.lib()
+        for ptr in self._opened:
+            L.codec_ipc_close(ptr)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+        for ptr in self._own:
+            L.codec_ipc_free(ptr)
+        self._own, self._opened, self._out_views = [], [], []
