@@ -1,7 +1,8 @@
 """Paged KV pools (paging.py, codec_dims.page_size / page_table): the page
 layout and the table builder's checks on CPU; on the GPU, a step over
 randomly permuted physical pages equals the step over the contiguous pool
-bit for bit (same tiles, same order, same arithmetic)."""
+bit for bit (same tiles, same order, same arithmetic) and the float64
+oracle within the bf16 bar."""
 from __future__ import annotations
 
 import ctypes as C
@@ -119,3 +120,19 @@ class TestPaged:
             torch.cuda.synchronize()
             assert torch.isfinite(ref).all()
             assert torch.equal(ref, got), (page, shape, concurrent, float((ref - got).abs().max()))
+        # and the paged output against the float64 restatement of the
+        # reference's single-softmax attention (oracle/attention.py
+        # naive_attention, attention.py:164-187) on the same bf16 values,
+        # every request: the bf16 bar of the north star
+        from oracle import attention as OA
+        up = lambda t: t.double().cpu().numpy()
+        kp_h, vp_h = up(kp), up(vp)
+        z = np.zeros((0, 8, 128))
+        node_k = [z] + [kp_h[:, f.token_offset[n]:f.token_offset[n] + f.nodes[n].len].transpose(1, 0, 2)
+                        for n in range(1, len(f.nodes))]
+        node_v = [z] + [vp_h[:, f.token_offset[n]:f.token_offset[n] + f.nodes[n].len].transpose(1, 0, 2)
+                        for n in range(1, len(f.nodes))]
+        fd = OA.ForestData(spec.parent, node_k, node_v, spec.paths)
+        want = OA.naive_attention(up(q), fd)
+        err = np.abs(got.double().cpu().numpy() - want)
+        assert err.max() <= 2e-3 and err.max() / np.abs(want).max() <= 1e-2, (page, shape, float(err.max()))
