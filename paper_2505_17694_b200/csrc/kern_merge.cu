@@ -107,6 +107,8 @@ __device__ __forceinline__ void merge128_row(const int32_t* __restrict__ table, 
                                              const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                              float* __restrict__ out, const PeerDev& pg);
 
+constexpr int kFastNp = 8;  // partials per entry merged with all their loads in flight at once
+
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
                                                        const float* __restrict__ part_o,
@@ -130,14 +132,69 @@ __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict
       }
     }
     __syncthreads();
-  } else {
-    wait_tc_done(tc_done, tc_ctas);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const int k = blockIdx.y * 4 + warp;
-  if (i < n_merge && k < g) merge128_row(table, off_req, off_ptr, off_slot, i, k, g, h_local, lane, part_o, part_ml,
-                                         out, pg);
+  const bool active = i < n_merge && k < g;
+  // The entry's task-table data (static) before waiting for the producers:
+  // after the wait only the partials' loads remain, (m, l) and o of up to
+  // kFastNp partials all in flight at once -- one memory latency instead of
+  // three on the step's tail.
+  const int hq_local = g * h_local;
+  int req = 0, qh = 0, np = 0;
+  int64_t ep[kFastNp] = {};
+  if (active) {
+    const int code = __ldg(table + off_req + i);
+    req = code / h_local;
+    qh = (code % h_local) * g + k;
+    const int p0 = __ldg(table + off_ptr + i);
+    np = __ldg(table + off_ptr + i + 1) - p0;
+#pragma unroll
+    for (int p = 0; p < kFastNp; ++p)
+      if (p < np) ep[p] = (int64_t)__ldg(table + off_slot + p0 + p) * hq_local + qh;
+  }
+  if (!cnt) wait_tc_done(tc_done, tc_ctas);
+  if (active && np <= kFastNp) {
+    float2 ml[kFastNp];
+    float4 o[kFastNp];
+#pragma unroll
+    for (int p = 0; p < kFastNp; ++p) {
+      ml[p] = make_float2(0.f, 0.f);
+      o[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < np) {
+        ml[p] = __ldg(reinterpret_cast<const float2*>(part_ml) + ep[p]);
+        o[p] = __ldg(reinterpret_cast<const float4*>(part_o + ep[p] * 128) + lane);
+      }
+    }
+    float M = neg_inf<float>();
+#pragma unroll
+    for (int p = 0; p < kFastNp; ++p)
+      if (ml[p].y > 0) M = fmaxf(M, ml[p].x);
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < kFastNp; ++p) {
+      if (!(ml[p].y > 0)) continue;  // an empty partial (its o may be 0/0)
+      const float w = ml[p].y * __expf(ml[p].x - M);
+      L += w;
+      acc.x += w * o[p].x;
+      acc.y += w * o[p].y;
+      acc.z += w * o[p].z;
+      acc.w += w * o[p].w;
+    }
+    const float inv = 1.f / L;
+    const float4 res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (pg.n_peers > 0) {
+      const int64_t row = pg.row_map ? pg.row_map[req] : req;
+      const int64_t off = (row * pg.hq_global + pg.head0 + qh) * 128;
+      for (int p = 0; p < pg.n_peers; ++p) reinterpret_cast<float4*>(pg.peer_out[p] + off)[lane] = res;
+    } else {
+      reinterpret_cast<float4*>(out + ((int64_t)req * hq_local + qh) * 128)[lane] = res;
+    }
+  } else if (active) {
+    merge128_row(table, off_req, off_ptr, off_slot, i, k, g, h_local, lane, part_o, part_ml, out, pg);
+  }
   if (pg.n_peers > 0) {
     // every CTA's peer stores system-visible before it is counted; the
     // last CTA publishes this rank's rows to every rank
