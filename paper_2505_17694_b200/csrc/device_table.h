@@ -45,6 +45,9 @@ constexpr int kMultiMaxRows = CODEC_MULTI_MAX_ROWS;
 constexpr int kTcGroupRows = 256;
 // SMs (CTAs) that run one tensor-core schedule block
 constexpr int kTcCtasPerBlock = 2;
+// device balancer: a unit boundary inside a CTA pair costs this many KV
+// tiles (host_table.cpp; CODEC_TC_UNIT_COST overrides)
+constexpr int kTcUnitCostDefault = 0;
 
 // debug CTA log (CODEC_FLAG_CTALOG): TC records first, GEMV from this index
 constexpr int kCtaLogGemv = 4096;

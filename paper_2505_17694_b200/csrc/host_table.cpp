@@ -13,6 +13,7 @@
 // the GEMV / generic kernels. CTA = group x local kv head.
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <map>
 #include <set>
 #include <sstream>
@@ -44,6 +45,16 @@ struct codec_table {
 };
 
 namespace {
+// Cost of a unit boundary inside a CTA pair, in KV tiles (device balancer
+// below). CODEC_TC_UNIT_COST overrides it (tuning).
+int64_t tc_unit_cost() {
+  static const int64_t v = [] {
+    const char* e = getenv("CODEC_TC_UNIT_COST");
+    return e ? (int64_t)atoll(e) : (int64_t)codec::kTcUnitCostDefault;
+  }();
+  return v;
+}
+
 
 std::string py_list(const std::vector<int64_t>& v) {
   std::ostringstream os;
@@ -279,6 +290,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int32_t grp, head, t0, t1, pair;
   };
   std::vector<Piece> pieces;
+  const int64_t kTcUnitCost = tc_unit_cost();
   std::vector<int32_t> tcg;  // indices of TC groups in `groups`
   for (size_t i = 0; i < groups.size(); ++i)
     if (groups[i].kind == kKindTc) tcg.push_back((int32_t)i);
@@ -314,54 +326,118 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
       for (int32_t gi : lanes[c]) lane_w[c] += tiles_of(gi) * h_local;
       w_all += lane_w[c];
     }
-    // Every pair gets T = ceil(W / pairs) tiles. Lane c runs on floor(W_c /
-    // T) pairs of its own (in lockstep with the other lanes); the tails
-    // that do not fill a whole pair -- the ends of the lanes, which cover
-    // the same KV region in every lane -- are pooled in lane order and cut
-    // for the remaining pairs. (Whole lanes only would idle pairs whenever
-    // the lane count does not divide them: 10 of 74 at 16 lanes.)
-    const int64_t T = std::max<int64_t>(1, (w_all + pairs - 1) / pairs);
-    std::vector<int32_t> lane_p(lanes.size(), 0);
-    int32_t used = 0;
-    for (size_t c = 0; c < lanes.size(); ++c) {
-      lane_p[c] = (int32_t)(lane_w[c] / T);
-      used += lane_p[c];
-    }
-    // (lane-major unit sequence; pos = tiles of the lane before the unit)
-    int32_t tail_pair = used;  // pairs after the lane pairs take the pooled tails
-    int64_t tail_pos = 0;      // tiles already cut from the pool
-    int32_t pair0 = 0;
-    for (size_t c = 0; c < lanes.size(); ++c) {
-      if (lane_w[c] == 0) continue;
-      const int64_t main_end = (int64_t)lane_p[c] * T;  // lane tiles on the lane's own pairs
-      int64_t pos = 0;
-      for (int32_t gi : lanes[c])
-        for (int32_t h = 0; h < h_local; ++h) {
-          const int64_t nt = tiles_of(gi);
-          int64_t t = 0;
-          while (t < nt) {
-            int64_t take, pair;
-            if (pos < main_end) {
-              const int64_t k = pos / T;
-              take = std::min(nt - t, (k + 1) * T - pos);
-              pair = pair0 + k;
-            } else {
-              const int64_t k = tail_pos / T;
-              take = std::min(nt - t, (k + 1) * T - tail_pos);
-              pair = tail_pair + std::min<int64_t>(k, std::max(0, pairs - 1 - tail_pair));
-              tail_pos += take;
-            }
-            pieces.push_back({gi, h, (int32_t)t, (int32_t)(t + take), (int32_t)pair});
-            t += take;
-            pos += take;
+    // Every pair gets a budget of C cost units, a KV tile costing 1 and
+    // every piece after a pair's first kTcUnitCost more (a unit boundary
+    // inside a pair costs an epilogue and a pipeline refill, ~4-5 us on
+    // B200: the pairs that cross one ran ~7 % longer for the same tiles).
+    // Each lane's unit sequence is cut greedily into C-unit pairs of its own
+    // (in lockstep with the other lanes: the same sequence is cut the same
+    // way); what does not fill a whole pair -- the ends of the lanes, which
+    // cover the same KV region in every lane -- is pooled in lane order and
+    // cut the same way for the remaining pairs. (Whole lanes only would
+    // idle pairs whenever the lane count does not divide them: 10 of 74 at
+    // 16 lanes.) C is the smallest budget that needs no more than `pairs`
+    // pairs; with kTcUnitCost = 0 it is ceil(W / pairs).
+    struct Cut {
+      int32_t gi, h;
+      int64_t t0, t1, pair;
+    };
+    auto cut_lane = [&](const std::vector<std::pair<int32_t, int32_t>>& units,
+                        const std::vector<std::array<int64_t, 2>>& ranges, int64_t C, int64_t pair_base,
+                        std::vector<Cut>* out, std::vector<std::array<int64_t, 4>>* left) {
+      // greedy: returns the closed pairs; the open one's pieces go to *left
+      int64_t closed = 0, cost = 0;
+      size_t open_begin = out ? out->size() : 0;
+      std::vector<std::array<int64_t, 4>> cur;  // (unit index, t0, t1) of the open pair
+      for (size_t u = 0; u < units.size(); ++u) {
+        int64_t t = ranges[u][0];
+        const int64_t nt = ranges[u][1];
+        while (t < nt) {
+          const int64_t extra = cur.empty() ? 0 : kTcUnitCost;
+          const int64_t room = C - cost - extra;
+          if (room <= 0) {
+            ++closed;
+            cost = 0;
+            cur.clear();
+            if (out) open_begin = out->size();
+            continue;
+          }
+          const int64_t take = std::min(nt - t, room);
+          cur.push_back({(int64_t)u, t, t + take, 0});
+          if (out) out->push_back({units[u].first, units[u].second, t, t + take, pair_base + closed});
+          cost += take + extra;
+          t += take;
+          if (cost >= C) {
+            ++closed;
+            cost = 0;
+            cur.clear();
+            if (out) open_begin = out->size();
           }
         }
-      pair0 += lane_p[c];
+      }
+      if (out) out->resize(open_begin);  // the open pair's pieces are not this lane's
+      if (left)
+        for (auto& x : cur) left->push_back(x);
+      return closed;
+    };
+    // lane unit sequences: (group, head) with tile ranges [0, tiles)
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> lane_units(lanes.size());
+    std::vector<std::vector<std::array<int64_t, 2>>> lane_ranges(lanes.size());
+    for (size_t c = 0; c < lanes.size(); ++c)
+      for (int32_t gi : lanes[c])
+        for (int32_t h = 0; h < h_local; ++h) {
+          lane_units[c].push_back({gi, h});
+          lane_ranges[c].push_back({0, tiles_of(gi)});
+        }
+    // pairs a budget C needs (lane pairs + pooled tail pairs)
+    auto pool_of = [&](int64_t C, std::vector<std::pair<int32_t, int32_t>>* pu,
+                       std::vector<std::array<int64_t, 2>>* pr) {
+      int64_t used_c = 0;
+      for (size_t c = 0; c < lanes.size(); ++c) {
+        std::vector<std::array<int64_t, 4>> left;
+        used_c += cut_lane(lane_units[c], lane_ranges[c], C, 0, nullptr, &left);
+        for (auto& x : left) {
+          pu->push_back(lane_units[c][x[0]]);
+          pr->push_back({x[1], x[2]});
+        }
+      }
+      return used_c;
+    };
+    auto pairs_needed = [&](int64_t C) {
+      std::vector<std::pair<int32_t, int32_t>> pu;
+      std::vector<std::array<int64_t, 2>> pr;
+      const int64_t used_c = pool_of(C, &pu, &pr);
+      std::vector<std::array<int64_t, 4>> left;
+      const int64_t tail_c = cut_lane(pu, pr, C, 0, nullptr, &left);
+      return used_c + tail_c + (left.empty() ? 0 : 1);
+    };
+    int64_t lo = std::max<int64_t>(1, (w_all + pairs - 1) / pairs), hi = lo;
+    while (pairs_needed(hi) > pairs) hi = hi * 2;
+    while (lo < hi) {  // smallest budget that fits (pairs_needed is non-increasing in C)
+      const int64_t mid = (lo + hi) / 2;
+      if (pairs_needed(mid) <= pairs) hi = mid; else lo = mid + 1;
     }
-    const int32_t n_tail = (int32_t)((tail_pos + T - 1) / T);
-    n_pairs = std::min<int32_t>(pairs, used + n_tail);
-    pair0 = n_pairs;
-    n_pairs = pair0;
+    const int64_t C = lo;
+    std::vector<Cut> cuts;
+    int64_t pair0 = 0;
+    std::vector<std::pair<int32_t, int32_t>> pool_u;
+    std::vector<std::array<int64_t, 2>> pool_r;
+    for (size_t c = 0; c < lanes.size(); ++c) {
+      std::vector<std::array<int64_t, 4>> left;
+      pair0 += cut_lane(lane_units[c], lane_ranges[c], C, pair0, &cuts, &left);
+      for (auto& x : left) {
+        pool_u.push_back(lane_units[c][x[0]]);
+        pool_r.push_back({x[1], x[2]});
+      }
+    }
+    {
+      std::vector<std::array<int64_t, 4>> left;
+      const int64_t tail_closed = cut_lane(pool_u, pool_r, C, pair0, &cuts, &left);
+      for (auto& x : left)  // the last, partly filled tail pair
+        cuts.push_back({pool_u[x[0]].first, pool_u[x[0]].second, x[1], x[2], pair0 + tail_closed});
+      n_pairs = (int32_t)(pair0 + tail_closed + (left.empty() ? 0 : 1));
+    }
+    for (auto& x : cuts) pieces.push_back({x.gi, x.h, (int32_t)x.t0, (int32_t)x.t1, (int32_t)x.pair});
   }
   // piece rows (their own records: visible tokens within the piece) and the
   // per-(request, head) TC contributions, in piece order

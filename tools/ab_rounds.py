@@ -2,7 +2,8 @@
 once (subprocess: tensor-core kernel alone at a fixed SM budget, 200 calls,
 and the full step at that budget), medians over rounds.
 
-    python tools/ab_rounds.py rounds budget tag1 tag2 ...   (tag '-' = default library)
+    python tools/ab_rounds.py rounds budget tag1 tag2 ...   (tag '-' = default library;
+    tag@N also sets CODEC_TC_UNIT_COST=N)
 """
 import json, os, statistics, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -28,8 +29,11 @@ res = {t: [] for t in tags}
 for r in range(rounds):
     for tag in tags:
         env = dict(os.environ)
-        if tag != '-':
-            env["CODEC_B200_LIB"] = os.path.join(ROOT, "paper_2505_17694_b200", f"_codec_b200_{tag}.so")
+        lib, _, cost = tag.partition("@")
+        if cost:
+            env["CODEC_TC_UNIT_COST"] = cost
+        if lib != '-':
+            env["CODEC_B200_LIB"] = os.path.join(ROOT, "paper_2505_17694_b200", f"_codec_b200_{lib}.so")
         out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, budget)], env=env, capture_output=True, text=True)
         line = [l for l in out.stdout.splitlines() if l.startswith("{")]
         res[tag].append(json.loads(line[-1]) if line else {"err": out.stderr[-300:]})
