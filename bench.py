@@ -287,7 +287,7 @@ def prepare(config="cfg2", dev=None, rank=0, world=1, partition=None, flags=0, s
         if blocks:
             pl = P.divide_and_schedule(P.device_tasks(forest, g), table, blocks)
         else:
-            pl = P.plan_device(forest, g, table, h_local, sms, budget)
+            pl = P.plan_device(forest, g, table, h_local, sms, budget, multi=not (flags & 524288))  # FLAG_NO_MULTI
         ms_plan = (time.perf_counter() - t0) * 1e3
         st = DecodeStep(forest, pl, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
                         flags=flags, tc_sm_budget=budget, concurrent=not serial)

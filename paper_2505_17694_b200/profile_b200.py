@@ -9,7 +9,8 @@ rows of one kv head over n tokens.
 stream K+V (512 B/token at d=128 bf16) at a per-SM share of measured HBM
 bandwidth; tensor-core CTAs cost a fixed time per 128-token tile per
 128-row M tile. `measure` replaces it with CUDA-event timings of the real
-kernels on single-node forests (one CTA per SM, all SMs busy) and writes
+kernels (see measure_table: one work unit on one CTA slot with every slot
+busy, graph-replayed, launch overhead excluded) and writes
 profiles/b200_d128.csv.
 """
 from __future__ import annotations
@@ -41,39 +42,64 @@ def model_table() -> CostTable:
     return CostTable(NQ_KNOTS, N_KNOTS, grid, meta={"d": "128", "hardware": "b200", "source": "roofline-model"})
 
 
-def measure_table(reps: int = 5) -> CostTable:
+def measure_table(reps: int = 40, h_q: int = 32, h_kv: int = 8, d: int = 128) -> CostTable:
+    """cost_ms(n_q, n) = device time of ONE work unit -- one kv head of a
+    subtask of n_q requests x n tokens -- on one CTA slot of the kernel the
+    device router picks for it (a CTA pair of the tensor-core kernel for
+    more than MULTI_MAX_ROWS query-head rows, a CTA of the multi-request or
+    the suffix kernel below), with every slot of the GPU busy: U identical
+    single-node trees, the step's other kernels skipped, the launch replayed
+    from a CUDA graph (no launch overhead), kernel time / waves of units."""
     import torch
 
-    from . import DecodeStep, Task, forest_from_pool, plan_uniform_bk
-    from .cost_model import load_profile
+    from . import DecodeStep, device_tasks, forest_from_pool, plan_uniform_bk
+    from .executor import FLAG_NO_MULTI  # noqa: F401  (documented knob)
+    from .scheduler import MULTI_MAX_ROWS, TC_CTAS_PER_BLOCK, node_kernel
 
     dev = torch.device("cuda")
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    g = h_q // h_kv
     grid = np.zeros((len(N_KNOTS), len(NQ_KNOTS)))
-    h_kv, d = sms, 128   # one CTA per SM: `sms` kv heads, g = 1 row per request... (rows = n_q)
+    table = model_table()
+    slots_of = {"tc": sms // TC_CTAS_PER_BLOCK, "multi": sms * 3, "gemv": sms * 6}
+    skip = {"tc": 8 | 32 | 64, "multi": 8 | 16 | 64, "gemv": 8 | 16 | 64}
     for i, n in enumerate(N_KNOTS):
         for j, nq in enumerate(NQ_KNOTS):
-            g = 1
-            reqs = nq
-            f = forest_from_pool([0], [n], [(1,)] * reqs, h_kv, d)
-            k = torch.randn(h_kv, n, d, device=dev, dtype=torch.bfloat16) * (1 / math.sqrt(d))
-            v = torch.randn_like(k)
-            q = torch.randn(reqs, h_kv * g, d, device=dev, dtype=torch.bfloat16) * (1 / math.sqrt(d))
-            tab = load_profile(OUT) if OUT.exists() else model_table()
-            plan = plan_uniform_bk([Task(1, reqs, n)], tab, 1, 1)
-            step = DecodeStep(f, plan, h_kv * g, "bfloat16")
-            for _ in range(2):
-                step(q, k, v)
+            kind = node_kernel(nq * g, nq, True)
+            lanes = -(-nq * g // 256) if kind == "tc" else 1
+            slots = slots_of[kind]
+            per_tree = h_kv * lanes
+            U = max(1, -(-2 * slots // per_tree))           # ~2 full waves of units
+            U = max(1, min(U, (1 << 25) // (n * h_kv)))     # bounded pool (<= 2^25 token-heads)
+            f = forest_from_pool([0] * U, [n] * U, [(t + 1,) for t in range(U) for _ in range(nq)], h_kv, d)
+            T = f.total_tokens
+            k = (torch.randn(h_kv, T, d, device=dev) / math.sqrt(d)).to(torch.bfloat16)
+            v = (torch.randn(h_kv, T, d, device=dev) / math.sqrt(d)).to(torch.bfloat16)
+            q = (torch.randn(f.bs, h_q, d, device=dev) / math.sqrt(d)).to(torch.bfloat16)
+            plan = plan_uniform_bk(device_tasks(f, g), table, slots, 1)
+            step = DecodeStep(f, plan, h_q, "bfloat16", flags=skip[kind], tc_sm_budget=sms, concurrent=False)
+            out = torch.empty((f.bs, h_q, d), dtype=torch.float32, device=dev)
+            replay = step.capture(q, k, v, out)
+            for _ in range(3):
+                replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(reps):
-                step(q, k, v)
+                replay()
             e1.record()
             torch.cuda.synchronize()
-            grid[i, j] = e0.elapsed_time(e1) / reps
-            print(json.dumps({"n": n, "n_q": nq, "ms": grid[i, j]}), flush=True)
-    return CostTable(NQ_KNOTS, N_KNOTS, grid, meta={"d": "128", "hardware": "b200", "source": "measured"})
+            ms = e0.elapsed_time(e1) / reps
+            units = U * per_tree
+            waves = units / slots if kind == "tc" else math.ceil(units / slots)  # TC: stream-K spreads tiles evenly
+            grid[i, j] = ms / max(waves, 1e-9) if kind == "tc" else ms / waves
+            print(json.dumps({"n": n, "n_q": nq, "kernel": kind, "trees": U, "units": units, "slots": slots,
+                              "step_ms": ms, "unit_ms": grid[i, j]}), flush=True)
+            del step, k, v, q, out
+            torch.cuda.empty_cache()
+    return CostTable(NQ_KNOTS, N_KNOTS, grid,
+                     meta={"d": "128", "hardware": "b200", "source": "measured",
+                           "unit": f"one kv head of a subtask on one CTA slot (h_q {h_q}, h_kv {h_kv})"})
 
 
 if __name__ == "__main__":

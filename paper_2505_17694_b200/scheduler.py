@@ -137,10 +137,28 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
-MULTI_MAX_ROWS = 64  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
+MULTI_MAX_ROWS = 15  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
-SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into
+SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into (g = 4, d = 128)
+# Partial-output pricing: a slice writes one partial (o[d], m, l) per
+# query-head row and the merge reads it back, 2 * (4 d + 8) bytes per row;
+# plan_device keeps that below this fraction of the slice's KV bytes
+PARTIAL_FRACTION = 0.026
+
+
+def partial_bytes(rows: int, d: int = 128) -> int:
+    """HBM bytes one extra slice costs in partial outputs: written by the
+    split kernel, read by the merge (fp32 o[d] plus (m, l) per row)."""
+    return int(rows) * 2 * (4 * int(d) + 8)
+
+
+def min_slice_tokens(g: int, d: int = 128, elem: int = 2) -> int:
+    """Shortest slice whose partial bytes stay within PARTIAL_FRACTION of
+    its KV bytes (2 * d * elem per token per kv head), on 64-token steps:
+    320 for the Llama-3-8B shape (g = 4), 640 for g = 8."""
+    t = partial_bytes(g, d) / (PARTIAL_FRACTION * 2 * d * elem)
+    return max(64, -(-int(math.ceil(t)) // 64) * 64)
 SUFFIX_WAVES = 2        # suffix-grid CTA waves (of 6 CTAs per SM) plan_device aims for
 
 
@@ -204,11 +222,13 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     # GB/s (bytes in flight per CTA are bounded by its SMEM ring), so the
     # machine needs many CTAs: long slices are cut so the suffix grids hold
     # >= SUFFIX_WAVES waves of CTAs (6 per SM), never below
-    # SUFFIX_SLICE_MIN tokens (each slice adds a partial to merge) nor above
+    # min_slice_tokens (each slice adds a partial to write and merge:
+    # priced in HBM bytes, PARTIAL_FRACTION) nor above
     # SUFFIX_SLICE (a lightly shared 128K-token root in cfg4)
     work = sum(t.n for t in gv) * h_local
     target = max(1, sm_count * 6 * SUFFIX_WAVES)
-    slice_len = min(SUFFIX_SLICE, max(SUFFIX_SLICE_MIN, -(-work // target)))
+    slice_min = min_slice_tokens(g, forest.d)
+    slice_len = min(SUFFIX_SLICE, max(slice_min, -(-work // target)))
     slice_len = -(-slice_len // 64) * 64
     by_bk = {}
     for t in gv:

@@ -114,12 +114,10 @@ class TestCfg2BenchStep:
             dev = bench.path_reference(ns.forest, ns.kp, ns.vp, ns.q_dev, r).cpu().numpy()
             assert float(np.max(np.abs(dev - ref[i]))) <= 1e-10
 
-    def test_many_requests_vs_device_reference(self, cfg2_bench):
+    def test_all_requests_vs_device_reference(self, cfg2_bench):
         import bench
         ns = cfg2_bench
-        rng = np.random.default_rng(0)
-        reqs = sorted(set(rng.choice(256, 64, replace=False).tolist()) | {0, 1, 254, 255})
-        for r in reqs:
+        for r in range(256):  # every request, all 32 q heads
             ref = bench.path_reference(ns.forest, ns.kp, ns.vp, ns.q_dev, r)
             close(ns.out[r].double().cpu().numpy(), ref.cpu().numpy(), f"cfg2 request {r}")
 
