@@ -61,8 +61,8 @@ def measure_table(reps: int = 40, h_q: int = 32, h_kv: int = 8, d: int = 128) ->
     g = h_q // h_kv
     grid = np.zeros((len(N_KNOTS), len(NQ_KNOTS)))
     table = model_table()
-    slots_of = {"tc": sms // TC_CTAS_PER_BLOCK, "multi": sms * 3, "gemv": sms * 6}
-    skip = {"tc": 8 | 32 | 64, "multi": 8 | 16 | 64, "gemv": 8 | 16 | 64}
+    slots_of = {"tc": sms // TC_CTAS_PER_BLOCK, "multi": sms * 3, "suffix": sms * 6}
+    skip = {"tc": 8 | 32 | 64, "multi": 8 | 16 | 64, "suffix": 8 | 16 | 64}
     for i, n in enumerate(N_KNOTS):
         for j, nq in enumerate(NQ_KNOTS):
             kind = node_kernel(nq * g, nq, True)
@@ -92,14 +92,16 @@ def measure_table(reps: int = 40, h_q: int = 32, h_kv: int = 8, d: int = 128) ->
             ms = e0.elapsed_time(e1) / reps
             units = U * per_tree
             waves = units / slots if kind == "tc" else math.ceil(units / slots)  # TC: stream-K spreads tiles evenly
-            grid[i, j] = ms / max(waves, 1e-9) if kind == "tc" else ms / waves
+            # a kv head of the subtask = `lanes` units (256-row chunks) on the tensor cores
+            grid[i, j] = ms / waves * lanes
             print(json.dumps({"n": n, "n_q": nq, "kernel": kind, "trees": U, "units": units, "slots": slots,
                               "step_ms": ms, "unit_ms": grid[i, j]}), flush=True)
             del step, k, v, q, out
             torch.cuda.empty_cache()
     return CostTable(NQ_KNOTS, N_KNOTS, grid,
                      meta={"d": "128", "hardware": "b200", "source": "measured",
-                           "unit": f"one kv head of a subtask on one CTA slot (h_q {h_q}, h_kv {h_kv})"})
+                           "unit": f"one kv head of a subtask (all its 256-row tensor-core lanes) on one CTA slot, "
+                                   f"h_q {h_q} / h_kv {h_kv}, every slot busy, graph replay"})
 
 
 if __name__ == "__main__":
