@@ -37,7 +37,7 @@ constexpr int kTcMinRows = 16;
 // rows take it (in groups of kMultiRows rows), larger ones the tensor cores
 constexpr int kMultiRows = 32;
 #ifndef CODEC_MULTI_MAX_ROWS
-#define CODEC_MULTI_MAX_ROWS 15
+#define CODEC_MULTI_MAX_ROWS 16
 #endif
 constexpr int kMultiMaxRows = CODEC_MULTI_MAX_ROWS;
 // query-head rows of one tensor-core group (M = 256: one 128-row tile per

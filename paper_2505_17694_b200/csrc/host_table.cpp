@@ -47,6 +47,16 @@ struct codec_table {
 namespace {
 // Cost of a unit boundary inside a CTA pair, in KV tiles (device balancer
 // below). CODEC_TC_UNIT_COST overrides it (tuning).
+// Most query-head rows a slice may have to take the multi-request kernel
+// (CODEC_MULTI_MAX_ROWS overrides kMultiMaxRows; tuning, must match
+// scheduler.MULTI_MAX_ROWS)
+int64_t multi_max_rows() {
+  static const int64_t v = [] {
+    const char* e = getenv("CODEC_MULTI_MAX_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)codec::kMultiMaxRows;
+  }();
+  return v;
+}
 int64_t tc_unit_cost() {
   static const int64_t v = [] {
     const char* e = getenv("CODEC_TC_UNIT_COST");
@@ -198,7 +208,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   const bool multi_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & (CODEC_FLAG_NO_MULTI | CODEC_FLAG_GEMV_SIMT | CODEC_FLAG_NO_GEMV));
   const int32_t multi_reqs = std::max(1, kMultiRows / g);
-  const int64_t tc_min_rows = multi_ok ? kMultiMaxRows + 1 : kTcMinRows;
+  const int64_t tc_min_rows = multi_ok ? multi_max_rows() + 1 : kTcMinRows;
 
   // ---- rows and slots
   struct Grp {

@@ -137,7 +137,7 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
-MULTI_MAX_ROWS = 15  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
+MULTI_MAX_ROWS = 16  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
 SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into (g = 4, d = 128)

@@ -16,7 +16,7 @@ sequence is a prefix of lane 0's: pair k of every lane reads the same K/V
 tiles at the same time."""
 from __future__ import annotations
 
-MULTI_ROWS, MULTI_MAX_ROWS, TC_MIN_ROWS, TC_ROWS = 32, 15, 16, 256
+MULTI_ROWS, MULTI_MAX_ROWS, TC_MIN_ROWS, TC_ROWS = 32, 16, 16, 256
 
 
 def route(n_live: int, g: int, multi: bool = True, force_tc: bool = False) -> str:
