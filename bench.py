@@ -397,10 +397,19 @@ def main():
     import paper_2505_17694_b200 as P
     from paper_2505_17694_b200 import parallel as PL
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # CODEC_BENCH_ONE_GPU=1: every rank on cuda:0 with gloo for the control
+    # plane -- a single-GPU emulation of the multi-rank path (tests only;
+    # the fused gather's peer stores and counters work across processes
+    # sharing a GPU; the NCCL gather does not)
+    one_gpu = os.environ.get("CODEC_BENCH_ONE_GPU") == "1"
+    dev_index = 0 if one_gpu else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2505_17694_b200.executor import FLAG_MERGE_ALL
     fused = world > 1 and args.gather == "fused"
     flags = args.flags | (FLAG_MERGE_ALL if fused else 0)
@@ -462,6 +471,15 @@ def main():
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     stream = torch.cuda.current_stream(dev)
 
+    def all_done(local_done):
+        """Stop a timing loop on every rank together (each rank's wall
+        clock decides locally; the ranks' collectives must pair up)."""
+        if world == 1:
+            return local_done
+        f = torch.tensor([1 if local_done else 0], device=dev)
+        dist.all_reduce(f, op=dist.ReduceOp.MAX)
+        return bool(f.item())
+
     def timed(n, fn, min_seconds=0.0):
         """ms per call over n calls between barrier+sync on both sides, CUDA
         events on the launching stream, max over ranks. The n-call window
@@ -486,7 +504,7 @@ def main():
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             windows.append(ms)
-            if time.perf_counter() - t_start >= min_seconds or len(windows) >= 5000:
+            if all_done(time.perf_counter() - t_start >= min_seconds or len(windows) >= 5000):
                 break
         return statistics.median(windows), len(windows)
 
@@ -515,7 +533,7 @@ def main():
         ms_w, _ = timed(args.steps, lambda: step_ev(q_dev, kp, vp, out=out))
         ms_ev = ms_w
         kt_all.append(step_ev.kernel_times())
-        if time.perf_counter() - t_ev0 >= win_s:
+        if all_done(time.perf_counter() - t_ev0 >= win_s):
             break
     kt = np.concatenate(kt_all) if kt_all else np.zeros((0, 3))
     info = step.info
@@ -650,8 +668,10 @@ def main():
 
         e2e_window(3)
         wins, t0 = [], time.perf_counter()
-        while time.perf_counter() - t0 < win_s or not wins:
+        while True:
             wins.append(e2e_window(args.steps))
+            if all_done(time.perf_counter() - t0 >= win_s):
+                break
         e2e_ms = statistics.median(wins)
         e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "windows": len(wins),

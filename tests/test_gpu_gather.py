@@ -147,3 +147,31 @@ def test_fused_gather_two_ranks_one_gpu(partition):
         # the split points of the shared nodes (fp32 merge order)
         assert max(errs) <= 2e-5, (rank, errs)
         assert worst <= 2e-3, (rank, worst)
+
+
+def test_bench_two_ranks_one_gpu():
+    """bench.py's multi-rank path end to end (torchrun, 2 ranks, fused
+    gather) on one GPU: CODEC_BENCH_ONE_GPU=1 puts both ranks on cuda:0 with
+    gloo for the control plane. Timing is meaningless here (two contexts
+    time-slice the GPU); the line must verify and the gathered output must
+    hold every rank's rows."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, CODEC_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"), "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--config", "cfg1", "--no-cpu-baseline"]
+    res = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([l for l in res.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and "fused peer-store" in line["config"]["parallelism"]
+    v = line["verified"]
+    assert v["ok"] and v["gather_ok"] and v["all_ranks_ok"], v
