@@ -455,6 +455,18 @@ class TestGrow:
             f2 = forest(start + k)
             ref = DecodeStep(f2, P.plan_device(f2, 4, table, 8, 148), 32, "bfloat16", concurrent=False)(q, kp, vp)
             assert np.array_equal(np_(out), np_(ref)), k
+            # and the grown step against the float64 oracle on the same bf16
+            # values (root + each leaf's first start + k tokens)
+            up = lambda t: t.double().cpu().numpy()
+            kph, vph = up(kp), up(vp)
+            z = np.zeros((0, 8, 128))
+            nk = [z] + [kph[:, f2.token_offset[n]:f2.token_offset[n] + spec.length[n]].transpose(1, 0, 2)
+                        for n in range(1, len(spec.parent))]
+            nv = [z] + [vph[:, f2.token_offset[n]:f2.token_offset[n] + spec.length[n]].transpose(1, 0, 2)
+                        for n in range(1, len(spec.parent))]
+            vis = [None, None] + [{r: start + k} for r in range(bs)]
+            fd = OA.ForestData(spec.parent, nk, nv, spec.paths, vis)
+            assert_bf16_close(np_(out), OA.naive_attention(up(q), fd))
         with pytest.raises(ValueError, match="no room"):
             step.grow(cap)
 
