@@ -1059,7 +1059,7 @@ static long long* g_trace = nullptr;  // debug timeline (CODEC_FLAG_TRACE), one 
 // Q [bs][hq_local][128] bf16 viewed as [bs][hq_local][2 halves][64 d]: a box
 // of 64 d x 1 half x g heads x 128/g requests is one CTA's 128 Q rows of a
 // piece with consecutive requests, in the SW128 K-major layout the MMA reads
-static int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_local, int g) {
+int32_t encode_q_map(CUtensorMap* map, const void* q, int bs, int hq_local, int g) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult qr;

@@ -226,7 +226,7 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     # priced in HBM bytes, PARTIAL_FRACTION) nor above
     # SUFFIX_SLICE (a lightly shared 128K-token root in cfg4)
     work = sum(t.n for t in gv) * h_local
-    target = max(1, sm_count * 6 * SUFFIX_WAVES)
+    target = max(1, int(sm_count * 6 * SUFFIX_WAVES))
     slice_min = min_slice_tokens(g, forest.d)
     slice_len = min(SUFFIX_SLICE, max(slice_min, -(-work // target)))
     slice_len = -(-slice_len // 64) * 64

@@ -31,6 +31,12 @@ def suffix_alone(ns, n=20):
 if os.environ.get("MULTI_MAX_ROWS"):  # must match the library's -DCODEC_MULTI_MAX_ROWS
     from paper_2505_17694_b200 import scheduler
     scheduler.MULTI_MAX_ROWS = int(os.environ["MULTI_MAX_ROWS"])
+if os.environ.get("SUFFIX_WAVES"):
+    from paper_2505_17694_b200 import scheduler
+    scheduler.SUFFIX_WAVES = float(os.environ["SUFFIX_WAVES"])
+if os.environ.get("PARTIAL_FRACTION"):
+    from paper_2505_17694_b200 import scheduler
+    scheduler.PARTIAL_FRACTION = float(os.environ["PARTIAL_FRACTION"])
 if os.environ.get("SUFFIX_SLICE"):
     from paper_2505_17694_b200 import scheduler
     scheduler.SUFFIX_SLICE = int(os.environ["SUFFIX_SLICE"])
