@@ -274,7 +274,6 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_COUNTED_MERGE 1048576 /* partial producers count per merge entry and the merge starts each entry
                                             as soon as it is complete (opt-in: measured no faster on cfg2/cfg3) */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
-#define CODEC_FLAG_TC3 4194304 /* the three-softmax-group variant of the shared-node kernel (kern_tc3.cu) */
 #define CODEC_FLAG_MERGE_ALL 2097152 /* every (request, kv head) output goes through the merge kernel, single-partial
                                         ones too (no direct writes by the split kernels): what the fused peer-store
                                         output gather (codec_decode_attention_gather) needs */

@@ -17,10 +17,6 @@ int32_t launch_tc(const int32_t* table, const codec_table_info& in, const void* 
                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
                   cudaStream_t st, int flags, long long* ctalog, const int32_t* page_table, int page_shift,
                   int32_t* tc_done, const int32_t* entry_of, int32_t* cnt);
-int32_t launch_tc3(const int32_t* table, const codec_table_info& in, const void* q, const void* k, const void* v,
-                   int64_t pool_tokens, int g, int h_local, int bs, void* out, void* part_o, void* part_ml,
-                   cudaStream_t st, const int32_t* page_table, int page_shift, int32_t* tc_done,
-                   const int32_t* entry_of, int32_t* cnt);
 int32_t read_trace(long long* host, int64_t n);
 int32_t set_hang_buffer(void* dev_ptr);
 int32_t launch_gemv(int dtype, int d, int rows, const int32_t* table, int n_groups, int off_groups, int off_rows,
@@ -233,10 +229,7 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
   if ((done_target || counted) && cudaMemsetAsync(tc_done, 0, tail_bytes, st) != cudaSuccess)
     return fail(CODEC_ERR_CUDA, "tc counter reset");
   if (kev) CODEC_TRY(kev_record(timer, 0, st));
-  if (do_tc && (dims->flags & CODEC_FLAG_TC3))
-    CODEC_TRY(launch_tc3(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml,
-                         st, dims->page_table, page_shift, tc_done, entry_of, cnt));
-  else if (do_tc)
+  if (do_tc)
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
                         dims->flags, ctalog, dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (kev) CODEC_TRY(kev_record(timer, 1, st));
