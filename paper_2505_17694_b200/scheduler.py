@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -137,7 +138,10 @@ def device_tasks(forest, group_size: int, rows_per_tile: int = 256) -> list:
 
 
 TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core kernel (device_table.h)
-MULTI_MAX_ROWS = 16  # with the multi-request suffix kernel: slices up to this many rows take it (device_table.h)
+# with the multi-request suffix kernel: slices up to this many rows take it
+# (device_table.h kMultiMaxRows; the library and this module read the same
+# CODEC_MULTI_MAX_ROWS override)
+MULTI_MAX_ROWS = int(os.environ.get("CODEC_MULTI_MAX_ROWS", "16"))
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
 SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into (g = 4, d = 128)

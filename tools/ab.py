@@ -28,9 +28,7 @@ def suffix_alone(ns, n=20):
     return e0.elapsed_time(e1) / n
 
 
-if os.environ.get("MULTI_MAX_ROWS"):  # must match the library's -DCODEC_MULTI_MAX_ROWS
-    from paper_2505_17694_b200 import scheduler
-    scheduler.MULTI_MAX_ROWS = int(os.environ["MULTI_MAX_ROWS"])
+# (CODEC_MULTI_MAX_ROWS is read by both the library and scheduler.py)
 if os.environ.get("SUFFIX_WAVES"):
     from paper_2505_17694_b200 import scheduler
     scheduler.SUFFIX_WAVES = float(os.environ["SUFFIX_WAVES"])

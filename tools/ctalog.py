@@ -84,7 +84,11 @@ for x in range(2 * info.n_tc_blocks):
 rows = []
 for b in range(info.n_tc_blocks):
     if b in dur:
-        rows.append((max(dur[b]), tiles[b], int(units[b]), int(tcl[2 * b, 0])))
+        rows.append((max(dur[b]), tiles[b], int(units[b]), int(tcl[2 * b, 0]), b))
+if os.environ.get("CTALOG_ALL"):
+    for r in sorted(rows, key=lambda x: x[4]):
+        print("  pair %d: %.1f us, %d tiles, %d units" % (r[4], r[0], r[1], r[2]))
+rows = [r[:4] for r in rows]
 rows.sort()
 print("pair duration us / tiles / units / smid (fastest 8, slowest 8):")
 for r in rows[:8] + rows[-8:]:
