@@ -224,7 +224,7 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["label"], "sample": r.desc},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": r.workers, "kind": r.kind, "sample": r.desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -733,7 +733,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "timed_windows": windows, "us_per_step": ms * 1e3,
             "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",  # the config's workload, split over N GPUs
             "data": "synthetic: N(0,1)/sqrt(d) K/V/Q generated on device (seeded), no checkpoint",
             "config": {"workload": ns.cfg["label"], "bs": full_bs, "h_q": h_q, "h_kv": ns.cfg["h_kv"], "d": d,
                        "kv_tokens": int(sum(ns.spec.length[1:])), "nodes": int(ns.spec.n_nodes - 1),

@@ -124,14 +124,13 @@ def _worker(rank, world, port, partition, q):
         q.put((rank, None, None, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("partition", ["heads", "trees"])
-def test_fused_gather_two_ranks_one_gpu(partition):
+@pytest.mark.parametrize("partition,world", [("heads", 2), ("trees", 2), ("heads", 4)])
+def test_fused_gather_ranks_one_gpu(partition, world):
     import torch
     import torch.multiprocessing as mp
 
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
