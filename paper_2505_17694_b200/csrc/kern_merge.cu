@@ -107,7 +107,7 @@ __device__ __forceinline__ void merge128_row(const int32_t* __restrict__ table, 
                                              const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                              float* __restrict__ out, const PeerDev& pg);
 
-constexpr int kFastNp = 8;  // partials per entry merged with all their loads in flight at once
+constexpr int kFastNp = 16;  // partials per entry merged with all their loads in flight at once (cfg3: 6-17)
 
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
