@@ -836,6 +836,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       // The l / m barrier alternates with the unit parity so one epilogue
       // never joins the next.
       const int tl = t - 1, last = tl & 1, l_bar = 9 + (n & 1);
+#ifdef CODEC_TC_EPI_TIMING
+      const long long epi_t0 = clock64();
+#endif
       if (quad == 0) PROG(1 + grp, t, 7);
       if (grp != last) {
         // lx is single-buffered: the previous unit's epilogue group must
@@ -863,6 +866,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(&bars->o_free, 0);
         if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(15, tl);
+#ifdef CODEC_TC_EPI_TIMING
+        const long long epi_t1 = clock64();
+#endif
         // Write O through this unit's Q buffer (its S MMAs are complete) as a
         // staging area, 64 rows per pass: thread-per-row global stores touch
         // 32 lines per instruction; from SMEM each row goes out as one fully
@@ -925,6 +931,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars->epi_done[n & 1]);
+#ifdef CODEC_TC_EPI_TIMING
+          if (ctalog && tid == grp * 128) {  // epilogue clocks of this CTA: until O read / after
+            ctalog[4 * (2048 + blockIdx.x) + 1] += epi_t1 - epi_t0;
+            ctalog[4 * (2048 + blockIdx.x) + 2] += clock64() - epi_t1;
+          }
+#endif
           if (tid == grp * 128 + 32 * CODEC_TC_TRACE_QUAD) stamp(9, tl);
         }
       }
