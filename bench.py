@@ -282,26 +282,41 @@ def prepare(config="cfg2", dev=None, rank=0, world=1, partition=None, flags=0, s
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     out = torch.empty((bs, hq_local, d), dtype=torch.float32, device=dev)
 
-    def make(budget):
+    def make(cand):
+        budget, fl = cand
         t0 = time.perf_counter()
         if blocks:
             pl = P.divide_and_schedule(P.device_tasks(forest, g), table, blocks)
         else:
-            pl = P.plan_device(forest, g, table, h_local, sms, budget, multi=not (flags & 524288))  # FLAG_NO_MULTI
+            pl = P.plan_device(forest, g, table, h_local, sms, budget, multi=not (fl & 524288),  # FLAG_NO_MULTI
+                               tct=not (fl & 4194304))  # FLAG_NO_TCT
         ms_plan = (time.perf_counter() - t0) * 1e3
         st = DecodeStep(forest, pl, h_q, "bfloat16", head_begin=h0, head_end=h0 + h_local, device=dev,
-                        flags=flags, tc_sm_budget=budget, concurrent=not serial)
+                        flags=fl, tc_sm_budget=budget, concurrent=not serial)
         return pl, st, ms_plan
 
     # TC SM budget: the SMs the TC grid leaves free run the suffix kernel
-    # from the start (programmatic dependent launch); tuned once per plan
+    # from the start (programmatic dependent launch); tuned once per plan,
+    # together with the routing of lightly shared nodes (17..128 rows): the
+    # transposed tensor-core kernel takes them off the pair kernel's SMs
+    # (a gain when the step is tensor-bound, cfg4) but adds to the HBM-bound
+    # side (a loss when that is the long pole, cfg3)
     if budgets is None:
-        budgets = [sms] if (serial or quick) else [sms] + list(range(136, 63, -8))
+        budgets = [sms] if (serial or quick) else [sms] + list(range(136, 55, -8))
+    routings = [flags]
+    if not (flags & 4194304) and not blocks and not quick and len(budgets) > 1:
+        has = torch.tensor([int(make((budgets[0], flags))[1].info.n_tct_groups > 0)], device=dev)
+        if world > 1:  # every rank tunes the same candidates
+            dist.all_reduce(has, op=dist.ReduceOp.MAX)
+        if int(has.item()):
+            routings.append(flags | 4194304)
     tune_ms, best = {}, None
-    queue, refined = list(budgets), len(budgets) < 2
+    queue = [(b, fl) for fl in routings for b in budgets]
+    refined = len(budgets) < 2
     while queue:
-        b = queue.pop(0)
-        pl, st, ms_plan = make(b)
+        cand = queue.pop(0)
+        b = cand[0]
+        pl, st, ms_plan = make(cand)
         for _ in range(3):
             st(q_dev, kp, vp, out=out)
         torch.cuda.synchronize(dev)
@@ -316,18 +331,19 @@ def prepare(config="cfg2", dev=None, rank=0, world=1, partition=None, flags=0, s
             tt = torch.tensor([t_b], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_b = float(tt.item())
-        tune_ms[b] = round(t_b, 4)
+        tune_ms[f"{b}{'' if cand[1] & 4194304 == flags & 4194304 else '/notct'}"] = round(t_b, 4)
         if best is None or t_b < best[0]:
-            best = (t_b, b, pl, st, ms_plan)
+            best = (t_b, cand, pl, st, ms_plan)
         if not queue and not refined:  # a finer pass (+-4 SMs) around the coarse optimum
             refined = True
-            queue = [x for x in (best[1] - 4, best[1] + 4) if 16 <= x < sms and x not in tune_ms]
-    _, budget, plan, step, plan_ms = best
+            b0, f0 = best[1]
+            queue = [(x, f0) for x in (b0 - 4, b0 + 4) if 16 <= x < sms and x not in budgets]
+    _, (budget, flags), plan, step, plan_ms = best
     return SimpleNamespace(cfg=cfg, config=config, dev=dev, rank=rank, world=world, partition=partition,
                            spec=spec, full=full, forest=forest, shard=shard, shards=shards, h0=h0,
                            h_local=h_local, hq_local=hq_local, g=g, kp=kp, vp=vp, q_host=q_host, q_dev=q_dev,
                            out=out, sms=sms, plan=plan, budget=budget, step=step, plan_ms=plan_ms,
-                           tune_ms=tune_ms, table=table, blocks=blocks)
+                           tune_ms=tune_ms, table=table, blocks=blocks, flags=flags)
 
 
 def path_reference(forest, kp, vp, q, r):
@@ -551,7 +567,8 @@ def main():
     g = ns.g
     from paper_2505_17694_b200.scheduler import node_kernel
     on_tc = [n for n in ns.forest.nodes[1:] if n.query_set and
-             node_kernel(len(n.query_set) * g, len(n.query_set), not (args.flags & 524288)) == "tc"]
+             node_kernel(len(n.query_set) * g, len(n.query_set), not (ns.flags & 524288),
+                         not (ns.flags & 4194304)) == "tc"]
     kv_tc = sum(n.len for n in on_tc) * ns.h_local * d * 2 * 2
     kernels = {}
     if "tc" in phases:
@@ -747,6 +764,8 @@ def main():
                        "launch": "CUDA graph replay of the step" if replay is not None else "direct launches",
                        "suffix_kernel": "mma.sync, early launch on the SMs the TC grid leaves (PDL)",
                        "tc_sm_budget": step.tc_sm_budget, "tc_ctas": step.info.n_tc_blocks * 2,
+                       "lightly_shared": ("transposed tensor-core kernel (%d CTAs)" % (step.info.n_tct_groups * ns.h_local)
+                                          if step.info.n_tct_groups else "pair kernel / mma.sync kernels"),
                        "autotune_ms": ns.tune_ms},
             "roofline": roof,
             "hbm_roofline_step": {"achieved": value / world, "peak": hbm, "unit": "GB/s",

@@ -274,6 +274,8 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_COUNTED_MERGE 1048576 /* partial producers count per merge entry and the merge starts each entry
                                             as soon as it is complete (opt-in: measured no faster on cfg2/cfg3) */
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
+#define CODEC_FLAG_NO_TCT 4194304 /* lightly shared slices above the multi-request range on the M = 256 pair kernel
+                                      instead of the transposed tensor-core kernel */
 #define CODEC_FLAG_MERGE_ALL 2097152 /* every (request, kv head) output goes through the merge kernel, single-partial
                                         ones too (no direct writes by the split kernels): what the fused peer-store
                                         output gather (codec_decode_attention_gather) needs */
@@ -300,7 +302,9 @@ typedef struct {
   int32_t n_multi_groups, off_multi;                   /* lightly shared slices (2..32/g requests) on the
                                                           multi-request mma.sync kernel */
   int32_t off_entry_of;                                /* [bs][h_local] merge entry of (request, kv head), -1 none */
-  int32_t reserved1;
+  int32_t n_tct_groups;                                /* slices of nodes with 17..64 query-head rows (kTctMaxRows)
+                                                          on the transposed tensor-core kernel: records right
+                                                          after the multi-request ones (off_multi + 8 n_multi_groups) */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

@@ -11,6 +11,7 @@ constexpr int kKindTc = 0;       // tcgen05 shared-node kernel (bf16, d = 128)
 constexpr int kKindGemv = 1;     // CUDA-core warp-shuffle GEMV kernel
 constexpr int kKindGeneric = 2;  // any dtype / head dim (small or odd shapes)
 constexpr int kKindMulti = 3;    // multi-request mma.sync kernel: 2..kMultiRows/g requests of one slice
+constexpr int kKindTct = 4;      // transposed tcgen05 kernel (kern_tct.cu): up to kTctRows rows of one slice
 
 // a group record: 8 int32
 constexpr int kGroupInts = 8;
@@ -40,6 +41,14 @@ constexpr int kMultiRows = 32;
 #define CODEC_MULTI_MAX_ROWS 16
 #endif
 constexpr int kMultiMaxRows = CODEC_MULTI_MAX_ROWS;
+// transposed tensor-core kernel: slices of kMultiMaxRows + 1 .. kTctMaxRows
+// query-head rows (CODEC_TCT_MAX_ROWS overrides), in groups of at most
+// kTctRows rows (the MMA's N); larger slices take the M = 256 pair kernel
+constexpr int kTctRows = 64;
+#ifndef CODEC_TCT_MAX_ROWS
+#define CODEC_TCT_MAX_ROWS 64
+#endif
+constexpr int kTctMaxRows = CODEC_TCT_MAX_ROWS;
 // query-head rows of one tensor-core group (M = 256: one 128-row tile per
 // CTA of a cta_group::2 pair)
 constexpr int kTcGroupRows = 256;

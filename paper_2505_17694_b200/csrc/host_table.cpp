@@ -45,8 +45,6 @@ struct codec_table {
 };
 
 namespace {
-// Cost of a unit boundary inside a CTA pair, in KV tiles (device balancer
-// below). CODEC_TC_UNIT_COST overrides it (tuning).
 // Most query-head rows a slice may have to take the multi-request kernel
 // (CODEC_MULTI_MAX_ROWS overrides kMultiMaxRows; tuning, must match
 // scheduler.MULTI_MAX_ROWS)
@@ -57,6 +55,17 @@ int64_t multi_max_rows() {
   }();
   return v;
 }
+// ... and the transposed tensor-core kernel (CODEC_TCT_MAX_ROWS overrides
+// kTctMaxRows; must match scheduler.TCT_MAX_ROWS)
+int64_t tct_max_rows() {
+  static const int64_t v = [] {
+    const char* e = getenv("CODEC_TCT_MAX_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)codec::kTctMaxRows;
+  }();
+  return v;
+}
+// Cost of a unit boundary inside a CTA pair, in KV tiles (device balancer
+// below). CODEC_TC_UNIT_COST overrides it (tuning).
 int64_t tc_unit_cost() {
   static const int64_t v = [] {
     const char* e = getenv("CODEC_TC_UNIT_COST");
@@ -208,7 +217,14 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   const bool multi_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & (CODEC_FLAG_NO_MULTI | CODEC_FLAG_GEMV_SIMT | CODEC_FLAG_NO_GEMV));
   const int32_t multi_reqs = std::max(1, kMultiRows / g);
+  // slices above the multi-request range of nodes with at most
+  // tct_max_rows() query-head rows in all: the transposed tensor-core kernel
+  // (work proportional to the rows), in groups of kTctRows rows. (A larger
+  // node's last row chunk stays on the pair kernel, in lockstep with the
+  // node's other chunks: one HBM read of its KV.)
+  const bool tct_ok = tc_ok && g <= kTctRows && !(dims->flags & (CODEC_FLAG_NO_TCT | CODEC_FLAG_FORCE_TC));
   const int64_t tc_min_rows = multi_ok ? multi_max_rows() + 1 : kTcMinRows;
+  const int32_t tct_reqs = std::max(1, kTctRows / g);
 
   // ---- rows and slots
   struct Grp {
@@ -238,7 +254,11 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     if (live.empty()) continue;
     int kind;
     int32_t per;
-    if (tc_ok && ((int64_t)live.size() * g >= tc_min_rows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
+    const int64_t rows_live = (int64_t)live.size() * g, rows_node = (qptr[n + 1] - qptr[n]) * (int64_t)g;
+    if (tct_ok && rows_live >= tc_min_rows && rows_node <= tct_max_rows()) {
+      kind = kKindTct;
+      per = tct_reqs;
+    } else if (tc_ok && (rows_live >= tc_min_rows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
       kind = kKindTc;
       per = tc_reqs;
     } else if (multi_ok && live.size() >= 2) {
@@ -253,9 +273,10 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     }
     // paged pool: every TMA box (128-token K/V tiles, 32-token suffix
     // chunks) must sit inside one page
-    if (page && start % (kind == kKindTc ? 128 : 32) != 0)
+    const int64_t box = (kind == kKindTc || kind == kKindTct) ? 128 : 32;
+    if (page && start % box != 0)
       return fail(CODEC_ERR_UNSUPPORTED, "paged KV: node %lld slice starts at token %lld, not a multiple of %d",
-                  (long long)n, (long long)start, kind == kKindTc ? 128 : 32);
+                  (long long)n, (long long)start, (int)box);
     for (size_t a = 0; a < live.size(); a += per) {
       size_t b = std::min(live.size(), a + per);
       int32_t max_vis = 0;
@@ -592,6 +613,8 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
   emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
   emit_groups(kKindMulti, in.n_multi_groups, in.off_multi);
+  int32_t off_tct = 0;  // right after the multi-request records
+  emit_groups(kKindTct, in.n_tct_groups, off_tct);
   in.off_rows = (int32_t)blob.size();
   in.n_rows = (int32_t)(rows.size() / 4);
   blob.insert(blob.end(), rows.begin(), rows.end());

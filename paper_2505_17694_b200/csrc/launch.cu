@@ -31,6 +31,10 @@ int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int
                          const void* k, const void* v, int64_t pool_tokens, int g, int h_local, void* out,
                          void* part_o, void* part_ml, cudaStream_t st, bool pdl, const int32_t* page_table,
                          int page_shift, int32_t* done, const int32_t* entry_of, int32_t* cnt);
+int32_t launch_tct(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q, const void* k,
+                   const void* v, int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
+                   cudaStream_t st, bool pdl, const int32_t* page_table, int page_shift, int32_t* done,
+                   const int32_t* entry_of, int32_t* cnt);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -162,7 +166,8 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
   const bool do_gemv = info->n_gemv_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
   const bool do_gen = info->n_gen_groups && !(dims->flags & CODEC_FLAG_SKIP_GENERIC);
   const bool do_multi = info->n_multi_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
-  if ((do_tc || do_multi) && (dims->kv_dtype != CODEC_BF16 || d != 128 || g > 128))
+  const bool do_tct = info->n_tct_groups && !(dims->flags & CODEC_FLAG_SKIP_GEMV);
+  if ((do_tc || do_multi || do_tct) && (dims->kv_dtype != CODEC_BF16 || d != 128 || g > 128))
     return fail(CODEC_ERR_UNSUPPORTED, "tensor-core / multi-request groups need bf16, d = 128");
   if (do_multi && g > 8) return fail(CODEC_ERR_UNSUPPORTED, "multi-request groups need <= 8 query heads per kv head");
   // The mma.sync suffix kernel is launched right after the TC kernel on the
@@ -207,11 +212,12 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
   int64_t ml_bytes = (int64_t)info->n_slots * hq_local * 2 * elem;
   ml_bytes = (ml_bytes + 255) / 256 * 256;
   int32_t* tc_done = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(workspace) + o_bytes + ml_bytes);
-  const int done_target = (do_tc ? 2 * info->n_tc_blocks : 0) + (do_multi ? info->n_multi_groups * h_local : 0);
+  const int done_target = (do_tc ? 2 * info->n_tc_blocks : 0) + (do_multi ? info->n_multi_groups * h_local : 0) +
+                          (do_tct ? info->n_tct_groups * h_local : 0);
   // early (programmatic) launches of the kernels after the TC kernel; not
   // with the fused merge, which reads the TC partials from the suffix kernel
   const bool early = info->n_merge_fused == 0 && !kev;
-  const bool pdl = mma_gemv && (do_tc || do_multi) && early;
+  const bool pdl = mma_gemv && (do_tc || do_multi || do_tct) && early;
   // Counted merge (opt-in): every partial producer (TC epilogue rows, mma.sync
   // suffix / multi CTAs) bumps its merge entry's counter after its stores,
   // and each merge CTA starts as soon as its entry is complete -- the merge
@@ -233,9 +239,15 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
     CODEC_TRY(launch_tc(table_dev, *info, q, k, v, dims->pool_tokens, g, h_local, dims->bs, out, part_o, part_ml, st,
                         dims->flags, ctalog, dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (kev) CODEC_TRY(kev_record(timer, 1, st));
+  // the transposed tensor-core kernel first: its CTAs are the longest of the
+  // SMs the TC grid leaves (one per SM), the mma.sync grids fill in after
+  if (do_tct)
+    CODEC_TRY(launch_tct(table_dev, info->n_tct_groups, info->off_multi + kGroupInts * info->n_multi_groups,
+                         info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
+                         do_tc && early, dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (do_multi)
     CODEC_TRY(launch_mma_multi(table_dev, info->n_multi_groups, info->off_multi, info->off_rows, q, k, v,
-                               dims->pool_tokens, g, h_local, out, part_o, part_ml, st, do_tc && early,
+                               dims->pool_tokens, g, h_local, out, part_o, part_ml, st, (do_tc || do_tct) && early,
                                dims->page_table, page_shift, tc_done, entry_of, cnt));
   if (mma_gemv)
     CODEC_TRY(launch_mma_gemv(table_dev, info->n_gemv_groups, info->off_gemv, info->off_rows, q, k, v,
@@ -256,7 +268,7 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
   if (!(dims->flags & CODEC_FLAG_SKIP_MERGE))
     CODEC_TRY(launch_merge(dims->kv_dtype, table_dev, *info, d, hq_local, part_o, part_ml, out, st,
                            done_target ? tc_done : nullptr, done_target,
-                           (mma_gemv || do_multi || counted) && !fork && !kev &&
+                           (mma_gemv || do_multi || do_tct || counted) && !fork && !kev &&
                                !(dims->flags & CODEC_FLAG_SKIP_GEMV) && !(dims->flags & CODEC_FLAG_MERGE_NO_PDL),
                            cnt, gather));
   if (kev) {

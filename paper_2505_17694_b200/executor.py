@@ -36,6 +36,7 @@ FLAG_NO_TC = 1
 FLAG_FORCE_TC = 2
 FLAG_NO_GEMV = 4
 FLAG_NO_MULTI = 524288
+FLAG_NO_TCT = 4194304  # no transposed tensor-core kernel (its slices on the pair kernel)
 FLAG_MERGE_ALL = 2097152  # every output row through the merge kernel (the fused peer-store gather needs it)
 
 
@@ -182,7 +183,7 @@ class DecodeStep:
         """Kernels one call launches (for the bench's gpu_launches)."""
         i = self.info
         return (int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) +
-                int(bool(i.n_multi_groups)) + int(bool(i.n_merge)))
+                int(bool(i.n_multi_groups)) + int(bool(i.n_tct_groups)) + int(bool(i.n_merge)))
 
     def __call__(self, q, k_pool, v_pool, out=None, stream=None):
         """q [bs, h_q_local, d] and the pools [h_local, pool_tokens, d] in
@@ -289,7 +290,8 @@ class DecodeStep:
         leaf = {n.id for n in self.forest.nodes[1:] if not self.forest.children[n.id]}
         touched, grown = [], {}
         for off, count in ((i.off_gemv, i.n_gemv_groups), (i.off_gen, i.n_gen_groups),
-                           (i.off_multi, i.n_multi_groups)):
+                           (i.off_multi, i.n_multi_groups),
+                           (i.off_multi + 8 * i.n_multi_groups, i.n_tct_groups)):
             for gidx in range(count):
                 rec = off + 8 * gidx
                 node = int(blob[rec + 5])

@@ -142,6 +142,11 @@ TC_MIN_ROWS = 16  # query-head rows from which a subtask takes the tensor-core k
 # (device_table.h kMultiMaxRows; the library and this module read the same
 # CODEC_MULTI_MAX_ROWS override)
 MULTI_MAX_ROWS = int(os.environ.get("CODEC_MULTI_MAX_ROWS", "16"))
+# transposed tensor-core kernel (kern_tct.cu): nodes with at most this many
+# query-head rows in all (device_table.h kTctMaxRows; the library reads the
+# same CODEC_TCT_MAX_ROWS override), cut into slices of TCT_SLICE tokens
+TCT_MAX_ROWS = int(os.environ.get("CODEC_TCT_MAX_ROWS", "64"))
+TCT_SLICE = int(os.environ.get("CODEC_TCT_SLICE", "4096"))
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
 SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly shared node into (g = 4, d = 128)
@@ -185,12 +190,17 @@ def concat_plans(plans) -> DivisionPlan:
                         cost_l_ms=plans[0].cost_l_ms, search_truncated=any(p.search_truncated for p in plans))
 
 
-def node_kernel(rows: int, n_requests: int, multi: bool = True) -> str:
+def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True, node_rows: int | None = None) -> str:
     """Which kernel runs a slice with `rows` query-head rows of
-    `n_requests` requests (host_table.cpp's routing for bf16, d = 128,
-    g <= 8): "tc" (tcgen05 shared-node kernel), "multi" (multi-request
-    mma.sync kernel) or "suffix" (single-request mma.sync kernel)."""
-    if rows > (MULTI_MAX_ROWS if multi else TC_MIN_ROWS - 1):
+    `n_requests` requests of a node with `node_rows` rows in all (default:
+    rows) -- host_table.cpp's routing for bf16, d = 128, g <= 8: "tct"
+    (transposed tcgen05 kernel), "tc" (tcgen05 shared-node kernel),
+    "multi" (multi-request mma.sync kernel) or "suffix" (single-request
+    mma.sync kernel)."""
+    lo = MULTI_MAX_ROWS if multi else TC_MIN_ROWS - 1
+    if tct and rows > lo and (rows if node_rows is None else node_rows) <= TCT_MAX_ROWS:
+        return "tct"
+    if rows > lo:
         return "tc"
     if multi and n_requests >= 2:
         return "multi"
@@ -199,7 +209,7 @@ def node_kernel(rows: int, n_requests: int, multi: bool = True) -> str:
 
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
                 tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT, page_size: int = 0,
-                multi: bool = True) -> DivisionPlan:
+                multi: bool = True, tct: bool = True) -> DivisionPlan:
     """The B200 plan of one decode step. Shared nodes (more than
     MULTI_MAX_ROWS query-head rows per chunk; TC_MIN_ROWS with multi=False)
     stay whole here: on the tensor cores every KV tile costs the same (an
@@ -216,12 +226,21 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     whole: a slice must start on a 32-token chunk boundary of its node."""
     tasks = device_tasks(forest, group_size)
     g = int(group_size)
-    tc = [t for t in tasks if node_kernel(t.n_q, t.n_q // g, multi) == "tc"]
-    gv = [t for t in tasks if node_kernel(t.n_q, t.n_q // g, multi) != "tc"]
+    kind = [node_kernel(t.n_q, t.n_q // g, multi, tct, len(forest.node(t.node).query_set) * g) for t in tasks]
+    tc = [t for t, k in zip(tasks, kind) if k == "tc"]
+    tcts = [t for t, k in zip(tasks, kind) if k == "tct"]
+    gv = [t for t, k in zip(tasks, kind) if k not in ("tc", "tct")]
     pairs = max(1, (tc_sm_budget or sm_count) // TC_CTAS_PER_BLOCK)
     plans = []
     if tc:
         plans.append(plan_uniform_bk(tc, table, pairs, 1))
+    # transposed tensor-core kernel: one CTA per slice and kv head, slices
+    # of <= TCT_SLICE tokens (a paged pool keeps nodes whole, like below)
+    by_bk = {}
+    for t in tcts:
+        by_bk.setdefault(1 if page_size else max(1, -(-t.n // TCT_SLICE)), []).append(t)
+    for bk in sorted(by_bk):
+        plans.append(plan_uniform_bk(by_bk[bk], table, len(by_bk[bk]) * bk, bk))
     # mma.sync-kernel tasks: one CTA streams a slice at only a few tens of
     # GB/s (bytes in flight per CTA are bounded by its SMEM ring), so the
     # machine needs many CTAs: long slices are cut so the suffix grids hold

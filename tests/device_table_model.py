@@ -17,18 +17,23 @@ tiles at the same time."""
 from __future__ import annotations
 
 MULTI_ROWS, MULTI_MAX_ROWS, TC_MIN_ROWS, TC_ROWS = 32, 16, 16, 256
+TCT_ROWS, TCT_MAX_ROWS = 64, 64
 
 
-def route(n_live: int, g: int, multi: bool = True, force_tc: bool = False) -> str:
+def route(n_live: int, g: int, multi: bool = True, force_tc: bool = False, node_rows: int = 0,
+          tct: bool = True) -> str:
     rows = n_live * g
-    if force_tc or rows >= (MULTI_MAX_ROWS + 1 if multi else TC_MIN_ROWS):
+    lo = MULTI_MAX_ROWS + 1 if multi else TC_MIN_ROWS
+    if tct and not force_tc and rows >= lo and node_rows <= TCT_MAX_ROWS:
+        return "tct"
+    if force_tc or rows >= lo:
         return "tc"
     if multi and n_live >= 2:
         return "multi"
     return "gemv"
 
 
-def groups_of(forest, plan, g, multi=True, force_tc=False):
+def groups_of(forest, plan, g, multi=True, force_tc=False, tct=True):
     """[(kind, kv_tok, len, [(req, vis_local)], order)] in plan order, like
     the table builder (query-set chunks per task, rows with visible > start)."""
     qsets = {}
@@ -50,19 +55,20 @@ def groups_of(forest, plan, g, multi=True, force_tc=False):
                 if forest.visible_count(st.node, r) > st.start]
         if not live:
             continue
-        kind = route(len(live), g, multi, force_tc)
-        per = {"tc": max(1, TC_ROWS // g), "multi": max(1, MULTI_ROWS // g), "gemv": 1}[kind]
+        kind = route(len(live), g, multi, force_tc, len(forest.node(st.node).query_set) * g, tct)
+        per = {"tc": max(1, TC_ROWS // g), "tct": max(1, TCT_ROWS // g), "multi": max(1, MULTI_ROWS // g),
+               "gemv": 1}[kind]
         for a in range(0, len(live), per):
             out.append((kind, forest.token_offset[st.node] + st.start, st.stop - st.start, live[a:a + per],
                         len(out)))
     return out
 
 
-def tc_pieces(forest, plan, g, h_local, sms=148, budget=0, multi=True, force_tc=False):
+def tc_pieces(forest, plan, g, h_local, sms=148, budget=0, multi=True, force_tc=False, tct=True):
     """The TC piece records (kv_tok, len, n_rows, max_vis, qreq0, pair,
     head) in the table's order (pairs ascending), and the pair count."""
-    groups = groups_of(forest, plan, g, multi, force_tc)
-    order = {"tc": 0, "gemv": 1, "multi": 3}
+    groups = groups_of(forest, plan, g, multi, force_tc, tct)
+    order = {"tc": 0, "gemv": 1, "multi": 3, "tct": 4}
     # kind, then longest slices first (stable)
     groups = sorted(groups, key=lambda x: (order[x[0]], -x[2]))
     tcg = [x for x in groups if x[0] == "tc"]

@@ -10,7 +10,7 @@ import pytest
 
 import paper_2505_17694_b200 as P
 from paper_2505_17694_b200 import workloads as W
-from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_MULTI, make_dims, table_for
+from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_MULTI, FLAG_NO_TCT, make_dims, table_for
 
 from device_table_model import groups_of, tc_pieces
 
@@ -39,17 +39,18 @@ FORESTS = list(_forests())
 @pytest.mark.parametrize("name,spec", FORESTS, ids=[n for n, _ in FORESTS])
 @pytest.mark.parametrize("budget", [0, 96, 40])
 @pytest.mark.parametrize("heads", [(0, 8), (2, 4)])
-@pytest.mark.parametrize("flags", [0, FLAG_NO_MULTI, FLAG_FORCE_TC])
+@pytest.mark.parametrize("flags", [0, FLAG_NO_MULTI, FLAG_FORCE_TC, FLAG_NO_TCT])
 def test_pieces_match_model(name, spec, budget, heads, flags):
     f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, spec.h_kv, spec.d)
     g = spec.h_q // spec.h_kv
     h0, h1 = heads
-    multi = not (flags & FLAG_NO_MULTI)
-    plan = P.plan_device(f, g, P.load_default_profile(), h1 - h0, 148, budget, multi=multi)
+    multi, tct = not (flags & FLAG_NO_MULTI), not (flags & FLAG_NO_TCT)
+    plan = P.plan_device(f, g, P.load_default_profile(), h1 - h0, 148, budget, multi=multi, tct=tct)
     info, blob = table_for(f, plan, make_dims(f, spec.h_q, "bfloat16", h0, h1, flags, 148, budget))
     recs = blob[info.off_tc:info.off_tc + 8 * info.n_tc_groups].reshape(-1, 8)
     got = [(int(r[0]), int(r[1]), int(r[3]), int(r[4]), int(r[5]), int(r[6]), int(r[7])) for r in recs]
-    want, n_pairs = tc_pieces(f, plan, g, h1 - h0, 148, budget, multi=multi, force_tc=bool(flags & FLAG_FORCE_TC))
+    want, n_pairs = tc_pieces(f, plan, g, h1 - h0, 148, budget, multi=multi, force_tc=bool(flags & FLAG_FORCE_TC),
+                              tct=tct)
     assert got == want
     assert info.n_tc_blocks == (n_pairs if want else 0)
     # per-pair unit CSR covers the pieces in order
@@ -65,6 +66,7 @@ def test_pieces_match_model(name, spec, budget, heads, flags):
         total = sum(tiles.values())
         assert max(tiles.values()) <= -(-total // len(tiles)) * 2 + 1
     # routing: the other kinds' group counts
-    kinds = [x[0] for x in groups_of(f, plan, g, multi, bool(flags & FLAG_FORCE_TC))]
+    kinds = [x[0] for x in groups_of(f, plan, g, multi, bool(flags & FLAG_FORCE_TC), tct)]
     assert info.n_multi_groups == kinds.count("multi")
+    assert info.n_tct_groups == kinds.count("tct")
     assert info.n_gemv_groups == kinds.count("gemv")

@@ -100,7 +100,7 @@ class TestCfg2BenchStep:
         ns = cfg2_bench
         assert ns.forest.bs == 256 and ns.forest.total_tokens == 32768 + 256 * 512
         assert ns.step.info.n_tc_groups > 0 and ns.step.info.n_gemv_groups == 256 and ns.step.info.n_merge > 0
-        assert ns.step.aux is not None and ns.budget in ns.tune_ms
+        assert ns.step.aux is not None and (str(ns.budget) in ns.tune_ms or f"{ns.budget}/notct" in ns.tune_ms)
 
     def test_sampled_requests_vs_oracle(self, cfg2_bench):
         import bench
@@ -223,15 +223,16 @@ class TestShardedSteps:
 
 
 # ------------------------------------------------------------ score extremes
-def _extreme_spec(seed, mode):
-    """two-level forest (root shared by 64 requests -> tensor-core kernel,
-    300-token suffixes -> suffix kernel) with bf16-exact adversarial keys.
+def _extreme_spec(seed, mode, n_req=64):
+    """two-level forest (root shared by 64 requests -> tensor-core kernel;
+    by 12 -> the transposed tensor-core kernel; 300-token suffixes -> suffix
+    kernel) with bf16-exact adversarial keys.
     'extreme': q = 1 everywhere, 1 % of the keys set to +-44.25 in every
     coordinate (raw scores +-500.6 after 1/sqrt(128)), elsewhere N(0,1)/sqrt(d);
     'peaked': queries scaled by 800 (scores ~ N(0, 6^2), a softmax
     dominated by a few tokens of every slice)."""
     rng = np.random.default_rng(seed)
-    spec = W.two_level(3000, 300, 64, h_q=32, h_kv=8, d=128, seed=seed)
+    spec = W.two_level(3000, 300, n_req, h_q=32, h_kv=8, d=128, seed=seed)
     if mode == "extreme":
         spec.queries = np.ones_like(spec.queries)
         for n in range(1, spec.n_nodes):
@@ -249,11 +250,12 @@ def _extreme_spec(seed, mode):
 
 
 class TestScoreExtremes:
+    @pytest.mark.parametrize("n_req", [64, 12])
     @pytest.mark.parametrize("mode", ["extreme", "peaked"])
     @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC])
-    def test_bf16_kernels(self, table, mode, flags):
+    def test_bf16_kernels(self, table, mode, flags, n_req):
         import torch
-        spec = _extreme_spec(31, mode)
+        spec = _extreme_spec(31, mode, n_req)
         to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16)
         specs = [(p, to(k), to(v)) for p, k, v, _ in spec.node_specs()]
         qb = P.QueryBatch(to(spec.queries), spec.h_kv)
@@ -261,8 +263,10 @@ class TestScoreExtremes:
         plan = P.plan_device(f, 4, table, 8, 148)
         kp, vp = f.device_pool(torch.bfloat16)
         step = DecodeStep(f, plan, 32, "bfloat16", flags=flags)
-        if flags == 0:
+        if flags == 0 and n_req == 64:
             assert step.info.n_tc_groups > 0 and step.info.n_gemv_groups > 0
+        if flags == 0 and n_req == 12:
+            assert step.info.n_tct_groups > 0 and step.info.n_tc_groups == 0
         out = step(qb.queries.cuda(), kp, vp).double().cpu().numpy()
         ref = oracle_requests(f, kp, vp, qb.queries.cuda(), list(range(f.bs)))
         close(out, ref, f"{mode} flags={flags}")

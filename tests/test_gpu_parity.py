@@ -13,7 +13,8 @@ from recipes import PAC_SHAPES, pac_inputs, random_forest_spec
 from oracle import attention as OA
 import paper_2505_17694_b200 as P
 from paper_2505_17694_b200 import workloads as W
-from paper_2505_17694_b200.executor import FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_MULTI, FLAG_NO_TC, DecodeStep
+from paper_2505_17694_b200.executor import (FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_MULTI, FLAG_NO_TC, FLAG_NO_TCT,
+                                            DecodeStep)
 
 pytestmark = pytest.mark.gpu
 
@@ -216,7 +217,7 @@ def d128_forest(seed, with_masks):
 
 class TestBf16Kernels:
     @pytest.mark.parametrize("flags", [0, FLAG_FORCE_TC, FLAG_NO_TC, FLAG_NO_MULTI, FLAG_NO_TC | FLAG_NO_MULTI,
-                                       1048576, FLAG_FORCE_TC | 1048576])
+                                       FLAG_NO_TCT, FLAG_NO_MULTI | FLAG_NO_TCT, 1048576, FLAG_FORCE_TC | 1048576])
     def test_random_forests(self, cuda_ok, table, flags):
         for seed in range(24):
             spec = d128_forest(seed, with_masks=(seed % 2 == 1))
@@ -549,3 +550,60 @@ class TestMultiRequestKernel:
         assert_bf16_close(off, ref)
         # the same inputs, the same step: bit-repeatable
         assert np.array_equal(np_(multi(q, kp, vp)), got)
+
+
+class TestTransposedKernel:
+    @pytest.mark.parametrize("g", [2, 4, 8])
+    @pytest.mark.parametrize("counted", [0, 1048576])
+    def test_lightly_shared_roots(self, cuda_ok, table, g, counted):
+        """Roots read by 17..128 query-head rows (kern_tct.cu: tokens on the
+        MMA's M, rows on N): several KV slices per root (TCT_SLICE), 16..64
+        rows per CTA, ragged visible counts inside a group (per-column
+        masks), and a band of large keys in the middle of some roots so a
+        later tile passes the column references (the rescale of O^T in
+        TMEM). Against the float64 oracle and the same plan with the kernel
+        off (the M = 256 pair kernel), bit-repeatable."""
+        import torch
+        rng = np.random.default_rng(70 + g)
+        h_kv = 4
+        parent, length, paths, vis = [0], [0], [], [None]
+        for t in range(6):
+            root = len(parent)
+            parent.append(0)
+            length.append(int(rng.integers(300, 9000)))
+            vis.append(None)
+            n_req = int(rng.integers(max(2, 17 // g + 1), 128 // g + 1))
+            for _ in range(n_req):
+                parent.append(root)
+                length.append(int(rng.integers(5, 200)))
+                vis.append(None)
+                paths.append((root, len(parent) - 1))
+        bs = len(paths)
+        for r, (root, leaf) in enumerate(paths):
+            if rng.random() < 0.4:
+                vis[root] = vis[root] or {}
+                vis[root][r] = int(rng.integers(1, length[root] + 1))
+        f = P.forest_from_pool(parent[1:], length[1:], paths, h_kv, 128, visible=vis[1:])
+        gen = torch.Generator().manual_seed(g)
+        T = f.total_tokens
+        kp = torch.randn((h_kv, T, 128), generator=gen) * 0.088
+        vp = torch.randn((h_kv, T, 128), generator=gen) * 0.088
+        q = torch.randn((bs, h_kv * g, 128), generator=gen) * 0.5
+        for n in range(1, len(parent), 3):  # large keys past the first tiles of every third node
+            a = f.token_offset[n] + min(length[n] - 1, 700)
+            kp[:, a:a + 40] *= 60.0
+        kp, vp, q = (x.to(torch.bfloat16).cuda() for x in (kp, vp, q))
+        plan = P.plan_device(f, g, table, h_kv, 148)
+        step = DecodeStep(f, plan, h_kv * g, "bfloat16", flags=counted)
+        assert step.info.n_tct_groups > 0
+        got = np_(step(q, kp, vp))
+        off = np_(DecodeStep(f, P.plan_device(f, g, table, h_kv, 148, tct=False), h_kv * g, "bfloat16",
+                             flags=FLAG_NO_TCT)(q, kp, vp))
+        z = np.zeros((0, h_kv, 128))
+        node = lambda pool, n: pool[:, f.token_offset[n]:f.token_offset[n] + length[n]].permute(1, 0, 2).double().cpu().numpy()
+        fd = OA.ForestData(parent, [z] + [node(kp, n) for n in range(1, len(parent))],
+                           [z] + [node(vp, n) for n in range(1, len(parent))], paths, vis)
+        ref = OA.naive_attention(q.double().cpu().numpy(), fd)
+        assert_bf16_close(got, ref)
+        assert_bf16_close(off, ref)
+        assert np.array_equal(np_(step(q, kp, vp)), got)
