@@ -17,8 +17,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 echo "launches rc=$?"
 for c in cfg2 cfg3 cfg5 cfg4; do
   b=$(python -c "import json;print(json.loads(open('$OUT/bench_$c.json').read().strip().splitlines()[-1])['config']['tc_sm_budget'])" 2>/dev/null || echo 96)
+  f=$(python -c "import json;print(0 if json.loads(open('$OUT/bench_$c.json').read().strip().splitlines()[-1])['config']['lightly_shared'].startswith('transposed') else 4194304)" 2>/dev/null || echo 0)
   timeout 900 ncu --set full --profile-from-start off --clock-control none --import-source on \
-    -o $OUT/ncu_$c python tools/ncu_step.py $c $b > $OUT/ncu_$c.log 2>&1
+    -o $OUT/ncu_$c python tools/ncu_step.py $c $b $f > $OUT/ncu_$c.log 2>&1
   echo "ncu $c budget $b rc=$?"
   echo "$b" > $OUT/budget_$c.txt
 done

@@ -38,6 +38,8 @@ def kernel_key(name):
         return "tc"
     if "mma_multi" in name:
         return "multi"
+    if "tct_kernel" in name:
+        return "tct"
     if "mma_pac" in name or "gemv_pac" in name:
         return "gemv"
     if "merge" in name:
