@@ -18,7 +18,8 @@ LIB = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "paper_2505_17694_b200"
 WATCH = ["UTCHMMA", "UTCBAR", "UTMALDG", "UTMAPF", "UBLKCP", "UBLKPF", "LDTM", "STTM", "HMMA", "LDSM", "MOVM",
          "MUFU", "FFMA2", "SYNCS", "LDG", "STG", "LDS", "STS"]
 KERNELS = {"tc_pac_kernel": "K2 tcgen05 shared-node", "mma_pac_kernel": "K3 mma.sync suffix",
-           "mma_multi_kernel": "K3m mma.sync multi-request", "merge128_kernel": "K4 LSE merge (d=128)",
+           "mma_multi_kernel": "K3m mma.sync multi-request", "tct_kernel": "K2t transposed tcgen05 (lightly shared)",
+           "merge128_kernel": "K4 LSE merge (d=128)",
            "gemv_pac_kernel": "K3' CUDA-core GEMV", "gen_decode_kernel": "generic"}
 
 sass = subprocess.run(["cuobjdump", "-sass", str(LIB)], capture_output=True, text=True, check=True).stdout
