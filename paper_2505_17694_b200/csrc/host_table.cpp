@@ -217,11 +217,12 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   const bool multi_ok = dims->kv_dtype == CODEC_BF16 && d == 128 && g <= 8 &&
                         !(dims->flags & (CODEC_FLAG_NO_MULTI | CODEC_FLAG_GEMV_SIMT | CODEC_FLAG_NO_GEMV));
   const int32_t multi_reqs = std::max(1, kMultiRows / g);
-  // slices above the multi-request range of nodes with at most
-  // tct_max_rows() query-head rows in all: the transposed tensor-core kernel
-  // (work proportional to the rows), in groups of kTctRows rows. (A larger
-  // node's last row chunk stays on the pair kernel, in lockstep with the
-  // node's other chunks: one HBM read of its KV.)
+  // slices of 2+ requests of nodes with at most tct_max_rows() query-head
+  // rows in all: the transposed tensor-core kernel (work proportional to the
+  // rows; one CTA per SM streams ~2x what three multi-request CTAs do), in
+  // groups of kTctRows rows. (A larger node's last row chunk stays on the
+  // pair kernel, in lockstep with the node's other chunks: one HBM read of
+  // its KV.) The multi-request kernel takes them without it.
   const bool tct_ok = tc_ok && g <= kTctRows && !(dims->flags & (CODEC_FLAG_NO_TCT | CODEC_FLAG_FORCE_TC));
   const int64_t tc_min_rows = multi_ok ? multi_max_rows() + 1 : kTcMinRows;
   const int32_t tct_reqs = std::max(1, kTctRows / g);
@@ -255,7 +256,7 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int kind;
     int32_t per;
     const int64_t rows_live = (int64_t)live.size() * g, rows_node = (qptr[n + 1] - qptr[n]) * (int64_t)g;
-    if (tct_ok && rows_live >= tc_min_rows && rows_node <= tct_max_rows()) {
+    if (tct_ok && live.size() >= 2 && rows_node <= tct_max_rows()) {
       kind = kKindTct;
       per = tct_reqs;
     } else if (tc_ok && (rows_live >= tc_min_rows || (dims->flags & CODEC_FLAG_FORCE_TC))) {

@@ -194,11 +194,12 @@ def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True
     """Which kernel runs a slice with `rows` query-head rows of
     `n_requests` requests of a node with `node_rows` rows in all (default:
     rows) -- host_table.cpp's routing for bf16, d = 128, g <= 8: "tct"
-    (transposed tcgen05 kernel), "tc" (tcgen05 shared-node kernel),
+    (transposed tcgen05 kernel: 2+ requests of a node of <= TCT_MAX_ROWS
+    rows), "tc" (tcgen05 shared-node kernel),
     "multi" (multi-request mma.sync kernel) or "suffix" (single-request
     mma.sync kernel)."""
     lo = MULTI_MAX_ROWS if multi else TC_MIN_ROWS - 1
-    if tct and rows > lo and (rows if node_rows is None else node_rows) <= TCT_MAX_ROWS:
+    if tct and n_requests >= 2 and (rows if node_rows is None else node_rows) <= TCT_MAX_ROWS:
         return "tct"
     if rows > lo:
         return "tc"

@@ -24,7 +24,7 @@ def route(n_live: int, g: int, multi: bool = True, force_tc: bool = False, node_
           tct: bool = True) -> str:
     rows = n_live * g
     lo = MULTI_MAX_ROWS + 1 if multi else TC_MIN_ROWS
-    if tct and not force_tc and rows >= lo and node_rows <= TCT_MAX_ROWS:
+    if tct and not force_tc and n_live >= 2 and node_rows <= TCT_MAX_ROWS:
         return "tct"
     if force_tc or rows >= lo:
         return "tc"

@@ -536,11 +536,15 @@ class TestMultiRequestKernel:
         kp = (torch.randn((h_kv, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
         vp = (torch.randn((h_kv, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
         q = (torch.randn((bs, h_kv * g, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
-        plan = P.plan_device(f, g, table, h_kv, 148)
-        multi = DecodeStep(f, plan, h_kv * g, "bfloat16")
+        # the multi-request kernel takes these slices when the transposed
+        # tensor-core kernel is off (by default that one takes 2+ requests)
+        plan = P.plan_device(f, g, table, h_kv, 148, tct=False)
+        multi = DecodeStep(f, plan, h_kv * g, "bfloat16", flags=FLAG_NO_TCT)
         assert multi.info.n_multi_groups > 0  # root 0: 2 requests = 2 g <= 16 rows
         got = np_(multi(q, kp, vp))
-        off = np_(DecodeStep(f, plan, h_kv * g, "bfloat16", flags=FLAG_NO_MULTI)(q, kp, vp))
+        off = np_(DecodeStep(f, plan, h_kv * g, "bfloat16", flags=FLAG_NO_MULTI | FLAG_NO_TCT)(q, kp, vp))
+        tct = DecodeStep(f, P.plan_device(f, g, table, h_kv, 148), h_kv * g, "bfloat16")
+        assert tct.info.n_tct_groups > 0 and tct.info.n_multi_groups == 0
         z = np.zeros((0, h_kv, 128))
         node = lambda pool, n: pool[:, f.token_offset[n]:f.token_offset[n] + length[n]].permute(1, 0, 2).double().cpu().numpy()
         fd = OA.ForestData(parent, [z] + [node(kp, n) for n in range(1, len(parent))],
@@ -548,6 +552,7 @@ class TestMultiRequestKernel:
         ref = OA.naive_attention(q.double().cpu().numpy(), fd)
         assert_bf16_close(got, ref)
         assert_bf16_close(off, ref)
+        assert_bf16_close(np_(tct(q, kp, vp)), ref)
         # the same inputs, the same step: bit-repeatable
         assert np.array_equal(np_(multi(q, kp, vp)), got)
 

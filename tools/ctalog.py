@@ -51,7 +51,7 @@ if len(gv):
     print(f"GEMV CTAs started while TC ran: {len(during)} on {len(set(during[:,0]))} SMs; "
           f"SMs shared with a TC CTA: {len(set(during[:,0]) & set(tc[:,0]))}")
     # GEMV concurrency over time
-    for t in np.linspace(0, us(max(gv[:, 2].max(), tc[:, 2].max() if len(tc) else 0)), 12):
+    for t in np.linspace(0, us(max(gv[:, 2].max(), tc[:, 2].max() if len(tc) else 0)), int(os.environ.get("CTALOG_POINTS", "12"))):
         tt = t0 + t * 1e3
         live = ((gv[:, 1] <= tt) & (gv[:, 2] > tt)).sum()
         tlive = ((tc[:, 1] <= tt) & (tc[:, 2] > tt)).sum() if len(tc) else 0
