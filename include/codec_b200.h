@@ -305,6 +305,9 @@ typedef struct {
   int32_t n_tct_groups;                                /* slices of nodes with 17..64 query-head rows (kTctMaxRows)
                                                           on the transposed tensor-core kernel: records right
                                                           after the multi-request ones (off_multi + 8 n_multi_groups) */
+  int32_t tct_ctas;                                    /* its grid (CTAs loop over the (group, kv head) items):
+                                                          one per item unless CODEC_TCT_CTAS caps it */
+  int32_t reserved2;
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

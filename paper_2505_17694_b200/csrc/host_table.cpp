@@ -64,6 +64,14 @@ int64_t tct_max_rows() {
   }();
   return v;
 }
+// CODEC_TCT_CTAS: the transposed kernel's grid (0: by KV bytes, below)
+int64_t tct_ctas_env() {
+  static const int64_t v = [] {
+    const char* e = getenv("CODEC_TCT_CTAS");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  return v;
+}
 // Cost of a unit boundary inside a CTA pair, in KV tiles (device balancer
 // below). CODEC_TC_UNIT_COST overrides it (tuning).
 int64_t tc_unit_cost() {
@@ -616,6 +624,17 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   emit_groups(kKindMulti, in.n_multi_groups, in.off_multi);
   int32_t off_tct = 0;  // right after the multi-request records
   emit_groups(kKindTct, in.n_tct_groups, off_tct);
+  // The transposed kernel's grid: one CTA per (slice group, kv head) item by
+  // default. (A programmatically dependent grid launches only once every
+  // CTA of the one before it has started, so a multi-wave K2t grid holds the
+  // suffix kernel back -- 1.2 ms on cfg4 -- but a one-wave persistent grid
+  // sized by KV bytes was slower still: one K2t CTA per SM streams only
+  // ~30-50 GB/s, cfg4 4.99 vs 3.94 ms, cfg3 158 vs 84 us. CODEC_TCT_CTAS caps
+  // the grid for experiments; the kernel loops over items either way.)
+  if (in.n_tct_groups) {
+    const int64_t items = (int64_t)in.n_tct_groups * h_local;
+    in.tct_ctas = (int32_t)(tct_ctas_env() > 0 ? std::min(items, tct_ctas_env()) : items);
+  }
   in.off_rows = (int32_t)blob.size();
   in.n_rows = (int32_t)(rows.size() / 4);
   blob.insert(blob.end(), rows.begin(), rows.end());

@@ -25,6 +25,8 @@
 // slow path: column maxima through SMEM, rescale of the per-thread row sums
 // and of O^T in TMEM (after the previous PV landed). Row sums are per-thread
 // partials over the thread's tokens, reduced once in the epilogue.
+#include <algorithm>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -64,7 +66,7 @@ constexpr float kRefSlack = 8.f;  // a score may pass its column reference by 2^
 struct TctBars {
   uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], s_free[2], p_full[2], p_empty[2];
-  uint64_t q_full;
+  uint64_t q_full, o_free;  // per item: Q rows staged / the epilogue read O^T
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4]: a parity wait never sees a phase two behind
   uint32_t tmem_slot;
 };
@@ -111,7 +113,7 @@ __device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r) 
 // epilogue (row sums, O^T out of TMEM, one coalesced 128-byte warp store
 // per row and d quarter).
 template <int N>
-__device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint32_t tmem, int n_tiles, int n_cols,
+__device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint32_t tmem, int jb, int n_tiles, int n_cols,
                                              int kh, int g, int hq_local, float* __restrict__ out,
                                              float* __restrict__ part_o, float* __restrict__ part_ml,
                                              const int32_t* __restrict__ entry_of, int32_t* __restrict__ cnt) {
@@ -137,8 +139,8 @@ __device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint3
   if (t < kTctRows) mref[t] = 0.f;  // tile 0 always takes the slow path: its x are absolute
   named_sync(2, 128);
   for (int j = 0; j < n_tiles; ++j) {
-    const int b = j & 1;
-    mbar_wait(&bars->s_full[b], (j >> 1) & 1);
+    const int jg = jb + j, b = jg & 1;  // the CTA's tile sequence runs on across its items
+    mbar_wait(&bars->s_full[b], (jg >> 1) & 1);
     tc::fence_after();
     uint32_t sr[N];
     tmem_ld_cols<N>(tmem + lane_base + kColS + b * kTctRows, sr);
@@ -195,7 +197,7 @@ __device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint3
         }
       }
       if (j > 0) {  // O^T (thread = d lane) rescaled once PV(j - 1) landed; PV(j) waits for P(j)
-        mbar_wait(&bars->pv_done[(j - 1) & 3], ((j - 1) >> 2) & 1);
+        mbar_wait(&bars->pv_done[(jg - 1) & 3], ((jg - 1) >> 2) & 1);
         tc::fence_after();
 #pragma unroll
         for (int c = 0; c < N; c += 16) {
@@ -210,7 +212,7 @@ __device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint3
       }
     }
     // P^T(j) into SMEM buffer b once PV(j - 2) read it
-    if (j >= 2) mbar_wait(&bars->p_empty[b], ((j - 2) >> 1) & 1);
+    if (jg >= 2) mbar_wait(&bars->p_empty[b], ((jg - 2) >> 1) & 1);
     const uint32_t pb = pbase + b * kPtBytes + patom + pin;
 #pragma unroll
     for (int n = 0; n < N; ++n) {
@@ -231,11 +233,15 @@ __device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint3
     if (lane == 0) red[warp * kTctRows + n] = v;
   }
   named_sync(2, 128);
-  mbar_wait(&bars->pv_done[(n_tiles - 1) & 3], ((n_tiles - 1) >> 2) & 1);
+  const int jl = jb + n_tiles - 1;
+  mbar_wait(&bars->pv_done[jl & 3], (jl >> 2) & 1);
   tc::fence_after();
   uint32_t o[N];
   tmem_ld_cols<N>(tmem + lane_base + kColO, o);
   tc::wait_ld();
+  tc::fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&bars->o_free);  // the next item's first PV may overwrite O^T
 #pragma unroll
   for (int n = 0; n < N; ++n) {
     if (n < n_cols) {
@@ -263,23 +269,35 @@ __device__ __forceinline__ void softmax_unit(uint8_t* smem, TctBars* bars, uint3
 
 __global__ void __launch_bounds__(kTctThreads, 1)
     tct_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-               const int32_t* __restrict__ table, int off_groups, int off_rows, const __nv_bfloat16* __restrict__ q,
-               int64_t pool_tokens, int g, int hq_local, float* __restrict__ out, float* __restrict__ part_o,
-               float* __restrict__ part_ml, const int32_t* __restrict__ page_table, int page_shift,
-               int32_t* __restrict__ done, const int32_t* __restrict__ entry_of, int32_t* __restrict__ cnt) {
+               const int32_t* __restrict__ table, int off_groups, int off_rows, int n_groups, int h_local,
+               const __nv_bfloat16* __restrict__ q, int64_t pool_tokens, int g, float* __restrict__ out,
+               float* __restrict__ part_o, float* __restrict__ part_ml, const int32_t* __restrict__ page_table,
+               int page_shift, int32_t* __restrict__ done, const int32_t* __restrict__ entry_of,
+               int32_t* __restrict__ cnt) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   TctBars* bars = reinterpret_cast<TctBars*>(smem + kOffBar);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int32_t* grp = table + off_groups + blockIdx.x * kGroupInts;
-  const int kh = blockIdx.y;
-  const int32_t* rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
-  const int n_cols = grp[kGrpNRows] * g;
-  const int npad = (n_cols + 15) & ~15;
-  const int n_tiles = (grp[kGrpMaxVis] + kTctBN - 1) / kTctBN;
-  const int kv_tok = grp[kGrpKvTok];
-  if (n_cols > kTctRows) __trap();  // the host routes at most kTctRows rows here
+  const int hq_local = g * h_local, n_items = n_groups * h_local;
+  // item it = (group it / h_local, kv head it % h_local); a CTA takes items
+  // blockIdx.x, + gridDim.x, ... (the grid fits in one wave beside the TC
+  // grid, so the suffix kernel launched after it starts at once)
+  struct Item {
+    const int32_t* rows;
+    int kh, n_cols, npad, n_tiles, kv_tok;
+  };
+  auto item = [&](int it) {
+    const int32_t* grp = table + off_groups + (it / h_local) * kGroupInts;
+    Item x;
+    x.kh = it % h_local;
+    x.rows = table + off_rows + grp[kGrpRowBegin] * kRowInts;
+    x.n_cols = grp[kGrpNRows] * g;
+    x.npad = (x.n_cols + 15) & ~15;
+    x.n_tiles = (grp[kGrpMaxVis] + kTctBN - 1) / kTctBN;
+    x.kv_tok = grp[kGrpKvTok];
+    return x;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -295,8 +313,8 @@ __global__ void __launch_bounds__(kTctThreads, 1)
       mbar_init(&bars->p_empty[b], 1);
     }
     mbar_init(&bars->q_full, 4);
+    mbar_init(&bars->o_free, 4);
     for (int i = 0; i < 4; ++i) mbar_init(&bars->pv_done[i], 1);
-    reinterpret_cast<int32_t*>(smem + kOffMisc)[kTctRows] = 0x7fffffff;
     fence_barrier_init();
   }
   if (warp == 5) tc::tmem_alloc(&bars->tmem_slot, kTmemCols);
@@ -305,46 +323,57 @@ __global__ void __launch_bounds__(kTctThreads, 1)
   tc::fence_after();
   const uint32_t tmem = bars->tmem_slot;
 
+  int tiles_total = 0;  // this CTA's tiles over all its items (barrier phases run on across items)
   if (warp < 4) {
-    // ---- per column: visible tokens, slot, output row, request; Q rows
     int32_t* rinfo = reinterpret_cast<int32_t*>(smem + kOffRow);
-    if (tid < kTctRows) {
-      int vis = 0, slot = 0, orow = 0, req = 0;
-      if (tid < n_cols) {
-        const int32_t* row = rows + (tid / g) * kRowInts;
-        req = row[0];
-        vis = row[1];
-        slot = row[2];
-        const int qh = kh * g + tid % g;
-        orow = slot < 0 ? req * hq_local + qh : slot * hq_local + qh;
-        atomicMin(reinterpret_cast<int32_t*>(smem + kOffMisc) + kTctRows, vis);
+    int32_t* minv = reinterpret_cast<int32_t*>(smem + kOffMisc) + kTctRows;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const Item x = item(it);
+      if (x.n_cols > kTctRows) __trap();  // the host routes at most kTctRows rows here
+      // ---- per column: visible tokens, slot, output row, request; Q rows
+      // (the previous item's S MMAs are complete: its tiles were consumed)
+      if (tid == 0) *minv = 0x7fffffff;
+      named_sync(2, 128);
+      if (tid < kTctRows) {
+        int vis = 0, slot = 0, orow = 0, req = 0;
+        if (tid < x.n_cols) {
+          const int32_t* row = x.rows + (tid / g) * kRowInts;
+          req = row[0];
+          vis = row[1];
+          slot = row[2];
+          const int qh = x.kh * g + tid % g;
+          orow = slot < 0 ? req * hq_local + qh : slot * hq_local + qh;
+          atomicMin(minv, vis);
+        }
+        rinfo[tid] = vis;
+        rinfo[kTctRows + tid] = slot;
+        rinfo[2 * kTctRows + tid] = orow;
+        rinfo[3 * kTctRows + tid] = req;
       }
-      rinfo[tid] = vis;
-      rinfo[kTctRows + tid] = slot;
-      rinfo[2 * kTctRows + tid] = orow;
-      rinfo[3 * kTctRows + tid] = req;
-    }
-    // Q rows as the K-major SW128 B operand: 16-byte chunk c of row n at
-    // atom column c / 8, row n, chunk (c % 8) XOR (n % 8); padding rows zero
+      // Q rows as the K-major SW128 B operand: 16-byte chunk c of row n at
+      // atom column c / 8, row n, chunk (c % 8) XOR (n % 8); padding rows zero
 #pragma unroll
-    for (int i = 0; i < (kTctRows * 16) / 128; ++i) {
-      const int e = i * 128 + tid, n = e >> 4, c = e & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (n < n_cols) {
-        const int req = __ldg(rows + (n / g) * kRowInts);
-        v = __ldg(reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + kh * g + n % g) * kTctD) + c);
+      for (int i = 0; i < (kTctRows * 16) / 128; ++i) {
+        const int e = i * 128 + tid, n = e >> 4, c = e & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (n < x.n_cols) {
+          const int req = __ldg(x.rows + (n / g) * kRowInts);
+          v = __ldg(reinterpret_cast<const uint4*>(q + ((int64_t)req * hq_local + x.kh * g + n % g) * kTctD) + c);
+        }
+        *reinterpret_cast<uint4*>(smem + kOffQ + (c >> 3) * kAtomQ + n * 128 + (((c & 7) ^ (n & 7)) << 4)) = v;
       }
-      *reinterpret_cast<uint4*>(smem + kOffQ + (c >> 3) * kAtomQ + n * 128 + (((c & 7) ^ (n & 7)) << 4)) = v;
-    }
-    tc::fence_proxy_async_smem();
-    named_sync(2, 128);  // row info and min_vis before the softmax reads them
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&bars->q_full);
-    switch (npad) {
-      case 16: softmax_unit<16>(smem, bars, tmem, n_tiles, n_cols, kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
-      case 32: softmax_unit<32>(smem, bars, tmem, n_tiles, n_cols, kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
-      case 48: softmax_unit<48>(smem, bars, tmem, n_tiles, n_cols, kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
-      default: softmax_unit<64>(smem, bars, tmem, n_tiles, n_cols, kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
+      tc::fence_proxy_async_smem();
+      named_sync(2, 128);  // row info and min_vis before the softmax reads them
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->q_full);
+      switch (x.npad) {
+        case 16: softmax_unit<16>(smem, bars, tmem, tiles_total, x.n_tiles, x.n_cols, x.kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
+        case 32: softmax_unit<32>(smem, bars, tmem, tiles_total, x.n_tiles, x.n_cols, x.kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
+        case 48: softmax_unit<48>(smem, bars, tmem, tiles_total, x.n_tiles, x.n_cols, x.kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
+        default: softmax_unit<64>(smem, bars, tmem, tiles_total, x.n_tiles, x.n_cols, x.kh, g, hq_local, out, part_o, part_ml, entry_of, cnt); break;
+      }
+      tiles_total += x.n_tiles;
+      named_sync(2, 128);  // every thread's epilogue reads of the row info done before the next item's
     }
   } else if (warp == 4) {
     // ---- TMA producer: K and V tiles, both SW128 atom columns in one op
@@ -352,27 +381,30 @@ __global__ void __launch_bounds__(kTctThreads, 1)
       tc::prefetch_tmap(&tmk);
       tc::prefetch_tmap(&tmv);
       const uint64_t pol = tc::policy_evict_first();  // read by this CTA only
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        int x = kv_tok + j * kTctBN;  // paged pool: a 128-token tile never crosses a page
-        if (page_shift) x = (__ldg(page_table + (x >> page_shift)) << page_shift) | (x & ((1 << page_shift) - 1));
-        const int y = kh * (int)pool_tokens + x;
-        if (j >= kStages) mbar_wait(&bars->k_empty[s], ((j - kStages) >> 1) & 1);
-        mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
-        tc::tma_load_3d_hint(smem + kOffK + s * kTileBytes, &tmk, 0, y, 0, &bars->k_full[s], pol);
-        if (j >= kStages) mbar_wait(&bars->v_empty[s], ((j - kStages) >> 1) & 1);
-        mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
-        tc::tma_load_3d_hint(smem + kOffV + s * kTileBytes, &tmv, 0, y, 0, &bars->v_full[s], pol);
+      int jg = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const Item x = item(it);
+        for (int j = 0; j < x.n_tiles; ++j, ++jg) {
+          const int s = jg & 1;
+          int xt = x.kv_tok + j * kTctBN;  // paged pool: a 128-token tile never crosses a page
+          if (page_shift)
+            xt = (__ldg(page_table + (xt >> page_shift)) << page_shift) | (xt & ((1 << page_shift) - 1));
+          const int y = x.kh * (int)pool_tokens + xt;
+          if (jg >= kStages) mbar_wait(&bars->k_empty[s], ((jg - kStages) >> 1) & 1);
+          mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
+          tc::tma_load_3d_hint(smem + kOffK + s * kTileBytes, &tmk, 0, y, 0, &bars->k_full[s], pol);
+          if (jg >= kStages) mbar_wait(&bars->v_empty[s], ((jg - kStages) >> 1) & 1);
+          mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
+          tc::tma_load_3d_hint(smem + kOffV + s * kTileBytes, &tmv, 0, y, 0, &bars->v_full[s], pol);
+        }
       }
     }
   } else {
     // ---- MMA issuer: S^T(j), then PV(j - 1) (the tensor pipe computes
     // S^T(j + 1) while the softmax works on tile j)
     const uint32_t sbase = smem_u32(smem);
-    const uint32_t idesc_s = tc::idesc_bf16(128, npad, false, false);
-    const uint32_t idesc_o = tc::idesc_bf16(128, npad, true, false);
-    mbar_wait(&bars->q_full, 0);
-    auto pv = [&](int tp) {
+    int jg = 0, u = 0;
+    auto pv = [&](int tp, int j_item, uint32_t idesc_o) {
       const int vb = tp & 1;
       mbar_wait(&bars->p_full[vb], (tp >> 1) & 1);
       mbar_wait(&bars->v_full[vb], (tp >> 1) & 1);
@@ -383,7 +415,7 @@ __global__ void __launch_bounds__(kTctThreads, 1)
           // A = V^T: MN-major, 64-d blocks 16 KB apart (LBO), 8-token groups 1 KB apart (SBO)
           const uint64_t av = tc::smem_desc(sbase + kOffV + vb * kTileBytes + k * 2048, kAtomTile, 1024);
           const uint64_t bp = tc::smem_desc(sbase + kOffP + vb * kPtBytes + (k >> 2) * kAtomP + (k & 3) * 32, 16, 1024);
-          tc::mma_f16_ss(tmem + kColO, av, bp, idesc_o, (tp > 0 || k > 0) ? 1u : 0u);
+          tc::mma_f16_ss(tmem + kColO, av, bp, idesc_o, (j_item > 0 || k > 0) ? 1u : 0u);
         }
         tc::commit(&bars->v_empty[vb]);
         tc::commit(&bars->p_empty[vb]);
@@ -391,29 +423,41 @@ __global__ void __launch_bounds__(kTctThreads, 1)
       }
       __syncwarp();
     };
-    for (int j = 0; j < n_tiles; ++j) {
-      const int s = j & 1;
-      mbar_wait(&bars->k_full[s], (j >> 1) & 1);
-      if (j >= 2) mbar_wait(&bars->s_free[s], ((j - 2) >> 1) & 1);
-      tc::fence_after();
-      if (tc::elect_one()) {
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++u) {
+      const Item x = item(it);
+      const uint32_t idesc_s = tc::idesc_bf16(128, x.npad, false, false);
+      const uint32_t idesc_o = tc::idesc_bf16(128, x.npad, true, false);
+      mbar_wait(&bars->q_full, u & 1);
+      for (int j = 0; j < x.n_tiles; ++j, ++jg) {
+        const int s = jg & 1;
+        mbar_wait(&bars->k_full[s], (jg >> 1) & 1);
+        if (jg >= 2) mbar_wait(&bars->s_free[s], ((jg - 2) >> 1) & 1);
+        tc::fence_after();
+        if (tc::elect_one()) {
 #pragma unroll
-        for (int k = 0; k < kTctD / 16; ++k) {
-          const uint64_t ak = tc::smem_desc(sbase + kOffK + s * kTileBytes + (k >> 2) * kAtomTile + (k & 3) * 32, 16, 1024);
-          const uint64_t bq = tc::smem_desc(sbase + kOffQ + (k >> 2) * kAtomQ + (k & 3) * 32, 16, 1024);
-          tc::mma_f16_ss(tmem + kColS + s * kTctRows, ak, bq, idesc_s, k > 0 ? 1u : 0u);
+          for (int k = 0; k < kTctD / 16; ++k) {
+            const uint64_t ak = tc::smem_desc(sbase + kOffK + s * kTileBytes + (k >> 2) * kAtomTile + (k & 3) * 32, 16, 1024);
+            const uint64_t bq = tc::smem_desc(sbase + kOffQ + (k >> 2) * kAtomQ + (k & 3) * 32, 16, 1024);
+            tc::mma_f16_ss(tmem + kColS + s * kTctRows, ak, bq, idesc_s, k > 0 ? 1u : 0u);
+          }
+          tc::commit(&bars->k_empty[s]);
+          tc::commit(&bars->s_full[s]);
         }
-        tc::commit(&bars->k_empty[s]);
-        tc::commit(&bars->s_full[s]);
+        __syncwarp();
+        if (j >= 1) {
+          pv(jg - 1, j - 1, idesc_o);
+        } else if (u > 0) {
+          mbar_wait(&bars->o_free, (u - 1) & 1);  // the previous item's epilogue read O^T
+          tc::fence_after();
+        }
       }
-      __syncwarp();
-      if (j >= 1) pv(j - 1);
+      pv(jg - 1, x.n_tiles - 1, idesc_o);
     }
-    pv(n_tiles - 1);
+    tiles_total = jg;
     // every commit's arrival landed before the CTA exits (a late one would
     // hit the SMEM of the next CTA on this SM): the last phase of each
     for (int s = 0; s < kStages; ++s) {
-      const int uses = (n_tiles - s + 1) / 2;
+      const int uses = (tiles_total - s + 1) / 2;
       if (uses > 0) {
         mbar_wait(&bars->k_empty[s], (uses - 1) & 1);
         mbar_wait(&bars->v_empty[s], (uses - 1) & 1);
@@ -421,16 +465,21 @@ __global__ void __launch_bounds__(kTctThreads, 1)
       }
     }
     for (int i = 0; i < 4; ++i) {
-      const int uses = (n_tiles - i + 3) / 4;
+      const int uses = (tiles_total - i + 3) / 4;
       if (uses > 0) mbar_wait(&bars->pv_done[i], (uses - 1) & 1);
     }
   }
-  // completion count for the merge (it may start before this grid ends)
+  // completion count for the merge (it may start before this grid ends):
+  // one per item, as the table's CTA count expects
   __threadfence();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (tid == 0 && done) atomicAdd(done, 1);
+  if (tid == 0 && done) {
+    int mine = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) ++mine;
+    if (mine) atomicAdd(done, mine);
+  }
   if (warp == 5) tc::tmem_dealloc(tmem, kTmemCols);
 }
 
@@ -444,7 +493,7 @@ int32_t encode_pool_halves_map(CUtensorMap* map, const void* pool, int64_t rows,
 int32_t launch_tct(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q, const void* k,
                    const void* v, int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
                    cudaStream_t st, bool pdl, const int32_t* page_table, int page_shift, int32_t* done,
-                   const int32_t* entry_of, int32_t* cnt) {
+                   const int32_t* entry_of, int32_t* cnt, int max_ctas) {
   if (n_groups == 0) return CODEC_OK;
   if (g > kTctRows) return fail(CODEC_ERR_UNSUPPORTED, "transposed tensor-core kernel: g = %d > %d", g, kTctRows);
   CUtensorMap mk, mv;
@@ -453,7 +502,8 @@ int32_t launch_tct(const int32_t* table, int n_groups, int off_groups, int off_r
   cudaError_t e = cudaFuncSetAttribute(tct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTctSmem);
   if (e != cudaSuccess) return cuda_status(e, "tct smem attribute");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_groups, h_local);
+  const int n_items = n_groups * h_local;
+  cfg.gridDim = dim3(max_ctas > 0 ? std::min(n_items, max_ctas) : n_items);
   cfg.blockDim = dim3(kTctThreads);
   cfg.dynamicSmemBytes = kTctSmem;
   cfg.stream = st;
@@ -462,9 +512,9 @@ int32_t launch_tct(const int32_t* table, int n_groups, int off_groups, int off_r
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  e = cudaLaunchKernelEx(&cfg, tct_kernel, mk, mv, table, off_groups, off_rows, (const __nv_bfloat16*)q, pool_tokens,
-                         g, h_local * g, (float*)out, (float*)part_o, (float*)part_ml, page_table, page_shift, done,
-                         entry_of, cnt);
+  e = cudaLaunchKernelEx(&cfg, tct_kernel, mk, mv, table, off_groups, off_rows, n_groups, h_local,
+                         (const __nv_bfloat16*)q, pool_tokens, g, (float*)out, (float*)part_o, (float*)part_ml,
+                         page_table, page_shift, done, entry_of, cnt);
   if (e != cudaSuccess) return cuda_status(e, "tct launch");
   return cuda_status(cudaGetLastError(), "tct launch");
 }
