@@ -276,6 +276,8 @@ CODEC_API int32_t codec_page_layout(const codec_index* ix, int32_t page_size, in
 #define CODEC_FLAG_DBG_NO_PWAIT 65536 /* with DBG_NO_TMEM: softmax skips the P-buffer (PV(t-2)) wait: timing only (debug) */
 #define CODEC_FLAG_NO_TCT 4194304 /* lightly shared slices above the multi-request range on the M = 256 pair kernel
                                       instead of the transposed tensor-core kernel */
+#define CODEC_FLAG_TCT_WIDE 8388608 /* the transposed tensor-core kernel also takes nodes of 65..128 query-head rows
+                                       (its wide variant) instead of the pair kernel */
 #define CODEC_FLAG_MERGE_ALL 2097152 /* every (request, kv head) output goes through the merge kernel, single-partial
                                         ones too (no direct writes by the split kernels): what the fused peer-store
                                         output gather (codec_decode_attention_gather) needs */
@@ -302,12 +304,13 @@ typedef struct {
   int32_t n_multi_groups, off_multi;                   /* lightly shared slices (2..32/g requests) on the
                                                           multi-request mma.sync kernel */
   int32_t off_entry_of;                                /* [bs][h_local] merge entry of (request, kv head), -1 none */
-  int32_t n_tct_groups;                                /* slices of nodes with 17..64 query-head rows (kTctMaxRows)
+  int32_t n_tct_groups;                                /* slices of 2+ requests of nodes with <= 64 query-head rows (128 with TCT_WIDE)
                                                           on the transposed tensor-core kernel: records right
                                                           after the multi-request ones (off_multi + 8 n_multi_groups) */
   int32_t tct_ctas;                                    /* its grid (CTAs loop over the (group, kv head) items):
                                                           one per item unless CODEC_TCT_CTAS caps it */
-  int32_t reserved2;
+  int32_t n_tct_wide;                                  /* the last n_tct_wide of those groups have 65..128 rows
+                                                          (the wide variant; the others <= 64) */
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

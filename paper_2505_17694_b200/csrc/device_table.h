@@ -41,10 +41,12 @@ constexpr int kMultiRows = 32;
 #define CODEC_MULTI_MAX_ROWS 16
 #endif
 constexpr int kMultiMaxRows = CODEC_MULTI_MAX_ROWS;
-// transposed tensor-core kernel: slices of kMultiMaxRows + 1 .. kTctMaxRows
-// query-head rows (CODEC_TCT_MAX_ROWS overrides), in groups of at most
-// kTctRows rows (the MMA's N); larger slices take the M = 256 pair kernel
-constexpr int kTctRows = 64;
+// transposed tensor-core kernel: slices of 2+ requests of nodes with at
+// most kTctMaxRows query-head rows (CODEC_TCT_MAX_ROWS overrides;
+// CODEC_FLAG_TCT_WIDE raises it to kTctRows), in groups of at most kTctRows
+// rows (the MMA's N; groups of up to 64 rows run the narrow variant, 65..128
+// the wide one); larger nodes take the M = 256 pair kernel
+constexpr int kTctRows = 128;
 #ifndef CODEC_TCT_MAX_ROWS
 #define CODEC_TCT_MAX_ROWS 64
 #endif

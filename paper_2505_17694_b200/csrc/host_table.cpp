@@ -264,7 +264,8 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
     int kind;
     int32_t per;
     const int64_t rows_live = (int64_t)live.size() * g, rows_node = (qptr[n + 1] - qptr[n]) * (int64_t)g;
-    if (tct_ok && live.size() >= 2 && rows_node <= tct_max_rows()) {
+    const int64_t tct_max = (dims->flags & CODEC_FLAG_TCT_WIDE) ? (int64_t)kTctRows : tct_max_rows();
+    if (tct_ok && live.size() >= 2 && rows_node <= tct_max) {
       kind = kKindTct;
       per = tct_reqs;
     } else if (tc_ok && (rows_live >= tc_min_rows || (dims->flags & CODEC_FLAG_FORCE_TC))) {
@@ -622,8 +623,20 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   emit_groups(kKindGemv, in.n_gemv_groups, in.off_gemv);
   emit_groups(kKindGeneric, in.n_gen_groups, in.off_gen);
   emit_groups(kKindMulti, in.n_multi_groups, in.off_multi);
-  int32_t off_tct = 0;  // right after the multi-request records
-  emit_groups(kKindTct, in.n_tct_groups, off_tct);
+  // right after the multi-request records: groups of <= 64 rows (the
+  // narrow kernel) first, then those of 65..128 rows (the wide one)
+  {
+    in.n_tct_groups = 0;
+    in.n_tct_wide = 0;
+    for (int wide = 0; wide < 2; ++wide)
+      for (auto& gr : groups)
+        if (gr.kind == kKindTct && ((int64_t)gr.n_rows * g > 64) == (wide == 1)) {
+          int32_t rec[kGroupInts] = {gr.kv_tok, gr.len, gr.row_begin, gr.n_rows, gr.max_vis, gr.node, gr.start, 0};
+          blob.insert(blob.end(), rec, rec + kGroupInts);
+          ++in.n_tct_groups;
+          in.n_tct_wide += wide;
+        }
+  }
   // The transposed kernel's grid: one CTA per (slice group, kv head) item by
   // default. (A programmatically dependent grid launches only once every
   // CTA of the one before it has started, so a multi-wave K2t grid holds the

@@ -34,7 +34,7 @@ int32_t launch_mma_multi(const int32_t* table, int n_groups, int off_groups, int
 int32_t launch_tct(const int32_t* table, int n_groups, int off_groups, int off_rows, const void* q, const void* k,
                    const void* v, int64_t pool_tokens, int g, int h_local, void* out, void* part_o, void* part_ml,
                    cudaStream_t st, bool pdl, const int32_t* page_table, int page_shift, int32_t* done,
-                   const int32_t* entry_of, int32_t* cnt, int max_ctas);
+                   const int32_t* entry_of, int32_t* cnt, int max_ctas, int n_wide);
 int32_t launch_generic_groups(int dtype, const int32_t* table, int n_groups, int off_groups, int off_rows,
                               const void* q, const void* k, const void* v, int64_t pool_tokens, int d, int g,
                               int hq_local, void* out, void* part_o, void* part_ml, cudaStream_t st);
@@ -244,7 +244,8 @@ static int32_t decode_impl(const codec_dims* dims, const codec_table_info* info,
   if (do_tct)
     CODEC_TRY(launch_tct(table_dev, info->n_tct_groups, info->off_multi + kGroupInts * info->n_multi_groups,
                          info->off_rows, q, k, v, dims->pool_tokens, g, h_local, out, part_o, part_ml, st,
-                         do_tc && early, dims->page_table, page_shift, tc_done, entry_of, cnt, info->tct_ctas));
+                         do_tc && early, dims->page_table, page_shift, tc_done, entry_of, cnt, info->tct_ctas,
+                         info->n_tct_wide));
   if (do_multi)
     CODEC_TRY(launch_mma_multi(table_dev, info->n_multi_groups, info->off_multi, info->off_rows, q, k, v,
                                dims->pool_tokens, g, h_local, out, part_o, part_ml, st, (do_tc || do_tct) && early,

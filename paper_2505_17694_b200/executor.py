@@ -37,6 +37,7 @@ FLAG_FORCE_TC = 2
 FLAG_NO_GEMV = 4
 FLAG_NO_MULTI = 524288
 FLAG_NO_TCT = 4194304  # no transposed tensor-core kernel (its slices on the pair kernel)
+FLAG_TCT_WIDE = 8388608  # the transposed kernel also takes nodes of 65..128 rows (plan with tct_wide=True)
 FLAG_MERGE_ALL = 2097152  # every output row through the merge kernel (the fused peer-store gather needs it)
 
 

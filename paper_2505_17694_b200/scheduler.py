@@ -146,6 +146,7 @@ MULTI_MAX_ROWS = int(os.environ.get("CODEC_MULTI_MAX_ROWS", "16"))
 # query-head rows in all (device_table.h kTctMaxRows; the library reads the
 # same CODEC_TCT_MAX_ROWS override), cut into slices of TCT_SLICE tokens
 TCT_MAX_ROWS = int(os.environ.get("CODEC_TCT_MAX_ROWS", "64"))
+TCT_WIDE_ROWS = 128  # with CODEC_FLAG_TCT_WIDE (device_table.h kTctRows)
 TCT_SLICE = int(os.environ.get("CODEC_TCT_SLICE", "4096"))
 TC_CTAS_PER_BLOCK = 2  # a tensor-core schedule block is a cta_group::2 CTA pair (device_table.h)
 SUFFIX_SLICE = 4096    # longest KV slice one suffix-kernel CTA streams (plan_device)
@@ -190,7 +191,8 @@ def concat_plans(plans) -> DivisionPlan:
                         cost_l_ms=plans[0].cost_l_ms, search_truncated=any(p.search_truncated for p in plans))
 
 
-def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True, node_rows: int | None = None) -> str:
+def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True, node_rows: int | None = None,
+                tct_wide: bool = False) -> str:
     """Which kernel runs a slice with `rows` query-head rows of
     `n_requests` requests of a node with `node_rows` rows in all (default:
     rows) -- host_table.cpp's routing for bf16, d = 128, g <= 8: "tct"
@@ -199,7 +201,8 @@ def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True
     "multi" (multi-request mma.sync kernel) or "suffix" (single-request
     mma.sync kernel)."""
     lo = MULTI_MAX_ROWS if multi else TC_MIN_ROWS - 1
-    if tct and n_requests >= 2 and (rows if node_rows is None else node_rows) <= TCT_MAX_ROWS:
+    tmax = TCT_WIDE_ROWS if tct_wide else TCT_MAX_ROWS
+    if tct and n_requests >= 2 and (rows if node_rows is None else node_rows) <= tmax:
         return "tct"
     if rows > lo:
         return "tc"
@@ -210,7 +213,7 @@ def node_kernel(rows: int, n_requests: int, multi: bool = True, tct: bool = True
 
 def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_count: int = 148,
                 tc_sm_budget: int = 0, search_limit: int = DEFAULT_SEARCH_LIMIT, page_size: int = 0,
-                multi: bool = True, tct: bool = True) -> DivisionPlan:
+                multi: bool = True, tct: bool = True, tct_wide: bool = False) -> DivisionPlan:
     """The B200 plan of one decode step. Shared nodes (more than
     MULTI_MAX_ROWS query-head rows per chunk; TC_MIN_ROWS with multi=False)
     stay whole here: on the tensor cores every KV tile costs the same (an
@@ -227,7 +230,8 @@ def plan_device(forest, group_size: int, table: CostTable, h_local: int, sm_coun
     whole: a slice must start on a 32-token chunk boundary of its node."""
     tasks = device_tasks(forest, group_size)
     g = int(group_size)
-    kind = [node_kernel(t.n_q, t.n_q // g, multi, tct, len(forest.node(t.node).query_set) * g) for t in tasks]
+    kind = [node_kernel(t.n_q, t.n_q // g, multi, tct, len(forest.node(t.node).query_set) * g, tct_wide)
+            for t in tasks]
     tc = [t for t, k in zip(tasks, kind) if k == "tc"]
     tcts = [t for t, k in zip(tasks, kind) if k == "tct"]
     gv = [t for t, k in zip(tasks, kind) if k not in ("tc", "tct")]

@@ -17,7 +17,7 @@ tiles at the same time."""
 from __future__ import annotations
 
 MULTI_ROWS, MULTI_MAX_ROWS, TC_MIN_ROWS, TC_ROWS = 32, 16, 16, 256
-TCT_ROWS, TCT_MAX_ROWS = 64, 64
+TCT_ROWS, TCT_MAX_ROWS = 128, 64
 
 
 def route(n_live: int, g: int, multi: bool = True, force_tc: bool = False, node_rows: int = 0,

@@ -14,7 +14,7 @@ from oracle import attention as OA
 import paper_2505_17694_b200 as P
 from paper_2505_17694_b200 import workloads as W
 from paper_2505_17694_b200.executor import (FLAG_FORCE_TC, FLAG_NO_GEMV, FLAG_NO_MULTI, FLAG_NO_TC, FLAG_NO_TCT,
-                                            DecodeStep)
+                                            FLAG_TCT_WIDE, DecodeStep)
 
 pytestmark = pytest.mark.gpu
 
@@ -560,7 +560,8 @@ class TestMultiRequestKernel:
 class TestTransposedKernel:
     @pytest.mark.parametrize("g", [2, 4, 8])
     @pytest.mark.parametrize("counted", [0, 1048576])
-    def test_lightly_shared_roots(self, cuda_ok, table, g, counted):
+    @pytest.mark.parametrize("wide", [False, True])
+    def test_lightly_shared_roots(self, cuda_ok, table, g, counted, wide):
         """Roots read by 17..128 query-head rows (kern_tct.cu: tokens on the
         MMA's M, rows on N): several KV slices per root (TCT_SLICE), 16..64
         rows per CTA, ragged visible counts inside a group (per-column
@@ -598,9 +599,9 @@ class TestTransposedKernel:
             a = f.token_offset[n] + min(length[n] - 1, 700)
             kp[:, a:a + 40] *= 60.0
         kp, vp, q = (x.to(torch.bfloat16).cuda() for x in (kp, vp, q))
-        plan = P.plan_device(f, g, table, h_kv, 148)
-        step = DecodeStep(f, plan, h_kv * g, "bfloat16", flags=counted)
-        assert step.info.n_tct_groups > 0
+        plan = P.plan_device(f, g, table, h_kv, 148, tct_wide=wide)
+        step = DecodeStep(f, plan, h_kv * g, "bfloat16", flags=counted | (FLAG_TCT_WIDE if wide else 0))
+        assert step.info.n_tct_groups > 0 and (step.info.n_tct_wide > 0) == wide
         got = np_(step(q, kp, vp))
         off = np_(DecodeStep(f, P.plan_device(f, g, table, h_kv, 148, tct=False), h_kv * g, "bfloat16",
                              flags=FLAG_NO_TCT)(q, kp, vp))
