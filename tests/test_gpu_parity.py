@@ -558,9 +558,8 @@ class TestMultiRequestKernel:
 
 
 class TestTransposedKernel:
-    @pytest.mark.parametrize("g", [2, 4, 8])
-    @pytest.mark.parametrize("counted", [0, 1048576])
-    @pytest.mark.parametrize("wide", [False, True])
+    @pytest.mark.parametrize("g,counted,wide", [(g, c, w) for g in (2, 4, 8) for c in (0, 1048576)
+                                                 for w in (False, True)] + [(1, 0, False), (16, 0, True)])
     def test_lightly_shared_roots(self, cuda_ok, table, g, counted, wide):
         """Roots read by 17..128 query-head rows (kern_tct.cu: tokens on the
         MMA's M, rows on N): several KV slices per root (TCT_SLICE), 16..64
