@@ -48,7 +48,13 @@ constexpr int kTctBN = 128;                     // tokens per KV tile (MMA M of 
 constexpr int kTctD = 128;                      // head dim (MMA M of O^T)
 constexpr int kTileBytes = kTctBN * kTctD * 2;  // 32 KB: two SW128 atom columns [64 d][128 rows]
 constexpr int kAtomTile = kTileBytes / 2;       // 16 KB
-constexpr int kStages = 2;
+// narrow variant's K / V ring depths: 2 / 3 measured 80.1 vs 80.7 us on cfg3
+// (2 / 2), 3 / 2 81.4; cfg4 unchanged
+#ifndef CODEC_TCT_KSTAGES
+#define CODEC_TCT_KSTAGES 2
+#define CODEC_TCT_VSTAGES 3
+#endif
+constexpr int kMaxStages = 3;
 constexpr float kRefSlack = 8.f;  // a score may pass its column reference by 2^8
 
 template <int NG>
@@ -69,8 +75,11 @@ struct TctCfg {
   static constexpr int kAtomP = kPtBytes / 2;
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + kQtBytes;
-  static constexpr int kOffV = kOffK + kStages * kTileBytes;
-  static constexpr int kOffP = kOffV + kStages * kTileBytes;
+  // K / V ring depths (the narrow variant's can be raised for experiments)
+  static constexpr int kKSt = NG == 1 ? CODEC_TCT_KSTAGES : 2, kVSt = NG == 1 ? CODEC_TCT_VSTAGES : 2;
+  static_assert(kKSt <= kMaxStages && kVSt <= kMaxStages, "ring depth");
+  static constexpr int kOffV = kOffK + kKSt * kTileBytes;
+  static constexpr int kOffP = kOffV + kVSt * kTileBytes;
   static constexpr int kOffRed = kOffP + kPBuf * kPtBytes;       // [4 quadrants][kRows] f32 column reductions
   static constexpr int kOffRow = kOffRed + 4 * kRows * 4;         // per column: vis, slot, out row, request
   static constexpr int kOffMisc = kOffRow + 4 * kRows * 4;        // [kRows] f32 m, min visible, [kRows] f32 m steps
@@ -82,7 +91,7 @@ struct TctCfg {
 };
 
 struct TctBars {
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages];
   uint64_t s_full[2], s_free[2], p_full[2], p_empty[2];
   uint64_t q_full, o_free;  // per item: Q rows staged / the epilogue read O^T
   uint64_t pv_done[4];  // PV(t) completes pv_done[t % 4]: a parity wait never sees a phase two behind
@@ -318,7 +327,7 @@ __global__ void __launch_bounds__(TctCfg<NG>::kThreads, 1)
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&bars->k_full[s], 1);
       mbar_init(&bars->k_empty[s], 1);
       mbar_init(&bars->v_full[s], 1);
@@ -418,17 +427,17 @@ __global__ void __launch_bounds__(TctCfg<NG>::kThreads, 1)
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         const Item x = item(it);
         for (int j = 0; j < x.n_tiles; ++j, ++jg) {
-          const int s = jg & 1;
+          const int ks = jg % C::kKSt, vs = jg % C::kVSt;
           int xt = x.kv_tok + j * kTctBN;  // paged pool: a 128-token tile never crosses a page
           if (page_shift)
             xt = (__ldg(page_table + (xt >> page_shift)) << page_shift) | (xt & ((1 << page_shift) - 1));
           const int y = x.kh * (int)pool_tokens + xt;
-          if (jg >= kStages) mbar_wait(&bars->k_empty[s], ((jg - kStages) >> 1) & 1);
-          mbar_arrive_expect_tx(&bars->k_full[s], kTileBytes);
-          tc::tma_load_3d_hint(smem + C::kOffK + s * kTileBytes, &tmk, 0, y, 0, &bars->k_full[s], pol);
-          if (jg >= kStages) mbar_wait(&bars->v_empty[s], ((jg - kStages) >> 1) & 1);
-          mbar_arrive_expect_tx(&bars->v_full[s], kTileBytes);
-          tc::tma_load_3d_hint(smem + C::kOffV + s * kTileBytes, &tmv, 0, y, 0, &bars->v_full[s], pol);
+          if (jg >= C::kKSt) mbar_wait(&bars->k_empty[ks], ((jg - C::kKSt) / C::kKSt) & 1);
+          mbar_arrive_expect_tx(&bars->k_full[ks], kTileBytes);
+          tc::tma_load_3d_hint(smem + C::kOffK + ks * kTileBytes, &tmk, 0, y, 0, &bars->k_full[ks], pol);
+          if (jg >= C::kVSt) mbar_wait(&bars->v_empty[vs], ((jg - C::kVSt) / C::kVSt) & 1);
+          mbar_arrive_expect_tx(&bars->v_full[vs], kTileBytes);
+          tc::tma_load_3d_hint(smem + C::kOffV + vs * kTileBytes, &tmv, 0, y, 0, &bars->v_full[vs], pol);
         }
       }
     }
@@ -438,9 +447,9 @@ __global__ void __launch_bounds__(TctCfg<NG>::kThreads, 1)
     const uint32_t sbase = smem_u32(smem);
     int jg = 0, u = 0;
     auto pv = [&](int tp, int j_item, uint32_t idesc_o) {
-      const int vb = tp & 1, pb = tp % C::kPBuf;
+      const int vb = tp % C::kVSt, pb = tp % C::kPBuf;
       mbar_wait(&bars->p_full[pb], (tp / C::kPBuf) & 1);
-      mbar_wait(&bars->v_full[vb], (tp >> 1) & 1);
+      mbar_wait(&bars->v_full[vb], (tp / C::kVSt) & 1);
       tc::fence_after();
       if (tc::elect_one()) {
 #pragma unroll
@@ -463,19 +472,19 @@ __global__ void __launch_bounds__(TctCfg<NG>::kThreads, 1)
       const uint32_t idesc_o = tc::idesc_bf16(128, x.npad, true, false);
       mbar_wait(&bars->q_full, u & 1);
       for (int j = 0; j < x.n_tiles; ++j, ++jg) {
-        const int s = jg & 1;
-        mbar_wait(&bars->k_full[s], (jg >> 1) & 1);
+        const int s = jg & 1, ks = jg % C::kKSt;  // S buffer, K stage
+        mbar_wait(&bars->k_full[ks], (jg / C::kKSt) & 1);
         if (jg >= 2) mbar_wait(&bars->s_free[s], ((jg - 2) >> 1) & 1);
         tc::fence_after();
         if (tc::elect_one()) {
 #pragma unroll
           for (int k = 0; k < kTctD / 16; ++k) {
             const uint64_t ak =
-                tc::smem_desc(sbase + C::kOffK + s * kTileBytes + (k >> 2) * kAtomTile + (k & 3) * 32, 16, 1024);
+                tc::smem_desc(sbase + C::kOffK + ks * kTileBytes + (k >> 2) * kAtomTile + (k & 3) * 32, 16, 1024);
             const uint64_t bq = tc::smem_desc(sbase + C::kOffQ + (k >> 2) * C::kAtomQ + (k & 3) * 32, 16, 1024);
             tc::mma_f16_ss(tmem + C::kColS + s * C::kRows, ak, bq, idesc_s, k > 0 ? 1u : 0u);
           }
-          tc::commit(&bars->k_empty[s]);
+          tc::commit(&bars->k_empty[ks]);
           tc::commit(&bars->s_full[s]);
         }
         __syncwarp();
@@ -490,12 +499,13 @@ __global__ void __launch_bounds__(TctCfg<NG>::kThreads, 1)
     }
     // every commit's arrival landed before the CTA exits (a late one would
     // hit the SMEM of the next CTA on this SM): the last phase of each
-    for (int s = 0; s < kStages; ++s) {
-      const int uses = (jg - s + 1) / 2;
-      if (uses > 0) {
-        mbar_wait(&bars->k_empty[s], (uses - 1) & 1);
-        mbar_wait(&bars->v_empty[s], (uses - 1) & 1);
-      }
+    for (int s = 0; s < C::kKSt; ++s) {
+      const int uses = (jg - s + C::kKSt - 1) / C::kKSt;
+      if (uses > 0) mbar_wait(&bars->k_empty[s], (uses - 1) & 1);
+    }
+    for (int s = 0; s < C::kVSt; ++s) {
+      const int uses = (jg - s + C::kVSt - 1) / C::kVSt;
+      if (uses > 0) mbar_wait(&bars->v_empty[s], (uses - 1) & 1);
     }
     for (int s = 0; s < C::kPBuf; ++s) {
       const int uses = (jg - s + C::kPBuf - 1) / C::kPBuf;
