@@ -184,7 +184,8 @@ class DecodeStep:
         """Kernels one call launches (for the bench's gpu_launches)."""
         i = self.info
         return (int(bool(i.n_tc_groups)) + int(bool(i.n_gemv_groups)) + int(bool(i.n_gen_groups)) +
-                int(bool(i.n_multi_groups)) + int(bool(i.n_tct_groups)) + int(bool(i.n_merge)))
+                int(bool(i.n_multi_groups)) + int(bool(i.n_tct_groups - i.n_tct_wide)) + int(bool(i.n_tct_wide)) +
+                int(bool(i.n_merge)))
 
     def __call__(self, q, k_pool, v_pool, out=None, stream=None):
         """q [bs, h_q_local, d] and the pools [h_local, pool_tokens, d] in
