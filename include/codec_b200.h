@@ -311,6 +311,9 @@ typedef struct {
                                                           one per item unless CODEC_TCT_CTAS caps it */
   int32_t n_tct_wide;                                  /* the last n_tct_wide of those groups have 65..128 rows
                                                           (the wide variant; the others <= 64) */
+  int32_t merge_np;                                    /* the merge kernel's all-loads-in-flight width (4, 8, 16):
+                                                          holds 95 % of the entries */
+  int32_t reserved3;
   int64_t blob_len;                                    /* int32 elements */
   int64_t workspace_bytes;                             /* partial (o, m, l) storage */
 } codec_table_info;

@@ -78,7 +78,7 @@ class TableInfo(C.Structure):
                 ("off_merge_req", I32), ("off_merge_ptr", I32), ("off_merge_slot", I32),
                 ("h_local", I32), ("n_tc_blocks", I32), ("off_tc_block_ptr", I32),
                 ("max_merge", I32), ("n_merge_fused", I32), ("n_multi_groups", I32), ("off_multi", I32),
-                ("off_entry_of", I32), ("n_tct_groups", I32), ("tct_ctas", I32), ("n_tct_wide", I32),
+                ("off_entry_of", I32), ("n_tct_groups", I32), ("tct_ctas", I32), ("n_tct_wide", I32), ("merge_np", I32), ("reserved3", I32),
                 ("blob_len", I64), ("workspace_bytes", I64)]
 
 

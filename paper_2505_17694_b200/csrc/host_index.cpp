@@ -32,7 +32,7 @@ std::string& last_error() {
 using codec::fail;
 
 extern "C" const char* codec_last_error(void) { return codec::last_error().c_str(); }
-extern "C" int32_t codec_abi_version(void) { return 7; }
+extern "C" int32_t codec_abi_version(void) { return 8; }
 
 extern "C" int32_t codec_index_build(int32_t n_nodes, const int32_t* parent, const int64_t* length,
                                      int32_t bs, const int64_t* path_ptr, const int32_t* path_idx,

@@ -592,6 +592,28 @@ extern "C" int32_t codec_table_build(const codec_index* ix, const codec_dims* di
   codec_table_info& in = t->info;
   in.h_local = h_local;
   in.max_merge = max_merge;
+  // the merge kernel's all-loads-in-flight width: the smallest of 4 / 8 / 16
+  // that holds 95 % of the entries (the rest take its looped path) -- its
+  // registers grow with the width and cut the resident merge CTAs (cfg4:
+  // 37440 entries, 98 % with <= 4 partials, the largest 31)
+  {
+    std::vector<int32_t> cnt_np(17, 0);
+    int32_t n_e = 0;
+    for (size_t i = 0; i + 1 < merge_ptr.size() && (int32_t)i < n_merge_plain; ++i, ++n_e)
+      ++cnt_np[std::min(16, merge_ptr[i + 1] - merge_ptr[i])];
+    in.merge_np = 16;
+    const char* env = getenv("CODEC_MERGE_NP");  // (experiments)
+    if (env) in.merge_np = atoi(env);
+    for (int w : {4, 8}) {
+      if (env) break;
+      int32_t within = 0;
+      for (int k = 0; k <= w; ++k) within += cnt_np[k];
+      if (n_e == 0 || (int64_t)within * 100 >= (int64_t)n_e * 95) {
+        in.merge_np = w;
+        break;
+      }
+    }
+  }
   in.gemv_rows = gemv_rows;
   std::vector<int32_t>& blob = t->blob;
   auto emit_groups = [&](int kind, int32_t& count, int32_t& offset) {

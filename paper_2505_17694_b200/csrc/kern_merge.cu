@@ -108,10 +108,11 @@ __device__ __forceinline__ void merge128_row(const int32_t* __restrict__ table, 
                                              float* __restrict__ out, const PeerDev& pg);
 
 // kFastNp: partials per entry merged with all their loads in flight at once,
-// instantiated for 4 / 8 / 16 and chosen at launch as the smallest that
-// holds the table's largest entry (cfg2: <= 4, cfg3: 6-17) -- the registers
-// grow with it (16: 117 per thread, half the resident CTAs of 4, and a 5 us
-// slower cfg2 merge)
+// instantiated for 4 / 8 / 16 and chosen by the table (codec_table_info.
+// merge_np: the smallest that holds 95 % of the entries; cfg2 <= 4, cfg3
+// 10-13) -- the registers grow with it (16: 117 per thread, half the
+// resident CTAs of 4, and a 5 us slower cfg2 merge); larger entries take
+// merge128_row
 template <int kFastNp>
 __global__ void __launch_bounds__(128) merge128_kernel(const int32_t* __restrict__ table, int off_req, int off_ptr,
                                                        int off_slot, int n_merge, int g, int h_local,
@@ -366,7 +367,7 @@ int32_t launch_merge(int dtype, const int32_t* table, const codec_table_info& in
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    auto kern = in.max_merge <= 4 ? merge128_kernel<4> : in.max_merge <= 8 ? merge128_kernel<8> : merge128_kernel<16>;
+    auto kern = in.merge_np <= 4 ? merge128_kernel<4> : in.merge_np <= 8 ? merge128_kernel<8> : merge128_kernel<16>;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, table, in.off_merge_req, in.off_merge_ptr, in.off_merge_slot,
                                        in.n_merge, g, h_local, (const float*)part_o, (const float*)part_ml,
                                        (float*)out, tc_done, tc_ctas, cnt, pg);

@@ -121,7 +121,7 @@ class TestAbiSurface:
         for name in declared:
             assert hasattr(lib, name), name
         assert declared == set(_lib.exported_symbols())
-        assert lib.codec_abi_version() == 7
+        assert lib.codec_abi_version() == 8
 
     def test_library_is_sm100a(self):
         import subprocess
