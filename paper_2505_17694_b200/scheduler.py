@@ -154,7 +154,7 @@ SUFFIX_SLICE_MIN = 320  # shortest slice plan_device cuts a suffix / lightly sha
 # Partial-output pricing: a slice writes one partial (o[d], m, l) per
 # query-head row and the merge reads it back, 2 * (4 d + 8) bytes per row;
 # plan_device keeps that below this fraction of the slice's KV bytes
-PARTIAL_FRACTION = 0.026
+PARTIAL_FRACTION = float(os.environ.get("CODEC_PARTIAL_FRACTION", "0.026"))
 
 
 def partial_bytes(rows: int, d: int = 128) -> int:
@@ -169,7 +169,7 @@ def min_slice_tokens(g: int, d: int = 128, elem: int = 2) -> int:
     320 for the Llama-3-8B shape (g = 4), 640 for g = 8."""
     t = partial_bytes(g, d) / (PARTIAL_FRACTION * 2 * d * elem)
     return max(64, -(-int(math.ceil(t)) // 64) * 64)
-SUFFIX_WAVES = 2        # suffix-grid CTA waves (of 6 CTAs per SM) plan_device aims for
+SUFFIX_WAVES = float(os.environ.get("CODEC_SUFFIX_WAVES", "2"))  # suffix-grid CTA waves (of 6 CTAs per SM) plan_device aims for
 
 
 def concat_plans(plans) -> DivisionPlan:
