@@ -428,6 +428,23 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     from paper_2505_17694_b200.executor import FLAG_MERGE_ALL
     fused = world > 1 and args.gather == "fused"
+    gather_note = None
+    if fused:
+        # probe the peer mapping (CUDA IPC + peer access) once; every rank
+        # takes the NCCL gather if any rank cannot map its peers' buffers
+        err, probe = None, None
+        try:
+            probe = PL.PeerGather(1, 1, 1, dev)
+        except Exception as e:  # noqa: BLE001 -- reported in the bench line
+            err = f"{type(e).__name__}: {e}"
+        bad = torch.tensor([1 if err else 0], dtype=torch.int32, device="cpu" if one_gpu else dev)
+        dist.all_reduce(bad, op=dist.ReduceOp.MAX)
+        if not int(bad.item()):
+            probe.close()  # barriers inside: only when every rank holds a probe
+        else:  # a probe a rank did map stays allocated (16 bytes)
+            fused = False
+            gather_note = "fused peer-store gather unavailable on this box (" + (err or "another rank failed") + \
+                "); NCCL all-gather used"
     flags = args.flags | (FLAG_MERGE_ALL if fused else 0)
     ns = prepare(args.config, dev, rank, world, args.partition, flags, args.serial, args.blocks,
                  budgets=[args.budget] if args.budget else None, quick=args.quick)
@@ -758,6 +775,7 @@ def main():
                                        ("" if world == 1 else
                                         " + fused peer-store output gather (merge kernel -> NVLink)" if fused else
                                         (" + NCCL all-gather by request" if trees else " + NCCL all-gather"))),
+                       **({"gather_note": gather_note} if gather_note else {}),
                        "l2": "inputs larger than L2 (KV pool %.0f MB > 126 MB)" % (2 * kp.numel() * 2 / 1e6),
                        "planner": {"m_tc": m, "subtasks": len(plan.subtasks), "makespan_ms": plan.makespan_ms,
                                    "truncated": plan.search_truncated, "ms": ns.plan_ms},
