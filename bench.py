@@ -346,6 +346,26 @@ def prepare(config="cfg2", dev=None, rank=0, world=1, partition=None, flags=0, s
                            tune_ms=tune_ms, table=table, blocks=blocks, flags=flags)
 
 
+def library_reference(config):
+    """FlashInfer's B200 decode and cascade kernels on this workload, from
+    the committed same-box comparison (tools/library_baseline.py; not timed
+    in this run -- `source` names the capture), or None."""
+    p = ROOT / "profiles" / f"r02_library_baseline_{config}.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text().strip().splitlines()[-1])
+    except Exception:
+        return None
+    out = {"source": str(p.relative_to(ROOT)), "note": "separate run on one B200; both arms in >= 3-s windows",
+           "ours_us": d["ours"]["us"]}
+    for k in ("trtllm_gen_decode", "cascade"):
+        if "us" in d.get(k, {}):
+            out[k + "_us"] = d[k]["us"]
+            out[k + "_max_abs_vs_ours"] = d[k].get("max_abs_vs_ours")
+    return out
+
+
 def path_reference(forest, kp, vp, q, r):
     """Single-softmax attention of (local) request r over its root-to-leaf
     path (naive_attention, attention.py:164-187) in float64 on the device
@@ -795,6 +815,7 @@ def main():
                                     "reduction": traffic.bytes_baseline / total_bytes,
                                     "dram_bytes_ncu": ncu.get("step_dram_bytes")},
             "verified": check,
+            "library_reference": library_reference(args.config),
             "run_report": run_rep,
             "cpu_baseline": cpu,
             "e2e": e2e,
