@@ -396,6 +396,12 @@ CODEC_API int32_t codec_peer_wait(const int32_t* flags, int32_t n_peers, int32_t
 /* Symmetric buffers: a cudaMalloc allocation (zeroed) plus its 64-byte
  * CUDA IPC handle; open / close a peer's handle in this process. */
 CODEC_API int32_t codec_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64);
+/* Make `device` the calling thread's current device inside the library.
+ * The library links its own (static) CUDA runtime, so the host's
+ * cudaSetDevice / torch.cuda.set_device does not necessarily reach it;
+ * one process per GPU calls this once per thread before its first call
+ * (the Python layer does it in DecodeStep / PeerGather). */
+CODEC_API int32_t codec_bind_device(int32_t device);
 CODEC_API int32_t codec_ipc_free(void* dev_ptr);
 CODEC_API int32_t codec_ipc_open(const void* handle64, void** dev_ptr);
 CODEC_API int32_t codec_ipc_close(void* dev_ptr);

@@ -135,6 +135,7 @@ _SIGS = {
                                             C.POINTER(PeerGatherC)]),
     "codec_peer_wait": (I32, [P, I32, P, P]),
     "codec_ipc_alloc": (I32, [I64, C.POINTER(P), P]),
+    "codec_bind_device": (I32, [I32]),
     "codec_ipc_free": (I32, [P]),
     "codec_ipc_open": (I32, [P, C.POINTER(P)]),
     "codec_ipc_close": (I32, [P]),
@@ -158,6 +159,24 @@ def lib():
             fn.argtypes = args
         _lib = h
     return _lib
+
+
+_bound = __import__("threading").local()
+
+
+def bind_device(device) -> None:
+    """Make `device` (a torch.device / index) the library's current CUDA
+    device in this thread (codec_bind_device; the library's static CUDA
+    runtime does not see the host's cudaSetDevice). Cached per thread."""
+    import torch
+
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        return
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if getattr(_bound, "idx", None) != idx:
+        check(lib().codec_bind_device(int(idx)))
+        _bound.idx = idx
 
 
 def check(status: int):

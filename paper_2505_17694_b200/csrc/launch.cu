@@ -351,6 +351,12 @@ extern "C" int32_t codec_ipc_alloc(int64_t bytes, void** dev_ptr, void* handle64
   *dev_ptr = p;
   return CODEC_OK;
 }
+extern "C" int32_t codec_bind_device(int32_t device) {
+  int cur = -1;
+  if (device < 0) return fail(CODEC_ERR_VALUE, "bad device");
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == device) return CODEC_OK;
+  return cuda_status(cudaSetDevice(device), "cudaSetDevice");
+}
 extern "C" int32_t codec_ipc_free(void* dev_ptr) { return cuda_status(cudaFree(dev_ptr), "ipc free"); }
 extern "C" int32_t codec_ipc_open(const void* handle64, void** dev_ptr) {
   if (!handle64 || !dev_ptr) return fail(CODEC_ERR_VALUE, "bad ipc open arguments");

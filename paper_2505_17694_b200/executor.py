@@ -116,6 +116,8 @@ class DecodeStep:
         self.g = self.h_q // self.h_kv
         self.tdtype = torch_dtype(dtype)
         self.device = torch.device(device)
+        if torch.cuda.is_available():
+            _lib.bind_device(self.device)
         sm = torch.cuda.get_device_properties(self.device).multi_processor_count if torch.cuda.is_available() else 148
         self.plan, self.flags, self.tc_sm_budget = plan, int(flags), int(tc_sm_budget)
         self.page_size, self.page_table = int(page_size), page_table
@@ -203,6 +205,7 @@ class DecodeStep:
         else:
             self._check("out", out, (bs, self.hq_local, self.d), self.out_dtype)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.bind_device(self.device)
         _lib.check(_lib.lib().codec_decode_attention_ex(
             C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
             C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(out.data_ptr()),
@@ -232,6 +235,7 @@ class DecodeStep:
             self._check("row_map", row_map, (bs,), torch.int32)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         pg = peers.struct(self.head_begin * self.g if head0 is None else int(head0), row_map, buf)
+        _lib.bind_device(self.device)
         _lib.check(_lib.lib().codec_decode_attention_gather(
             C.byref(self.dims), C.byref(self.info), C.c_void_p(self.table.data_ptr()), C.c_void_p(q.data_ptr()),
             C.c_void_p(k_pool.data_ptr()), C.c_void_p(v_pool.data_ptr()), C.c_void_p(self.workspace.data_ptr()),

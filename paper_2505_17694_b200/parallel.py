@@ -252,6 +252,7 @@ class PeerGather:
 
         L = _lib.lib()
         self.device = torch.device(device)
+        _lib.bind_device(self.device)  # allocations and peer mappings on this rank's GPU
         self.rows, self.hq_global, self.d = int(rows), int(hq_global), int(d)
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -314,6 +315,7 @@ class PeerGather:
         from . import _lib
 
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.bind_device(self.device)
         _lib.check(_lib.lib().codec_peer_wait(C.c_void_p(self._flags_local), self.world,
                                               C.c_void_p(self._expected.data_ptr()), C.c_void_p(st.cuda_stream)))
 
