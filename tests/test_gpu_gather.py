@@ -174,3 +174,20 @@ def test_bench_two_ranks_one_gpu():
     assert line["n_gpus"] == 2 and "fused peer-store" in line["config"]["parallelism"]
     v = line["verified"]
     assert v["ok"] and v["gather_ok"] and v["all_ranks_ok"], v
+
+
+def test_bind_device():
+    """codec_bind_device: binding this process's GPU succeeds (and is
+    cached per thread); a device index the box does not have raises the
+    library's CUDA error instead of silently launching elsewhere."""
+    import torch
+
+    from paper_2505_17694_b200 import _lib
+
+    _lib.bind_device(torch.device("cuda", 0))
+    assert _lib.lib().codec_bind_device(0) == 0
+    n = torch.cuda.device_count()
+    with pytest.raises(Exception) as ei:
+        _lib.check(_lib.lib().codec_bind_device(n))
+    assert "cudaSetDevice" in str(ei.value)
+    _lib.check(_lib.lib().codec_bind_device(0))  # back on cuda:0 for the tests after this one
