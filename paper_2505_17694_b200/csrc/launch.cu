@@ -355,7 +355,9 @@ extern "C" int32_t codec_bind_device(int32_t device) {
   int cur = -1;
   if (device < 0) return fail(CODEC_ERR_VALUE, "bad device");
   if (cudaGetDevice(&cur) == cudaSuccess && cur == device) return CODEC_OK;
-  return cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  const cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) cudaGetLastError();  // not sticky: later launch checks must not see it
+  return cuda_status(e, "cudaSetDevice");
 }
 extern "C" int32_t codec_ipc_free(void* dev_ptr) { return cuda_status(cudaFree(dev_ptr), "ipc free"); }
 extern "C" int32_t codec_ipc_open(const void* handle64, void** dev_ptr) {
