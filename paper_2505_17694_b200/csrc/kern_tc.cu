@@ -890,6 +890,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             }
           }
           const int wq = warp & 3;
+#ifdef CODEC_TC_EPI_SPLIT
+          long long t_stage = 0, t_store = 0, t_a = clock64();
+#endif
 #pragma unroll 1
           for (int pass = 0; pass < 2; ++pass) {
             if ((quad >> 1) == pass) {
@@ -902,6 +905,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
               rdst[x] = reinterpret_cast<long long>(dst);
             }
             named_sync(12, 128);
+#ifdef CODEC_TC_EPI_SPLIT
+            { const long long tb = clock64(); t_stage += tb - t_a; t_a = tb; }
+#endif
 #pragma unroll 4
             for (int i = 0; i < 16; ++i) {
               const int x = wq * 16 + i;
@@ -915,7 +921,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
               }
             }
             named_sync(12, 128);
+#ifdef CODEC_TC_EPI_SPLIT
+            { const long long tb = clock64(); t_store += tb - t_a; t_a = tb; }
+#endif
           }
+#ifdef CODEC_TC_EPI_SPLIT
+          if (ctalog && tid == grp * 128) {  // [0] staging writes, [3] global stores (debug build only)
+            ctalog[4 * (2048 + blockIdx.x) + 0] += t_stage;
+            ctalog[4 * (2048 + blockIdx.x) + 3] += t_store;
+          }
+#endif
           // readiness count of the merge entry of (req, kv head): every
           // thread's stores of the group fenced, then one arrival per row
           if (cnt) {
@@ -942,10 +957,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       }
       if (quad == 0) PROG(1 + grp, t, 8);
     }
+#ifndef CODEC_TC_EPI_SPLIT
     if (ctalog && tid == 0) {
       ctalog[4 * (2048 + blockIdx.x)] = global_ns();
       ctalog[4 * (2048 + blockIdx.x) + 3] = t_start;
     }
+#endif
   }
   // Drain (both CTAs, once every warp of this CTA is done): tcgen05.commit
   // arrivals land asynchronously, after the MMAs they track. Those nobody

@@ -33,3 +33,6 @@ for name, extra in (("full step", 0), ("TC alone", 8 | 32 | 64)):
     u = np.repeat(units, 2)[:len(a)]
     print(f"{config} budget {budget} {name}: per epilogue: unit end -> O read {np.median(a[:, 1] / u):.0f} clk, "
           f"O read -> stores done {np.median(a[:, 2] / u):.0f} clk (medians over {len(a)} CTAs)", flush=True)
+    if os.environ.get("EPI_SPLIT"):  # library built with -DCODEC_TC_EPI_TIMING -DCODEC_TC_EPI_SPLIT
+        print(f"    of which staging writes {np.median(a[:, 0] / u):.0f} clk, global stores {np.median(a[:, 3] / u):.0f} clk",
+              flush=True)
