@@ -108,6 +108,12 @@ constexpr float kRescaleLog2 = 8.f;
 #ifndef CODEC_TC_POLY_PAIRS
 #define CODEC_TC_POLY_PAIRS 0
 #endif
+// epilogue row stores as 256-bit STG (two rows per warp instruction): the
+// per-unit global stores 4424 -> 2916 clk, K2 alone 139.9 -> 138.6 us on
+// cfg2 (tools/epi_timing.py, tools/ab_rounds.py); =0 restores STG.128
+#ifndef CODEC_TC_STG256
+#define CODEC_TC_STG256 1
+#endif
 constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 
 struct TcBars {
@@ -908,6 +914,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #ifdef CODEC_TC_EPI_SPLIT
             { const long long tb = clock64(); t_stage += tb - t_a; t_a = tb; }
 #endif
+#if CODEC_TC_STG256
+            // 256-bit stores (STG.256): one instruction writes two staging
+            // rows (a half-warp per row), half the store instructions
+#pragma unroll 4
+            for (int i = 0; i < 8; ++i) {
+              const int x = wq * 16 + 2 * i + (lane >> 4), cp = lane & 15;
+              float* d = reinterpret_cast<float*>(rdst[x]);
+              if (d) {
+                const float4 a = stg[x * 32 + ((2 * cp) ^ (x & 31))];
+                const float4 b = stg[x * 32 + ((2 * cp + 1) ^ (x & 31))];
+                asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d + 8 * cp),
+                             "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                             : "memory");
+              }
+            }
+#else
 #pragma unroll 4
             for (int i = 0; i < 16; ++i) {
               const int x = wq * 16 + i;
@@ -920,6 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
                              : "memory");
               }
             }
+#endif
             named_sync(12, 128);
 #ifdef CODEC_TC_EPI_SPLIT
             { const long long tb = clock64(); t_store += tb - t_a; t_a = tb; }
