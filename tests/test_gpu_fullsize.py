@@ -223,7 +223,7 @@ class TestShardedSteps:
 
 
 # ------------------------------------------------------------ score extremes
-def _extreme_spec(seed, mode, n_req=64):
+def _extreme_spec(seed, mode, n_req=64, h_q=32):
     """two-level forest (root shared by 64 requests -> tensor-core kernel;
     by 12 -> the transposed tensor-core kernel; 300-token suffixes -> suffix
     kernel) with bf16-exact adversarial keys.
@@ -232,7 +232,7 @@ def _extreme_spec(seed, mode, n_req=64):
     'peaked': queries scaled by 800 (scores ~ N(0, 6^2), a softmax
     dominated by a few tokens of every slice)."""
     rng = np.random.default_rng(seed)
-    spec = W.two_level(3000, 300, n_req, h_q=32, h_kv=8, d=128, seed=seed)
+    spec = W.two_level(3000, 300, n_req, h_q=h_q, h_kv=8, d=128, seed=seed)
     if mode == "extreme":
         spec.queries = np.ones_like(spec.queries)
         for n in range(1, spec.n_nodes):
@@ -270,6 +270,26 @@ class TestScoreExtremes:
         out = step(qb.queries.cuda(), kp, vp).double().cpu().numpy()
         ref = oracle_requests(f, kp, vp, qb.queries.cuda(), list(range(f.bs)))
         close(out, ref, f"{mode} flags={flags}")
+
+    @pytest.mark.parametrize("mode", ["extreme", "peaked"])
+    def test_bf16_kernels_g8(self, table, mode):
+        """The same adversarial scores at the Llama-3-70B head ratio (64 q /
+        8 kv heads, g = 8, cfg5's shape): 32 requests x 8 heads fill one
+        256-row pair tile of the shared root, the suffixes run the mma.sync
+        kernel with all 8 of its N columns live."""
+        import torch
+        spec = _extreme_spec(37, mode, 32, h_q=64)
+        to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16)
+        specs = [(p, to(k), to(v)) for p, k, v, _ in spec.node_specs()]
+        qb = P.QueryBatch(to(spec.queries), spec.h_kv)
+        f = P.build_forest(specs, spec.paths, qb)
+        plan = P.plan_device(f, 8, table, 8, 148)
+        kp, vp = f.device_pool(torch.bfloat16)
+        step = DecodeStep(f, plan, 64, "bfloat16")
+        assert step.info.n_tc_groups > 0 and step.info.n_gemv_groups > 0
+        out = step(qb.queries.cuda(), kp, vp).double().cpu().numpy()
+        ref = oracle_requests(f, kp, vp, qb.queries.cuda(), list(range(f.bs)))
+        close(out, ref, f"g8 {mode}")
 
 
 # ------------------------------------------------------------ other shapes

@@ -136,3 +136,42 @@ class TestPaged:
         want = OA.naive_attention(up(q), fd)
         err = np.abs(got.double().cpu().numpy() - want)
         assert err.max() <= 2e-3 and err.max() / np.abs(want).max() <= 1e-2, (page, shape, float(err.max()))
+
+    @pytest.mark.parametrize("page", [128, 256])
+    def test_paged_head_shard(self, table, page):
+        """A kv-head shard (heads [2, 6) of 8) over a paged
+        pool: the shard's slab of the physical pages with the shared page
+        table equals the contiguous shard step bit for bit, and its q heads
+        [8, 24) match the float64 oracle of the whole forest."""
+        import torch
+        from paper_2505_17694_b200.executor import DecodeStep
+        from paper_2505_17694_b200.paging import paged_pools
+        spec = W.two_level(3000, 260, 24, h_q=32, h_kv=8, d=128, seed=5, tensors=False)
+        f = P.forest_from_pool(spec.parent[1:], spec.length[1:], spec.paths, 8, 128)
+        gen = torch.Generator().manual_seed(page + 1)
+        T = f.total_tokens
+        kp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        vp = (torch.randn((8, T, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        q = (torch.randn((f.bs, 32, 128), generator=gen) * 0.088).to(torch.bfloat16).cuda()
+        kx, vx, pt = paged_pools(f, kp, vp, page, n_phys_pages=page_layout(f, page)[1] + 3, generator=gen)
+        h0, h1, g = 2, 6, 4
+        plan = P.plan_device(f, g, table, h1 - h0, 148, page_size=page)
+        qs = q[:, h0 * g:h1 * g].contiguous()
+        ref = DecodeStep(f, plan, 32, "bfloat16", head_begin=h0, head_end=h1)(
+            qs, kp[h0:h1].contiguous(), vp[h0:h1].contiguous())
+        got = DecodeStep(f, plan, 32, "bfloat16", head_begin=h0, head_end=h1, page_size=page, page_table=pt,
+                         pool_tokens=kx.shape[1])(qs, kx[h0:h1].contiguous(), vx[h0:h1].contiguous())
+        torch.cuda.synchronize()
+        assert torch.isfinite(ref).all()
+        assert torch.equal(ref, got), (page, float((ref - got).abs().max()))
+        from oracle import attention as OA
+        up = lambda t: t.double().cpu().numpy()
+        kp_h, vp_h = up(kp), up(vp)
+        z = np.zeros((0, 8, 128))
+        node_k = [z] + [kp_h[:, f.token_offset[n]:f.token_offset[n] + f.nodes[n].len].transpose(1, 0, 2)
+                        for n in range(1, len(f.nodes))]
+        node_v = [z] + [vp_h[:, f.token_offset[n]:f.token_offset[n] + f.nodes[n].len].transpose(1, 0, 2)
+                        for n in range(1, len(f.nodes))]
+        want = OA.naive_attention(up(q), OA.ForestData(spec.parent, node_k, node_v, spec.paths))[:, h0 * g:h1 * g]
+        err = np.abs(got.double().cpu().numpy() - want)
+        assert err.max() <= 2e-3 and err.max() / np.abs(want).max() <= 1e-2, (page, float(err.max()))
