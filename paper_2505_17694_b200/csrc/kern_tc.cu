@@ -114,6 +114,13 @@ constexpr float kRescaleLog2 = 8.f;
 #ifndef CODEC_TC_STG256
 #define CODEC_TC_STG256 1
 #endif
+// epilogue without staging: each thread stores its own row as 16 full
+// 32-byte sectors (STG.256), all four warps at once -- stores 2430 clk per
+// unit boundary vs 808 + 2921 staged (tools/epi_timing.py), K2 alone 138.7
+// -> 137.5 us on cfg2 (tools/ab_rounds.py); =0 restores the staged path
+#ifndef CODEC_TC_DIRECT_STORE
+#define CODEC_TC_DIRECT_STORE 1
+#endif
 constexpr int kGroupWarpArrivals = 2 * 4;  // one group's 4 warps in both CTAs
 
 struct TcBars {
@@ -899,6 +906,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 #ifdef CODEC_TC_EPI_SPLIT
           long long t_stage = 0, t_store = 0, t_a = clock64();
 #endif
+#if CODEC_TC_DIRECT_STORE
+          // no staging: every thread writes its own row as 16 full 32-byte
+          // sectors (STG.256), all four warps at once
+          (void)stg;
+          (void)rdst;
+          (void)wq;
+          if (dst) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + 8 * c),
+                           "f"(__uint_as_float(o[8 * c]) * inv), "f"(__uint_as_float(o[8 * c + 1]) * inv),
+                           "f"(__uint_as_float(o[8 * c + 2]) * inv), "f"(__uint_as_float(o[8 * c + 3]) * inv),
+                           "f"(__uint_as_float(o[8 * c + 4]) * inv), "f"(__uint_as_float(o[8 * c + 5]) * inv),
+                           "f"(__uint_as_float(o[8 * c + 6]) * inv), "f"(__uint_as_float(o[8 * c + 7]) * inv)
+                           : "memory");
+          }
+#ifdef CODEC_TC_EPI_SPLIT
+          t_store = clock64() - t_a;
+#endif
+#else
 #pragma unroll 1
           for (int pass = 0; pass < 2; ++pass) {
             if ((quad >> 1) == pass) {
@@ -948,6 +975,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             { const long long tb = clock64(); t_store += tb - t_a; t_a = tb; }
 #endif
           }
+#endif  // CODEC_TC_DIRECT_STORE
 #ifdef CODEC_TC_EPI_SPLIT
           if (ctalog && tid == grp * 128) {  // [0] staging writes, [3] global stores (debug build only)
             ctalog[4 * (2048 + blockIdx.x) + 0] += t_stage;
